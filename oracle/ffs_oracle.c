@@ -1,0 +1,938 @@
+/*
+ * ffs_oracle.c -- CPU ORACLE for arXiv 1903.10741.  See ffs_oracle.h.
+ *
+ * TEST INFRASTRUCTURE, NOT PRODUCT CODE: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference leg may load it.  It shares
+ * nothing with the CUDA path.  Deliberately plain: no blocking, no fusion,
+ * no incremental data structures -- each function follows the paper's
+ * statement in its order and notation so that it can be checked by eye.
+ *
+ * Readings of the paper used here are numbered R1..R26 in DESIGN.md
+ * ("Readings") and cited inline.
+ */
+#include "ffs_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define Z_COMPLETED (-2)   /* the paper's "C" in Z(k) */
+#define Z_UNRANKED  (-3)
+
+struct or_ctx {
+  or_instance in;
+  int32_t *Pbuf, *Qbuf, *Rbuf, *Dbuf;
+  int32_t rs;
+  int32_t NJ, cells, K;
+  int32_t *state;      /* [cells] OR_PENDING / OR_RUNNING / OR_COMPLETED */
+  int32_t *fassign;    /* [cells] frozen machine (plan), -1 when pending  */
+  int32_t *fstart;     /* [cells] frozen start (plan), -1 when pending    */
+  int32_t *gene_cell;  /* [K] pending cells in row-major order            */
+  int32_t *cell_gene;  /* [cells] gene index or -1                         */
+};
+
+/* ------------------------------------------------------------------ */
+/* small helpers                                                       */
+/* ------------------------------------------------------------------ */
+static int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+static int32_t Pjsm(const or_instance *in, int j, int s, int m) {
+  return in->P[((int64_t)j * in->g + s) * in->o + m];
+}
+static int32_t Qjsm(const or_instance *in, int j, int s, int m) {
+  return in->Q[((int64_t)j * in->g + s) * in->o + m];
+}
+
+/* one committed processing interval [start, end) drawing power q (Eq. (9)) */
+typedef struct { int64_t start, end; int64_t q; } interval;
+
+/* Q_t of Eq. (8) at instant t: sum of q over intervals with start <= t < end */
+static int64_t level_at(const interval *iv, int n, int64_t t) {
+  int64_t L = 0;
+  for (int i = 0; i < n; ++i)
+    if (iv[i].start <= t && t < iv[i].end) L += iv[i].q;
+  return L;
+}
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al., Random123)                            */
+/* ------------------------------------------------------------------ */
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { k0 += W0; k1 += W1; }
+    uint64_t p0 = (uint64_t)M0 * c0;
+    uint64_t p1 = (uint64_t)M1 * c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* draw word `word` of block `block` for purpose/individual/generation/island
+ * (ctr = (purpose<<24 | block, individual, k, island)). */
+static uint32_t draw(uint64_t seed, uint32_t purpose, uint32_t block, uint32_t word,
+                     uint32_t individual, uint32_t k, uint32_t island) {
+  uint32_t ctr[4] = {(purpose << 24) | block, individual, k, island};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t out[4];
+  or_philox4x32_10(ctr, key, out);
+  return out[word];
+}
+/* floor(u * n / 2^32) */
+static uint32_t bounded(uint32_t u, uint32_t n) { return (uint32_t)(((uint64_t)u * n) >> 32); }
+
+/* ------------------------------------------------------------------ */
+/* Instance / plan checks                                              */
+/* ------------------------------------------------------------------ */
+static int check_instance(const or_instance *in) {
+  if (!in || in->n < 0 || in->n_prime < 0 || in->n + in->n_prime < 1 || in->g < 1 || in->o < 1)
+    return OR_ERR_ARG;
+  if (!in->P || !in->Q || !in->R || !in->D || in->wt < 0) return OR_ERR_ARG;
+  int NJ = in->n + in->n_prime;
+  for (int j = 0; j < NJ; ++j) {
+    if (in->D[j] < in->R[j] || in->R[j] < 0) return OR_ERR_ARG;
+    for (int s = 0; s < in->g; ++s)
+      for (int m = 0; m < in->o; ++m) {
+        if (Pjsm(in, j, s, m) <= 0 || Qjsm(in, j, s, m) < 0) return OR_ERR_ARG;
+        if (Qjsm(in, j, s, m) > in->q_max) return OR_ERR_INFEASIBLE;
+      }
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Freeze at RS (Algorithm 1 frozen branch)                 */
+/* ------------------------------------------------------------------ */
+int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
+                  const int32_t *orig_start, or_ctx **out) {
+  int st = check_instance(inst);
+  if (st != OR_OK) return st;
+  if (rs < 0 || !out) return OR_ERR_ARG;
+  int NJ = inst->n + inst->n_prime, g = inst->g, o = inst->o;
+  int cells = NJ * g;
+  or_ctx *c = (or_ctx *)calloc(1, sizeof(or_ctx));
+  c->in = *inst;
+  size_t tab = (size_t)cells * o;
+  c->Pbuf = (int32_t *)malloc(tab * sizeof(int32_t));
+  c->Qbuf = (int32_t *)malloc(tab * sizeof(int32_t));
+  c->Rbuf = (int32_t *)malloc(NJ * sizeof(int32_t));
+  c->Dbuf = (int32_t *)malloc(NJ * sizeof(int32_t));
+  memcpy(c->Pbuf, inst->P, tab * sizeof(int32_t));
+  memcpy(c->Qbuf, inst->Q, tab * sizeof(int32_t));
+  memcpy(c->Rbuf, inst->R, NJ * sizeof(int32_t));
+  memcpy(c->Dbuf, inst->D, NJ * sizeof(int32_t));
+  c->in.P = c->Pbuf; c->in.Q = c->Qbuf; c->in.R = c->Rbuf; c->in.D = c->Dbuf;
+  c->rs = rs; c->NJ = NJ; c->cells = cells;
+  c->state = (int32_t *)malloc(cells * sizeof(int32_t));
+  c->fassign = (int32_t *)malloc(cells * sizeof(int32_t));
+  c->fstart = (int32_t *)malloc(cells * sizeof(int32_t));
+  c->cell_gene = (int32_t *)malloc(cells * sizeof(int32_t));
+  c->gene_cell = (int32_t *)malloc((cells + 1) * sizeof(int32_t));
+
+  const or_instance *in = &c->in;
+  if (orig_assign && orig_start) {
+    /* the original plan must itself satisfy Eqs. (4)-(7) over J */
+    for (int j = 0; j < inst->n; ++j)
+      for (int s = 0; s < g; ++s) {
+        int32_t m = orig_assign[j * g + s];
+        if (m < 0 || m >= o || orig_start[j * g + s] < 0) { or_ctx_destroy(c); return OR_ERR_SCHEDULE; }
+      }
+    for (int j = 0; j < inst->n; ++j) {
+      if (orig_start[j * g] < in->R[j]) { or_ctx_destroy(c); return OR_ERR_SCHEDULE; } /* Eq. (4) */
+      for (int s = 1; s < g; ++s) {
+        int64_t prevC = (int64_t)orig_start[j * g + s - 1] + Pjsm(in, j, s - 1, orig_assign[j * g + s - 1]);
+        if (orig_start[j * g + s] < prevC) { or_ctx_destroy(c); return OR_ERR_SCHEDULE; } /* Eq. (5) */
+      }
+    }
+    for (int a = 0; a < inst->n * g; ++a)      /* Eq. (6), read symmetrically (R-M7) */
+      for (int b = a + 1; b < inst->n * g; ++b) {
+        int ja = a / g, sa = a % g, jb = b / g, sb = b % g;
+        if (sa != sb || orig_assign[a] != orig_assign[b]) continue;
+        int64_t ea = (int64_t)orig_start[a] + Pjsm(in, ja, sa, orig_assign[a]);
+        int64_t eb = (int64_t)orig_start[b] + Pjsm(in, jb, sb, orig_assign[b]);
+        if (orig_start[a] < eb && orig_start[b] < ea) { or_ctx_destroy(c); return OR_ERR_SCHEDULE; }
+      }
+    for (int a = 0; a < inst->n * g; ++a) {    /* Eq. (7) at every start instant */
+      int64_t t = orig_start[a], L = 0;
+      for (int b = 0; b < inst->n * g; ++b) {
+        int jb = b / g, sb = b % g;
+        int64_t e = (int64_t)orig_start[b] + Pjsm(in, jb, sb, orig_assign[b]);
+        if (orig_start[b] <= t && t < e) L += Qjsm(in, jb, sb, orig_assign[b]);
+      }
+      if (L > in->q_max) { or_ctx_destroy(c); return OR_ERR_SCHEDULE; }
+    }
+  }
+
+  /* Case rules and Algorithm 1's frozen branch:
+   * RUNNING iff S_js < RS < S_js + P (z = 0); COMPLETED iff it finished by
+   * RS (z = C); everything else, and every op of a new job, is PENDING.
+   * Boundaries per R7: C == RS -> COMPLETED, S == RS -> PENDING. */
+  int64_t running_power = 0;
+  for (int j = 0; j < NJ; ++j)
+    for (int s = 0; s < g; ++s) {
+      int cell = j * g + s;
+      c->state[cell] = OR_PENDING;
+      c->fassign[cell] = -1;
+      c->fstart[cell] = -1;
+      if (j < inst->n && orig_assign && orig_start) {
+        int32_t m = orig_assign[cell];
+        int64_t S = orig_start[cell];
+        int64_t C = S + Pjsm(in, j, s, m);
+        if (S < rs && rs < C) {
+          c->state[cell] = OR_RUNNING;
+          running_power += Qjsm(in, j, s, m);
+        } else if (C <= rs) {
+          c->state[cell] = OR_COMPLETED;
+        }
+        if (c->state[cell] != OR_PENDING) { c->fassign[cell] = m; c->fstart[cell] = (int32_t)S; }
+      }
+    }
+  if (running_power > in->q_max) { or_ctx_destroy(c); return OR_ERR_INFEASIBLE; }
+  /* canonical gene order: pending cells row-major (job-major, stage-minor) */
+  int K = 0;
+  for (int cell = 0; cell < cells; ++cell) {
+    if (c->state[cell] == OR_PENDING) { c->cell_gene[cell] = K; c->gene_cell[K++] = cell; }
+    else c->cell_gene[cell] = -1;
+  }
+  c->K = K;
+  *out = c;
+  return OR_OK;
+}
+
+void or_ctx_destroy(or_ctx *c) {
+  if (!c) return;
+  free(c->Pbuf); free(c->Qbuf); free(c->Rbuf); free(c->Dbuf);
+  free(c->state); free(c->fassign); free(c->fstart); free(c->cell_gene); free(c->gene_cell);
+  free(c);
+}
+int32_t or_ctx_K(const or_ctx *c) { return c->K; }
+int32_t or_ctx_cells(const or_ctx *c) { return c->cells; }
+void or_ctx_states(const or_ctx *c, int32_t *state) { memcpy(state, c->state, c->cells * sizeof(int32_t)); }
+void or_ctx_pending_cells(const or_ctx *c, int32_t *cg) { memcpy(cg, c->gene_cell, c->K * sizeof(int32_t)); }
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 1                                             */
+/* ------------------------------------------------------------------ */
+/* Greedy reading (R1): the stage rule (s < s'' => earlier) is kept
+ * absolutely by only ranking ops whose predecessor is frozen or already
+ * ranked; among those eligible ops the y rule (larger y => earlier) picks
+ * the next rank.  y is unique, so there are no ties. */
+int or_order(const or_ctx *c, const int32_t *Y, int32_t *Z) {
+  int g = c->in.g;
+  for (int cell = 0; cell < c->cells; ++cell) {
+    if (c->state[cell] == OR_RUNNING) Z[cell] = 0;
+    else if (c->state[cell] == OR_COMPLETED) Z[cell] = Z_COMPLETED;
+    else Z[cell] = Z_UNRANKED;
+  }
+  for (int rank = 1; rank <= c->K; ++rank) {
+    int best = -1;
+    for (int cell = 0; cell < c->cells; ++cell) {
+      if (c->state[cell] != OR_PENDING || Z[cell] != Z_UNRANKED) continue;
+      int s = cell % g;
+      int pred_ok = (s == 0) || c->state[cell - 1] != OR_PENDING || Z[cell - 1] != Z_UNRANKED;
+      if (!pred_ok) continue;
+      if (best < 0 || Y[cell] > Y[best]) best = cell;
+    }
+    if (best < 0) return OR_ERR_ARG;
+    Z[best] = rank;
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 2: the decoding rule                          */
+/* ------------------------------------------------------------------ */
+int or_decode(const or_ctx *c, const int32_t *X, const int32_t *Y, const int32_t *Zin,
+              int32_t *assign_out, int32_t *start_out, int64_t *sumT_out,
+              int64_t *cmax_out, int64_t *obj_out, or_counters *cnt) {
+  const or_instance *in = &c->in;
+  int g = in->g, o = in->o, cells = c->cells, K = c->K;
+  int64_t rs = c->rs;
+  int32_t *Z = (int32_t *)malloc(cells * sizeof(int32_t));
+  int32_t *byrank = (int32_t *)malloc((K + 1) * sizeof(int32_t));
+  int32_t *asg = (int32_t *)malloc(cells * sizeof(int32_t));
+  int64_t *S = (int64_t *)malloc(cells * sizeof(int64_t));
+  int64_t *C = (int64_t *)malloc(cells * sizeof(int64_t));
+  int64_t *mfree = (int64_t *)malloc((size_t)g * o * sizeof(int64_t));
+  interval *iv = (interval *)malloc((cells + 1) * sizeof(interval));
+  int64_t *cand = (int64_t *)malloc((cells + 2) * sizeof(int64_t));
+  int niv = 0, st = OR_OK;
+
+  if (Zin) memcpy(Z, Zin, cells * sizeof(int32_t));
+  else if ((st = or_order(c, Y, Z)) != OR_OK) goto done;
+  for (int r = 0; r <= K; ++r) byrank[r] = -1;
+  for (int cell = 0; cell < cells; ++cell)
+    if (c->state[cell] == OR_PENDING) {
+      if (Z[cell] < 1 || Z[cell] > K || byrank[Z[cell]] >= 0) { st = OR_ERR_ARG; goto done; }
+      byrank[Z[cell]] = cell;
+    }
+
+  /* frozen operations keep their plan; RUNNING ones occupy their machine and
+   * draw power until completion (R3); COMPLETED ones are over by RS. */
+  for (int s = 0; s < g; ++s)
+    for (int m = 0; m < o; ++m) mfree[s * o + m] = rs;
+  for (int cell = 0; cell < cells; ++cell) {
+    asg[cell] = -1; S[cell] = -1; C[cell] = -1;
+    if (c->state[cell] == OR_PENDING) continue;
+    int j = cell / g, s = cell % g, m = c->fassign[cell];
+    asg[cell] = m;
+    S[cell] = c->fstart[cell];
+    C[cell] = S[cell] + Pjsm(in, j, s, m);
+    if (c->state[cell] == OR_RUNNING) {
+      iv[niv].start = S[cell]; iv[niv].end = C[cell]; iv[niv].q = Qjsm(in, j, s, m); ++niv;
+      mfree[s * o + m] = max64(mfree[s * o + m], C[cell]);
+    }
+  }
+
+  for (int r = 1; r <= K; ++r) {
+    int cell = byrank[r];
+    int j = cell / g, s = cell % g, m = X[cell];
+    if (m < 0 || m >= o) { st = OR_ERR_ARG; goto done; }
+    int64_t p = Pjsm(in, j, s, m), q = Qjsm(in, j, s, m);
+    /* earliest start allowed by Eq. (10) RS <= S (R8), Eq. (4) release /
+     * Eq. (5) predecessor completion, and the machine's previous operation
+     * in Z order (append-only R6) */
+    int64_t ready = (s == 0) ? (int64_t)in->R[j] : C[cell - 1];
+    int64_t t = max64(max64(rs, ready), mfree[s * o + m]);
+    if (cnt) cnt->dispatches++;
+    for (;;) {
+      /* if Q_max >= Q_t + Q_jsm over the whole processing interval (R2):
+       * level can only rise at an interval start, so test t and every start
+       * inside (t, t+p) in ascending order */
+      int nc = 0;
+      cand[nc++] = t;
+      for (int i = 0; i < niv; ++i)
+        if (iv[i].start > t && iv[i].start < t + p) cand[nc++] = iv[i].start;
+      for (int a = 1; a < nc; ++a)            /* insertion sort */
+        for (int b = a; b > 1 && cand[b - 1] > cand[b]; --b) {
+          int64_t tmp = cand[b]; cand[b] = cand[b - 1]; cand[b - 1] = tmp;
+        }
+      int64_t viol = -1;
+      for (int a = 0; a < nc; ++a) {
+        if (cnt) cnt->checks++;
+        if (level_at(iv, niv, cand[a]) + q > in->q_max) { viol = cand[a]; break; }
+      }
+      if (viol < 0) break;
+      /* "needs be delayed ... until finishing job i' at stage s'", the
+       * earliest finished one among the operations processing at that
+       * period (R5) */
+      int64_t e = -1;
+      for (int i = 0; i < niv; ++i)
+        if (iv[i].start <= viol && viol < iv[i].end && (e < 0 || iv[i].end < e)) e = iv[i].end;
+      t = e;
+      if (cnt) cnt->jumps++;
+    }
+    asg[cell] = m; S[cell] = t; C[cell] = t + p;
+    iv[niv].start = t; iv[niv].end = t + p; iv[niv].q = q; ++niv;
+    mfree[s * o + m] = t + p;
+    if (cnt) cnt->updates++;
+  }
+
+  {
+    /* Eqs. (1)-(3) over every job of J u J' (R9) */
+    int64_t sumT = 0, cmax = 0;
+    for (int j = 0; j < c->NJ; ++j) {
+      int64_t Cj = C[j * g + g - 1];
+      int64_t Tj = Cj - in->D[j];
+      if (Tj < 0) Tj = 0;
+      sumT += Tj;
+      if (Cj > cmax) cmax = Cj;
+    }
+    if (sumT_out) *sumT_out = sumT;
+    if (cmax_out) *cmax_out = cmax;
+    if (obj_out) *obj_out = in->wt * sumT + cmax;
+  }
+  if (assign_out) memcpy(assign_out, asg, cells * sizeof(int32_t));
+  if (start_out)
+    for (int cell = 0; cell < cells; ++cell) start_out[cell] = (int32_t)S[cell];
+done:
+  free(Z); free(byrank); free(asg); free(S); free(C); free(mfree); free(iv); free(cand);
+  return st;
+}
+
+void or_objective(const or_instance *in, const int32_t *assign, const int32_t *start,
+                  int64_t *sumT_out, int64_t *cmax_out, int64_t *obj_out) {
+  int g = in->g, NJ = in->n + in->n_prime;
+  int64_t sumT = 0, cmax = 0;
+  for (int j = 0; j < NJ; ++j) {
+    int cell = j * g + g - 1;
+    int64_t Cj = (int64_t)start[cell] + Pjsm(in, j, g - 1, assign[cell]);  /* Eq. (2)/(3) */
+    int64_t Tj = Cj - in->D[j];
+    sumT += Tj > 0 ? Tj : 0;
+    if (Cj > cmax) cmax = Cj;
+  }
+  *sumT_out = sumT; *cmax_out = cmax; *obj_out = in->wt * sumT + cmax;      /* Eq. (1) */
+}
+
+int64_t or_power_at(const or_instance *in, const int32_t *assign, const int32_t *start, int64_t t) {
+  int g = in->g, NJ = in->n + in->n_prime;
+  int64_t L = 0;
+  for (int cell = 0; cell < NJ * g; ++cell) {
+    int j = cell / g, s = cell % g;
+    int64_t e = (int64_t)start[cell] + Pjsm(in, j, s, assign[cell]);
+    if (start[cell] <= t && t < e) L += Qjsm(in, j, s, assign[cell]);   /* Eqs. (8)-(9) */
+  }
+  return L;
+}
+
+int or_validate(const or_ctx *c, const int32_t *assign, const int32_t *start, int32_t *kinds_out) {
+  const or_instance *in = &c->in;
+  int g = in->g, o = in->o, cells = c->cells, nviol = 0, kinds = 0;
+  for (int cell = 0; cell < cells; ++cell)
+    if (assign[cell] < 0 || assign[cell] >= o) { ++nviol; kinds |= 64; }
+  if (kinds & 64) { if (kinds_out) *kinds_out = kinds; return nviol; }
+  for (int j = 0; j < c->NJ; ++j) {
+    if (start[j * g] < in->R[j]) { ++nviol; kinds |= 1; }                    /* Eq. (4) */
+    for (int s = 1; s < g; ++s) {
+      int64_t prevC = (int64_t)start[j * g + s - 1] + Pjsm(in, j, s - 1, assign[j * g + s - 1]);
+      if (start[j * g + s] < prevC) { ++nviol; kinds |= 2; }                 /* Eq. (5) */
+    }
+  }
+  for (int a = 0; a < cells; ++a)
+    for (int b = a + 1; b < cells; ++b) {                                    /* Eq. (6) */
+      int sa = a % g, sb = b % g;
+      if (sa != sb || assign[a] != assign[b]) continue;
+      int64_t ea = (int64_t)start[a] + Pjsm(in, a / g, sa, assign[a]);
+      int64_t eb = (int64_t)start[b] + Pjsm(in, b / g, sb, assign[b]);
+      if (start[a] < eb && start[b] < ea) { ++nviol; kinds |= 4; }
+    }
+  for (int a = 0; a < cells; ++a)                                            /* Eq. (7) */
+    if (or_power_at(in, assign, start, start[a]) > in->q_max) { ++nviol; kinds |= 8; }
+  for (int cell = 0; cell < cells; ++cell) {
+    if (c->state[cell] == OR_PENDING) {
+      if (start[cell] < c->rs) { ++nviol; kinds |= 16; }                     /* Eq. (10) */
+    } else if (assign[cell] != c->fassign[cell] || start[cell] != c->fstart[cell]) {
+      ++nviol; kinds |= 32;
+    }
+  }
+  if (kinds_out) *kinds_out = kinds;
+  return nviol;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eq. (13) and the E_max rule                      */
+/* ------------------------------------------------------------------ */
+int64_t or_emax(const int64_t *objectives, int64_t count) {
+  /* "a is kept increasing from 1 until all individuals' initial objective
+   * function values are smaller than E_max" */
+  int64_t E = 10;
+  for (;;) {
+    int all_smaller = 1;
+    for (int64_t i = 0; i < count; ++i)
+      if (!(objectives[i] < E)) { all_smaller = 0; break; }
+    if (all_smaller) return E;
+    E *= 10;
+  }
+}
+int64_t or_fitness(int64_t objective, int64_t emax) {
+  int64_t f = emax - objective;
+  return f > 0 ? f : 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Brute force over the decoder-reachable set                          */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const or_ctx *c;
+  int32_t *X, *Z, *bestX, *bestZ;
+  int64_t best, evaluated;
+  int32_t *next_stage;  /* per job: next pending stage to rank */
+} bf_state;
+
+static void bf_all_X(bf_state *b) {
+  const or_ctx *c = b->c;
+  int K = c->K, o = c->in.o;
+  int32_t *digit = (int32_t *)calloc(K + 1, sizeof(int32_t));
+  for (;;) {
+    for (int gi = 0; gi < K; ++gi) b->X[c->gene_cell[gi]] = digit[gi];
+    int64_t obj;
+    or_decode(c, b->X, NULL, b->Z, NULL, NULL, NULL, NULL, &obj, NULL);
+    b->evaluated++;
+    if (b->best < 0 || obj < b->best) {
+      b->best = obj;
+      if (b->bestX) memcpy(b->bestX, b->X, c->cells * sizeof(int32_t));
+      if (b->bestZ) memcpy(b->bestZ, b->Z, c->cells * sizeof(int32_t));
+    }
+    int gi = 0;
+    while (gi < K && ++digit[gi] == o) digit[gi++] = 0;
+    if (gi == K) break;
+  }
+  free(digit);
+}
+
+static void bf_orders(bf_state *b, int rank) {
+  const or_ctx *c = b->c;
+  int g = c->in.g;
+  if (rank > c->K) { bf_all_X(b); return; }
+  for (int j = 0; j < c->NJ; ++j) {
+    int s = b->next_stage[j];
+    if (s >= g) continue;
+    b->Z[j * g + s] = rank;
+    b->next_stage[j]++;
+    bf_orders(b, rank + 1);
+    b->next_stage[j]--;
+    b->Z[j * g + s] = Z_UNRANKED;
+  }
+}
+
+int or_brute_force(const or_ctx *c, int64_t limit, int64_t *best_objective,
+                   int64_t *evaluated, int32_t *best_X, int32_t *best_Z) {
+  int g = c->in.g, K = c->K;
+  /* search size o^K * K! / prod_j L_j! */
+  double size = 1.0;
+  for (int i = 0; i < K; ++i) size *= c->in.o;
+  double orders = 1.0;
+  int idx = 1;
+  for (int j = 0; j < c->NJ; ++j) {
+    int L = 0;
+    for (int s = 0; s < g; ++s) L += c->state[j * g + s] == OR_PENDING;
+    for (int k = 1; k <= L; ++k) { orders *= (double)idx++; orders /= k; }
+  }
+  size *= orders;
+  if (size > (double)limit) return OR_ERR_LIMIT;
+  bf_state b;
+  b.c = c; b.best = -1; b.evaluated = 0; b.bestX = best_X; b.bestZ = best_Z;
+  b.X = (int32_t *)malloc(c->cells * sizeof(int32_t));
+  b.Z = (int32_t *)malloc(c->cells * sizeof(int32_t));
+  b.next_stage = (int32_t *)malloc(c->NJ * sizeof(int32_t));
+  for (int cell = 0; cell < c->cells; ++cell) {
+    b.X[cell] = -1;
+    b.Z[cell] = c->state[cell] == OR_RUNNING ? 0 : c->state[cell] == OR_COMPLETED ? Z_COMPLETED : Z_UNRANKED;
+  }
+  for (int j = 0; j < c->NJ; ++j) {
+    int s = 0;
+    while (s < g && c->state[j * g + s] != OR_PENDING) ++s;
+    b.next_stage[j] = s;
+  }
+  bf_orders(&b, 1);
+  *best_objective = b.best;
+  *evaluated = b.evaluated;
+  free(b.X); free(b.Z); free(b.next_stage);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* GA operators                                            */
+/* ------------------------------------------------------------------ */
+void or_repair(const or_ctx *c, int32_t *Y) {
+  /* "a correction step is required to replace the duplicate values by the
+   * missing values in ascending order" (R14) */
+  int K = c->K;
+  char *seen = (char *)calloc(K + 2, 1);
+  char *dup = (char *)calloc(c->cells, 1);
+  for (int cell = 0; cell < c->cells; ++cell) {       /* row-major scan */
+    if (c->state[cell] != OR_PENDING) continue;
+    int v = Y[cell];
+    if (v >= 1 && v <= K && !seen[v]) seen[v] = 1;  /* first occurrence kept */
+    else dup[cell] = 1;
+  }
+  int next_missing = 1;
+  for (int cell = 0; cell < c->cells; ++cell) {
+    if (!dup[cell]) continue;
+    while (seen[next_missing]) ++next_missing;
+    Y[cell] = next_missing;
+    seen[next_missing] = 1;
+  }
+  free(seen); free(dup);
+}
+
+void or_crossover(const or_ctx *c, const int32_t *XA, const int32_t *YA,
+                  const int32_t *XB, const int32_t *YB, int32_t p,
+                  int32_t *XA2, int32_t *YA2, int32_t *XB2, int32_t *YB2) {
+  /* "a 2D single point crossover is executed for the target machine matrix
+   * and the priority matrix respectively": one row-major cut p,
+   * shared by X and Y (R13); cells at position >= p are exchanged. */
+  for (int cell = 0; cell < c->cells; ++cell) {
+    if (cell < p) { XA2[cell] = XA[cell]; YA2[cell] = YA[cell]; XB2[cell] = XB[cell]; YB2[cell] = YB[cell]; }
+    else          { XA2[cell] = XB[cell]; YA2[cell] = YB[cell]; XB2[cell] = XA[cell]; YB2[cell] = YA[cell]; }
+  }
+  or_repair(c, YA2);
+  or_repair(c, YB2);
+}
+
+void or_mutate(const or_ctx *c, int32_t *X, int32_t *Y, const uint32_t *rx,
+               int32_t gene_a, int32_t gene_b) {
+  /* "The non-negative elements of the target machine matrix ... are
+   * replaced by random values in the range, apart from the original ones.
+   * Regarding the priority matrix, two non-negative elements are chosen
+   * randomly to exchange the values." (R15) */
+  int o = c->in.o, K = c->K;
+  if (o >= 2 && rx)
+    for (int gi = 0; gi < K; ++gi) {
+      int cell = c->gene_cell[gi];
+      X[cell] = (X[cell] + 1 + (int32_t)bounded(rx[gi], (uint32_t)(o - 1))) % o;
+    }
+  if (K >= 2 && gene_a >= 0 && gene_b >= 0 && gene_a != gene_b) {
+    int ca = c->gene_cell[gene_a], cb = c->gene_cell[gene_b];
+    int32_t t = Y[ca]; Y[ca] = Y[cb]; Y[cb] = t;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* threaded evaluation (for baseline timing; results are per-cell)     */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const or_ctx *c;
+  int64_t begin, end;
+  const int32_t *Xs, *Ys;        /* matrix form [count*cells] or NULL */
+  const int8_t *xc; const int16_t *yc;   /* compact form [count*K]  */
+  int64_t *obj, *sumT, *cmax;
+  or_counters cnt;
+  int status;
+} eval_job;
+
+static void *eval_worker(void *arg) {
+  eval_job *w = (eval_job *)arg;
+  const or_ctx *c = w->c;
+  int32_t *X = NULL, *Y = NULL;
+  if (!w->Xs) {
+    X = (int32_t *)malloc(c->cells * sizeof(int32_t));
+    Y = (int32_t *)malloc(c->cells * sizeof(int32_t));
+    for (int cell = 0; cell < c->cells; ++cell) { X[cell] = -1; Y[cell] = -1; }
+  }
+  for (int64_t i = w->begin; i < w->end; ++i) {
+    const int32_t *Xi, *Yi;
+    if (w->Xs) { Xi = w->Xs + i * c->cells; Yi = w->Ys + i * c->cells; }
+    else {
+      for (int gi = 0; gi < c->K; ++gi) {
+        X[c->gene_cell[gi]] = w->xc[i * c->K + gi];
+        Y[c->gene_cell[gi]] = w->yc[i * c->K + gi];
+      }
+      Xi = X; Yi = Y;
+    }
+    int64_t T, M, O;
+    int st = or_decode(c, Xi, Yi, NULL, NULL, NULL, &T, &M, &O, &w->cnt);
+    if (st != OR_OK) { w->status = st; break; }
+    if (w->obj) w->obj[i] = O;
+    if (w->sumT) w->sumT[i] = T;
+    if (w->cmax) w->cmax[i] = M;
+  }
+  free(X); free(Y);
+  return NULL;
+}
+
+static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int32_t *Ys,
+                    const int8_t *xc, const int16_t *yc, int64_t *obj, int64_t *sumT,
+                    int64_t *cmax, int nthreads, or_counters *cnt) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > count) nthreads = count > 0 ? (int)count : 1;
+  eval_job *jobs = (eval_job *)calloc(nthreads, sizeof(eval_job));
+  pthread_t *th = (pthread_t *)calloc(nthreads, sizeof(pthread_t));
+  for (int t = 0; t < nthreads; ++t) {           /* static partition */
+    jobs[t].c = c;
+    jobs[t].begin = count * t / nthreads;
+    jobs[t].end = count * (t + 1) / nthreads;
+    jobs[t].Xs = Xs; jobs[t].Ys = Ys; jobs[t].xc = xc; jobs[t].yc = yc;
+    jobs[t].obj = obj; jobs[t].sumT = sumT; jobs[t].cmax = cmax;
+  }
+  if (nthreads == 1) eval_worker(&jobs[0]);
+  else {
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, eval_worker, &jobs[t]);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  }
+  int st = OR_OK;
+  for (int t = 0; t < nthreads; ++t) {
+    if (jobs[t].status != OR_OK) st = jobs[t].status;
+    if (cnt) {
+      cnt->dispatches += jobs[t].cnt.dispatches; cnt->checks += jobs[t].cnt.checks;
+      cnt->jumps += jobs[t].cnt.jumps; cnt->updates += jobs[t].cnt.updates;
+    }
+  }
+  free(jobs); free(th);
+  return st;
+}
+
+int or_evaluate_batch(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
+                      int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
+                      int32_t nthreads, or_counters *cnt) {
+  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, nthreads, cnt);
+}
+
+/* ------------------------------------------------------------------ */
+/* The hybrid island GA (R13-R23)                */
+/* ------------------------------------------------------------------ */
+struct or_run {
+  const or_ctx *c;
+  or_ga_cfg cfg;
+  int32_t tile, nisl, nloc;          /* cells per island, local islands, local cells */
+  int32_t gen;                       /* last completed generation (-1 = fresh) */
+  int64_t emax;
+  int32_t *X, *Y;                    /* [nloc*cells] */
+  int64_t *obj, *fit;                /* [nloc] */
+  int32_t *HX, *HY;                  /* history elites [nisl*cells] */
+  int64_t *hobj, *hfit;
+  int64_t *tmin, *tsum;              /* [G+1] local trace */
+};
+
+int or_ga_create(const or_ctx *c, const or_ga_cfg *cfg, or_run **out) {
+  if (cfg->island_w < 2 || (cfg->island_w & 1) || cfg->island_h < 1) return OR_ERR_ARG;
+  if (cfg->island_begin < 0 || cfg->island_end > cfg->islands_total ||
+      cfg->island_begin >= cfg->island_end || cfg->generations < 0 || cfg->migration_interval < 1)
+    return OR_ERR_ARG;
+  or_run *r = (or_run *)calloc(1, sizeof(or_run));
+  r->c = c; r->cfg = *cfg;
+  r->tile = cfg->island_w * cfg->island_h;
+  r->nisl = cfg->island_end - cfg->island_begin;
+  r->nloc = r->nisl * r->tile;
+  r->gen = -1;
+  size_t cells = c->cells;
+  r->X = (int32_t *)malloc((size_t)r->nloc * cells * sizeof(int32_t));
+  r->Y = (int32_t *)malloc((size_t)r->nloc * cells * sizeof(int32_t));
+  r->obj = (int64_t *)malloc(r->nloc * sizeof(int64_t));
+  r->fit = (int64_t *)malloc(r->nloc * sizeof(int64_t));
+  r->HX = (int32_t *)malloc((size_t)r->nisl * cells * sizeof(int32_t));
+  r->HY = (int32_t *)malloc((size_t)r->nisl * cells * sizeof(int32_t));
+  r->hobj = (int64_t *)malloc(r->nisl * sizeof(int64_t));
+  r->hfit = (int64_t *)malloc(r->nisl * sizeof(int64_t));
+  r->tmin = (int64_t *)calloc(cfg->generations + 1, sizeof(int64_t));
+  r->tsum = (int64_t *)calloc(cfg->generations + 1, sizeof(int64_t));
+  *out = r;
+  return OR_OK;
+}
+
+void or_ga_destroy(or_run *r) {
+  if (!r) return;
+  free(r->X); free(r->Y); free(r->obj); free(r->fit); free(r->HX); free(r->HY);
+  free(r->hobj); free(r->hfit); free(r->tmin); free(r->tsum); free(r);
+}
+
+static int32_t *cellX(or_run *r, int idx) { return r->X + (size_t)idx * r->c->cells; }
+static int32_t *cellY(or_run *r, int idx) { return r->Y + (size_t)idx * r->c->cells; }
+
+static void evaluate_population(or_run *r) {
+  run_eval(r->c, r->nloc, r->X, r->Y, NULL, NULL, r->obj, NULL, NULL, r->cfg.nthreads, NULL);
+  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness(r->obj[i], r->emax);
+}
+
+static void record_trace(or_run *r, int k) {
+  int64_t mn = r->obj[0], sum = 0;
+  for (int i = 0; i < r->nloc; ++i) { if (r->obj[i] < mn) mn = r->obj[i]; sum += r->obj[i]; }
+  r->tmin[k] = mn; r->tsum[k] = sum;
+}
+
+/* argmax fitness inside island li (ties -> lowest cell index) */
+static int island_best(const or_run *r, int li) {
+  int base = li * r->tile, b = base;
+  for (int i = base + 1; i < base + r->tile; ++i) if (r->fit[i] > r->fit[b]) b = i;
+  return b;
+}
+/* argmin fitness inside island li (ties -> lowest cell index) */
+static int island_worst(const or_run *r, int li) {
+  int base = li * r->tile, w = base;
+  for (int i = base + 1; i < base + r->tile; ++i) if (r->fit[i] < r->fit[w]) w = i;
+  return w;
+}
+
+static void set_history(or_run *r, int li, int idx) {
+  size_t cells = r->c->cells;
+  memcpy(r->HX + li * cells, cellX(r, idx), cells * sizeof(int32_t));
+  memcpy(r->HY + li * cells, cellY(r, idx), cells * sizeof(int32_t));
+  r->hobj[li] = r->obj[idx]; r->hfit[li] = r->fit[idx];
+}
+
+static int ga_init(or_run *r) {
+  const or_ctx *c = r->c;
+  int K = c->K, o = c->in.o;
+  uint64_t seed = r->cfg.seed;
+  uint32_t *keys = (uint32_t *)malloc((K + 1) * sizeof(uint32_t));
+  for (int li = 0; li < r->nisl; ++li) {
+    uint32_t I = (uint32_t)(r->cfg.island_begin + li);
+    for (int i = 0; i < r->tile; ++i) {
+      int32_t *X = cellX(r, li * r->tile + i), *Y = cellY(r, li * r->tile + i);
+      for (int cell = 0; cell < c->cells; ++cell) { X[cell] = -1; Y[cell] = -1; }
+      /* "x_js(k) is equal to a random integer representing the target
+       * machine"; "y_js(k) is also generated randomly from the range
+       * starting from 1 to the amount of unassigned operations ... unique"
+       * (P:227): y = 1 + rank of the gene's random key. */
+      for (int gi = 0; gi < K; ++gi) {
+        X[c->gene_cell[gi]] = (int32_t)bounded(draw(seed, 1, gi / 4, gi % 4, i, 0, I), (uint32_t)o);
+        keys[gi] = draw(seed, 2, gi / 4, gi % 4, i, 0, I);
+      }
+      for (int gi = 0; gi < K; ++gi) {
+        int rank = 0;
+        for (int h = 0; h < K; ++h)
+          if (keys[h] < keys[gi] || (keys[h] == keys[gi] && h < gi)) ++rank;
+        Y[c->gene_cell[gi]] = rank + 1;
+      }
+    }
+  }
+  free(keys);
+  /* E_max from every individual's initial objective (R23: global) */
+  r->emax = 10;   /* placeholder so evaluate_population computes fitness */
+  evaluate_population(r);
+  int64_t mx = r->obj[0];
+  for (int i = 1; i < r->nloc; ++i) if (r->obj[i] > mx) mx = r->obj[i];
+  if (r->cfg.allreduce_max && r->cfg.allreduce_max(r->cfg.user, &mx) != 0) return OR_ERR_ARG;
+  r->emax = or_emax(&mx, 1);
+  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness(r->obj[i], r->emax);
+  for (int li = 0; li < r->nisl; ++li) set_history(r, li, island_best(r, li));
+  record_trace(r, 0);
+  r->gen = 0;
+  return OR_OK;
+}
+
+static int ga_generation(or_run *r, int k) {
+  const or_ctx *c = r->c;
+  int K = c->K, o = c->in.o, cells = c->cells;
+  int w = r->cfg.island_w, h = r->cfg.island_h, tile = r->tile;
+  uint64_t seed = r->cfg.seed;
+  size_t bytes = (size_t)r->nloc * cells * sizeof(int32_t);
+  /* snapshot of generation k-1 (synchronous update, R18) */
+  int32_t *PX = (int32_t *)malloc(bytes), *PY = (int32_t *)malloc(bytes);
+  int64_t *Pfit = (int64_t *)malloc(r->nloc * sizeof(int64_t));
+  memcpy(PX, r->X, bytes); memcpy(PY, r->Y, bytes);
+  memcpy(Pfit, r->fit, r->nloc * sizeof(int64_t));
+  int32_t *winner = (int32_t *)malloc(tile * sizeof(int32_t));
+  uint32_t *rx = (uint32_t *)malloc((K + 1) * sizeof(uint32_t));
+
+  for (int li = 0; li < r->nisl; ++li) {
+    uint32_t I = (uint32_t)(r->cfg.island_begin + li);
+    int base = li * tile;
+    /* local asteroid selection: tournament over self, N, S, E, W
+     * (torus inside the island tile, R17); largest fitness wins, ties in
+     * that order (R18) */
+    for (int row = 0; row < h; ++row)
+      for (int col = 0; col < w; ++col) {
+        int nb[5] = {row * w + col,
+                     ((row + h - 1) % h) * w + col,
+                     ((row + 1) % h) * w + col,
+                     row * w + (col + 1) % w,
+                     row * w + (col + w - 1) % w};
+        int best = nb[0];
+        for (int t = 1; t < 5; ++t) if (Pfit[base + nb[t]] > Pfit[base + best]) best = nb[t];
+        winner[row * w + col] = best;
+      }
+    /* neighbouring paired crossover: pairs (r,2c),(r,2c+1) (R19) */
+    for (int row = 0; row < h; ++row)
+      for (int cp = 0; cp < w / 2; ++cp) {
+        int a = row * w + 2 * cp, b = a + 1;
+        const int32_t *XA = PX + (size_t)(base + winner[a]) * cells, *YA = PY + (size_t)(base + winner[a]) * cells;
+        const int32_t *XB = PX + (size_t)(base + winner[b]) * cells, *YB = PY + (size_t)(base + winner[b]) * cells;
+        uint32_t fire = draw(seed, 3, 0, 0, (uint32_t)a, (uint32_t)k, I);
+        if (fire < r->cfg.xo_threshold) {
+          uint32_t ucut = draw(seed, 3, 0, 1, (uint32_t)a, (uint32_t)k, I);
+          int32_t p = 1 + (int32_t)bounded(ucut, (uint32_t)(cells - 1));
+          or_crossover(c, XA, YA, XB, YB, p, cellX(r, base + a), cellY(r, base + a),
+                       cellX(r, base + b), cellY(r, base + b));
+        } else {
+          memcpy(cellX(r, base + a), XA, cells * sizeof(int32_t));
+          memcpy(cellY(r, base + a), YA, cells * sizeof(int32_t));
+          memcpy(cellX(r, base + b), XB, cells * sizeof(int32_t));
+          memcpy(cellY(r, base + b), YB, cells * sizeof(int32_t));
+        }
+      }
+    /* mutation: per individual with probability p_m (R16) */
+    for (int i = 0; i < tile; ++i) {
+      uint32_t fire = draw(seed, 4, 0, 0, (uint32_t)i, (uint32_t)k, I);
+      if (fire >= r->cfg.mut_threshold) continue;
+      for (int gi = 0; gi < K; ++gi) rx[gi] = draw(seed, 5, gi / 4, gi % 4, (uint32_t)i, (uint32_t)k, I);
+      int32_t ga = -1, gb = -1;
+      if (K >= 2) {
+        ga = (int32_t)bounded(draw(seed, 4, 0, 1, (uint32_t)i, (uint32_t)k, I), (uint32_t)K);
+        gb = (int32_t)bounded(draw(seed, 4, 0, 2, (uint32_t)i, (uint32_t)k, I), (uint32_t)(K - 1));
+        if (gb >= ga) ++gb;
+      }
+      or_mutate(c, cellX(r, base + i), cellY(r, base + i), o >= 2 ? rx : NULL, ga, gb);
+    }
+  }
+  free(PX); free(PY); free(Pfit); free(winner); free(rx);
+
+  evaluate_population(r);
+
+  /* elitist replacement (R21) */
+  for (int li = 0; li < r->nisl; ++li) {
+    int b = island_best(r, li);
+    if (r->fit[b] > r->hfit[li]) set_history(r, li, b);
+    int wst = island_worst(r, li);
+    memcpy(cellX(r, wst), r->HX + (size_t)li * cells, cells * sizeof(int32_t));
+    memcpy(cellY(r, wst), r->HY + (size_t)li * cells, cells * sizeof(int32_t));
+    r->obj[wst] = r->hobj[li]; r->fit[wst] = r->hfit[li];
+  }
+
+  /* single-ring migration every migration_interval generations (R22) */
+  if (k % r->cfg.migration_interval == 0 && r->cfg.islands_total >= 2) {
+    size_t rec = (size_t)cells * 2 * sizeof(int32_t) + 2 * sizeof(int64_t);
+    char *donors = (char *)malloc(rec * r->nisl);
+    int *worst = (int *)malloc(r->nisl * sizeof(int));
+    for (int li = 0; li < r->nisl; ++li) {    /* snapshot first: synchronous */
+      int b = island_best(r, li);
+      char *d = donors + rec * li;
+      memcpy(d, cellX(r, b), cells * sizeof(int32_t));
+      memcpy(d + cells * sizeof(int32_t), cellY(r, b), cells * sizeof(int32_t));
+      memcpy(d + cells * 2 * sizeof(int32_t), &r->obj[b], sizeof(int64_t));
+      memcpy(d + cells * 2 * sizeof(int32_t) + sizeof(int64_t), &r->fit[b], sizeof(int64_t));
+      worst[li] = island_worst(r, li);
+    }
+    /* island begin receives from global island begin-1: the last island of
+     * the previous shard (rank-1 mod world) */
+    char *incoming = (char *)malloc(rec);
+    if (r->cfg.allgather && r->cfg.world > 1) {
+      char *all = (char *)malloc(rec * r->cfg.world);
+      r->cfg.allgather(r->cfg.user, donors + rec * (r->nisl - 1), all, rec);
+      memcpy(incoming, all + rec * ((r->cfg.rank + r->cfg.world - 1) % r->cfg.world), rec);
+      free(all);
+    } else {
+      memcpy(incoming, donors + rec * (r->nisl - 1), rec);
+    }
+    for (int li = 0; li < r->nisl; ++li) {
+      const char *src = li == 0 ? incoming : donors + rec * (li - 1);
+      int wst = worst[li];
+      memcpy(cellX(r, wst), src, cells * sizeof(int32_t));
+      memcpy(cellY(r, wst), src + cells * sizeof(int32_t), cells * sizeof(int32_t));
+      memcpy(&r->obj[wst], src + cells * 2 * sizeof(int32_t), sizeof(int64_t));
+      memcpy(&r->fit[wst], src + cells * 2 * sizeof(int32_t) + sizeof(int64_t), sizeof(int64_t));
+    }
+    free(donors); free(worst); free(incoming);
+  }
+  record_trace(r, k);
+  r->gen = k;
+  return OR_OK;
+}
+
+int or_ga_step(or_run *r) {
+  if (r->c->K == 0) return OR_ERR_ARG;
+  if (r->gen < 0) return ga_init(r);
+  if (r->gen >= r->cfg.generations) return OR_ERR_ARG;
+  return ga_generation(r, r->gen + 1);
+}
+int32_t or_ga_generation(const or_run *r) { return r->gen; }
+int64_t or_ga_emax(const or_run *r) { return r->emax; }
+
+void or_ga_population(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+  const or_ctx *c = r->c;
+  for (int i = 0; i < r->nloc; ++i)
+    for (int gi = 0; gi < c->K; ++gi) {
+      int cell = c->gene_cell[gi];
+      if (x) x[(size_t)i * c->K + gi] = (int8_t)r->X[(size_t)i * c->cells + cell];
+      if (y) y[(size_t)i * c->K + gi] = (int16_t)r->Y[(size_t)i * c->cells + cell];
+    }
+  if (obj) memcpy(obj, r->obj, r->nloc * sizeof(int64_t));
+  if (fit) memcpy(fit, r->fit, r->nloc * sizeof(int64_t));
+}
+
+void or_ga_history(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+  const or_ctx *c = r->c;
+  for (int li = 0; li < r->nisl; ++li)
+    for (int gi = 0; gi < c->K; ++gi) {
+      int cell = c->gene_cell[gi];
+      if (x) x[(size_t)li * c->K + gi] = (int8_t)r->HX[(size_t)li * c->cells + cell];
+      if (y) y[(size_t)li * c->K + gi] = (int16_t)r->HY[(size_t)li * c->cells + cell];
+    }
+  if (obj) memcpy(obj, r->hobj, r->nisl * sizeof(int64_t));
+  if (fit) memcpy(fit, r->hfit, r->nisl * sizeof(int64_t));
+}
+
+void or_ga_trace(const or_run *r, int64_t *tmin, int64_t *tsum) {
+  int n = r->cfg.generations + 1;
+  if (tmin) memcpy(tmin, r->tmin, n * sizeof(int64_t));
+  if (tsum) memcpy(tsum, r->tsum, n * sizeof(int64_t));
+}

@@ -1,0 +1,367 @@
+"""ctypes wrapper of the C ORACLE (oracle/ffs_oracle.c).
+
+TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / ``--impl reference`` leg may import this module.
+It shares nothing with the CUDA path (paper_1903_10741_b200/); the product
+never imports it.
+
+Notation follows PAPER.md: X, Y, Z are (n+n') x g matrices (row-major, -1 on
+frozen cells) -- Eqs. (10)-(12).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "ffs_oracle.c")
+LIB = os.path.join(HERE, "libffs_oracle.so")
+
+PENDING, RUNNING, COMPLETED = 0, 1, 2
+Z_COMPLETED = -2
+OK, ERR_ARG, ERR_INFEASIBLE, ERR_SCHEDULE, ERR_LIMIT = 0, 1, 2, 3, 4
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc (no GPU, no shared code)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
+            os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "ffs_oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-Wextra", "-Wno-unused-parameter",
+                               "-shared", "-fPIC", "-o", LIB, SRC, "-lpthread"])
+    return LIB
+
+
+class _Inst(C.Structure):
+    _fields_ = [("n", C.c_int32), ("n_prime", C.c_int32), ("g", C.c_int32), ("o", C.c_int32),
+                ("P", C.POINTER(C.c_int32)), ("Q", C.POINTER(C.c_int32)),
+                ("R", C.POINTER(C.c_int32)), ("D", C.POINTER(C.c_int32)),
+                ("q_max", C.c_int32), ("wt", C.c_int64)]
+
+
+class _Cnt(C.Structure):
+    _fields_ = [("dispatches", C.c_int64), ("checks", C.c_int64),
+                ("jumps", C.c_int64), ("updates", C.c_int64)]
+
+
+_ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64))
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class _GaCfg(C.Structure):
+    _fields_ = [("island_w", C.c_int32), ("island_h", C.c_int32), ("islands_total", C.c_int32),
+                ("island_begin", C.c_int32), ("island_end", C.c_int32),
+                ("xo_threshold", C.c_uint32), ("mut_threshold", C.c_uint32),
+                ("migration_interval", C.c_int32), ("generations", C.c_int32),
+                ("seed", C.c_uint64), ("nthreads", C.c_int32),
+                ("allreduce_max", _ALLRED), ("allgather", _ALLGATHER),
+                ("rank", C.c_int32), ("world", C.c_int32), ("user", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.c_void_p
+        _lib.or_ctx_create.argtypes = [C.POINTER(_Inst), C.c_int32, P, P, C.POINTER(P)]
+        _lib.or_ctx_destroy.argtypes = [P]
+        _lib.or_ctx_K.argtypes = [P]
+        _lib.or_ctx_cells.argtypes = [P]
+        _lib.or_ctx_states.argtypes = [P, P]
+        _lib.or_ctx_pending_cells.argtypes = [P, P]
+        _lib.or_order.argtypes = [P, P, P]
+        _lib.or_decode.argtypes = [P, P, P, P, P, P, P, P, P, C.POINTER(_Cnt)]
+        _lib.or_objective.argtypes = [C.POINTER(_Inst), P, P, P, P, P]
+        _lib.or_validate.argtypes = [P, P, P, P]
+        _lib.or_power_at.argtypes = [C.POINTER(_Inst), P, P, C.c_int64]
+        _lib.or_power_at.restype = C.c_int64
+        _lib.or_emax.argtypes = [P, C.c_int64]
+        _lib.or_emax.restype = C.c_int64
+        _lib.or_fitness.argtypes = [C.c_int64, C.c_int64]
+        _lib.or_fitness.restype = C.c_int64
+        _lib.or_brute_force.argtypes = [P, C.c_int64, P, P, P, P]
+        _lib.or_philox4x32_10.argtypes = [P, P, P]
+        _lib.or_repair.argtypes = [P, P]
+        _lib.or_crossover.argtypes = [P, P, P, P, P, C.c_int32, P, P, P, P]
+        _lib.or_mutate.argtypes = [P, P, P, P, C.c_int32, C.c_int32]
+        _lib.or_ga_create.argtypes = [P, C.POINTER(_GaCfg), C.POINTER(P)]
+        _lib.or_ga_step.argtypes = [P]
+        _lib.or_ga_generation.argtypes = [P]
+        _lib.or_ga_emax.argtypes = [P]
+        _lib.or_ga_emax.restype = C.c_int64
+        _lib.or_ga_population.argtypes = [P, P, P, P, P]
+        _lib.or_ga_trace.argtypes = [P, P, P]
+        _lib.or_ga_history.argtypes = [P, P, P, P, P]
+        _lib.or_ga_destroy.argtypes = [P]
+        _lib.or_evaluate_batch.argtypes = [P, C.c_int64, P, P, P, P, P, C.c_int32, C.POINTER(_Cnt)]
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+@dataclass
+class Instance:
+    """EDFFS instance in integer ticks (Table 2)."""
+    n: int
+    n_prime: int
+    g: int
+    o: int
+    P: np.ndarray      # [(n+n'), g, o]
+    Q: np.ndarray      # [(n+n'), g, o]
+    R: np.ndarray      # [n+n']
+    D: np.ndarray      # [n+n']
+    q_max: int
+    wt: int
+
+    def _c(self):
+        self._keep = [_i32(self.P).ravel(), _i32(self.Q).ravel(), _i32(self.R), _i32(self.D)]
+        ptr = [a.ctypes.data_as(C.POINTER(C.c_int32)) for a in self._keep]
+        return _Inst(self.n, self.n_prime, self.g, self.o, ptr[0], ptr[1], ptr[2], ptr[3],
+                     int(self.q_max), int(self.wt))
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, what):
+        super().__init__(f"oracle {what} failed with status {code}")
+        self.code = code
+
+
+def _chk(st, what):
+    if st != OK:
+        raise OracleError(st, what)
+
+
+def philox(ctr, key):
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def emax(objectives) -> int:
+    a = np.ascontiguousarray(np.asarray(objectives, dtype=np.int64))
+    return int(lib().or_emax(_p(a), len(a)))
+
+
+def fitness(objective: int, e_max: int) -> int:
+    return int(lib().or_fitness(int(objective), int(e_max)))
+
+
+def objective(inst: Instance, assign, start):
+    ci = inst._c()
+    a, s = _i32(assign).ravel(), _i32(start).ravel()
+    T, M, O = C.c_int64(), C.c_int64(), C.c_int64()
+    lib().or_objective(C.byref(ci), _p(a), _p(s), C.byref(T), C.byref(M), C.byref(O))
+    return T.value, M.value, O.value
+
+
+def power_at(inst: Instance, assign, start, t) -> int:
+    ci = inst._c()
+    a, s = _i32(assign).ravel(), _i32(start).ravel()
+    return int(lib().or_power_at(C.byref(ci), _p(a), _p(s), int(t)))
+
+
+class Ctx:
+    """Frozen rescheduling context at RS (Algorithm 1 frozen branch)."""
+
+    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None):
+        self.inst = inst
+        self._ci = inst._c()
+        self._oa = None if orig_assign is None else _i32(orig_assign).ravel()
+        self._os = None if orig_start is None else _i32(orig_start).ravel()
+        h = C.c_void_p()
+        _chk(lib().or_ctx_create(C.byref(self._ci), int(rs), _p(self._oa), _p(self._os),
+                                 C.byref(h)), "ctx_create")
+        self.h = h
+        self.rs = int(rs)
+        self.K = lib().or_ctx_K(h)
+        self.cells = lib().or_ctx_cells(h)
+        st = np.zeros(self.cells, dtype=np.int32)
+        lib().or_ctx_states(h, _p(st))
+        self.states = st.reshape(inst.n + inst.n_prime, inst.g)
+        pc = np.zeros(max(self.K, 1), dtype=np.int32)
+        lib().or_ctx_pending_cells(h, _p(pc))
+        self.pending_cells = pc[:self.K].copy()
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.or_ctx_destroy(self.h)
+            self.h = None
+
+    # compact canonical genes <-> paper matrices
+    def to_matrix(self, x_genes, y_genes):
+        X = -np.ones(self.cells, dtype=np.int32)
+        Y = -np.ones(self.cells, dtype=np.int32)
+        X[self.pending_cells] = np.asarray(x_genes, dtype=np.int32)
+        Y[self.pending_cells] = np.asarray(y_genes, dtype=np.int32)
+        return X, Y
+
+    def to_genes(self, X, Y):
+        X = np.asarray(X).ravel()
+        Y = np.asarray(Y).ravel()
+        return X[self.pending_cells].astype(np.int8), Y[self.pending_cells].astype(np.int16)
+
+    def order(self, Y):
+        Yc = _i32(Y).ravel()
+        Z = np.zeros(self.cells, dtype=np.int32)
+        _chk(lib().or_order(self.h, _p(Yc), _p(Z)), "order")
+        return Z
+
+    def decode(self, X, Y=None, Z=None):
+        Xc = _i32(X).ravel()
+        Yc = None if Y is None else _i32(Y).ravel()
+        Zc = None if Z is None else _i32(Z).ravel()
+        asg = np.zeros(self.cells, dtype=np.int32)
+        st = np.zeros(self.cells, dtype=np.int32)
+        T, M, O = C.c_int64(), C.c_int64(), C.c_int64()
+        cnt = _Cnt()
+        _chk(lib().or_decode(self.h, _p(Xc), _p(Yc), _p(Zc), _p(asg), _p(st), C.byref(T),
+                             C.byref(M), C.byref(O), C.byref(cnt)), "decode")
+        return dict(assign=asg, start=st, sum_tardiness=T.value, makespan=M.value,
+                    objective=O.value,
+                    counters=dict(dispatches=cnt.dispatches, checks=cnt.checks,
+                                  jumps=cnt.jumps, updates=cnt.updates))
+
+    def decode_genes(self, x_genes, y_genes):
+        X, Y = self.to_matrix(x_genes, y_genes)
+        return self.decode(X, Y)
+
+    def validate(self, assign, start):
+        a, s = _i32(assign).ravel(), _i32(start).ravel()
+        kinds = C.c_int32()
+        n = lib().or_validate(self.h, _p(a), _p(s), C.byref(kinds))
+        return n, kinds.value
+
+    def brute_force(self, limit=10**7):
+        best = C.c_int64()
+        ev = C.c_int64()
+        bx = np.zeros(self.cells, dtype=np.int32)
+        bz = np.zeros(self.cells, dtype=np.int32)
+        _chk(lib().or_brute_force(self.h, int(limit), C.byref(best), C.byref(ev), _p(bx), _p(bz)),
+             "brute_force")
+        return best.value, ev.value, bx, bz
+
+    def repair(self, Y):
+        Yc = _i32(Y).ravel().copy()
+        lib().or_repair(self.h, _p(Yc))
+        return Yc
+
+    def crossover(self, XA, YA, XB, YB, p):
+        ins = [_i32(a).ravel() for a in (XA, YA, XB, YB)]
+        outs = [np.zeros(self.cells, dtype=np.int32) for _ in range(4)]
+        lib().or_crossover(self.h, *[_p(a) for a in ins], int(p), *[_p(a) for a in outs])
+        return outs
+
+    def mutate(self, X, Y, rx, gene_a, gene_b):
+        Xc, Yc = _i32(X).ravel().copy(), _i32(Y).ravel().copy()
+        r = None if rx is None else np.ascontiguousarray(np.asarray(rx, dtype=np.uint32))
+        lib().or_mutate(self.h, _p(Xc), _p(Yc), _p(r), int(gene_a), int(gene_b))
+        return Xc, Yc
+
+    def evaluate_batch(self, x, y, nthreads=1):
+        """Decode + evaluate compact chromosomes x[count,K] int8, y[count,K] int16."""
+        x = np.ascontiguousarray(x, dtype=np.int8)
+        y = np.ascontiguousarray(y, dtype=np.int16)
+        count = x.shape[0]
+        obj = np.zeros(count, dtype=np.int64)
+        T = np.zeros(count, dtype=np.int64)
+        M = np.zeros(count, dtype=np.int64)
+        cnt = _Cnt()
+        _chk(lib().or_evaluate_batch(self.h, count, _p(x), _p(y), _p(obj), _p(T), _p(M),
+                                     int(nthreads), C.byref(cnt)), "evaluate_batch")
+        return obj, T, M, dict(dispatches=cnt.dispatches, checks=cnt.checks, jumps=cnt.jumps,
+                               updates=cnt.updates)
+
+
+XO_090 = 3865470566   # floor(0.9 * 2^32)
+MUT_010 = 429496729   # floor(0.1 * 2^32)
+
+
+class GA:
+    """Literal island GA of one rescheduling point (shard-aware)."""
+
+    def __init__(self, ctx: Ctx, island_w, island_h, islands_total, generations, seed,
+                 island_begin=0, island_end=None, xo_threshold=XO_090, mut_threshold=MUT_010,
+                 migration_interval=10, nthreads=1, allreduce_max=None, allgather=None,
+                 rank=0, world=1):
+        self.ctx = ctx
+        island_end = islands_total if island_end is None else island_end
+        self._cb = []
+        ar = _ALLRED()
+        ag = _ALLGATHER()
+        if allreduce_max is not None:
+            def _ar(user, ptr):
+                ptr[0] = int(allreduce_max(int(ptr[0])))
+                return 0
+            ar = _ALLRED(_ar)
+        if allgather is not None:
+            def _ag(user, send, recv, nbytes):
+                buf = C.string_at(send, nbytes)
+                out = allgather(buf)  # list of bytes, rank-major
+                joined = b"".join(out)
+                C.memmove(recv, joined, len(joined))
+                return 0
+            ag = _ALLGATHER(_ag)
+        self._cb = [ar, ag]
+        self.cfg = _GaCfg(island_w, island_h, islands_total, island_begin, island_end,
+                          xo_threshold, mut_threshold, migration_interval, generations, seed,
+                          nthreads, ar, ag, rank, world, None)
+        h = C.c_void_p()
+        _chk(lib().or_ga_create(ctx.h, C.byref(self.cfg), C.byref(h)), "ga_create")
+        self.h = h
+        self.generations = generations
+        self.nloc = (island_end - island_begin) * island_w * island_h
+        self.nisl = island_end - island_begin
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.or_ga_destroy(self.h)
+            self.h = None
+
+    def step(self):
+        _chk(lib().or_ga_step(self.h), "ga_step")
+
+    @property
+    def generation(self):
+        return lib().or_ga_generation(self.h)
+
+    @property
+    def emax(self):
+        return int(lib().or_ga_emax(self.h))
+
+    def population(self):
+        K = self.ctx.K
+        x = np.zeros((self.nloc, K), dtype=np.int8)
+        y = np.zeros((self.nloc, K), dtype=np.int16)
+        obj = np.zeros(self.nloc, dtype=np.int64)
+        fit = np.zeros(self.nloc, dtype=np.int64)
+        lib().or_ga_population(self.h, _p(x), _p(y), _p(obj), _p(fit))
+        return x, y, obj, fit
+
+    def history(self):
+        K = self.ctx.K
+        x = np.zeros((self.nisl, K), dtype=np.int8)
+        y = np.zeros((self.nisl, K), dtype=np.int16)
+        obj = np.zeros(self.nisl, dtype=np.int64)
+        fit = np.zeros(self.nisl, dtype=np.int64)
+        lib().or_ga_history(self.h, _p(x), _p(y), _p(obj), _p(fit))
+        return x, y, obj, fit
+
+    def trace(self):
+        tmin = np.zeros(self.generations + 1, dtype=np.int64)
+        tsum = np.zeros(self.generations + 1, dtype=np.int64)
+        lib().or_ga_trace(self.h, _p(tmin), _p(tsum))
+        return tmin, tsum
