@@ -31,6 +31,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define FFS_API __attribute__((visibility("default")))
+#else
+#define FFS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -48,9 +54,9 @@ typedef enum {
 } ffs_status;
 
 /* Message of the last non-OK status on this thread ("" if none). */
-const char *ffs_last_error(void);
+FFS_API const char *ffs_last_error(void);
 /* Library version string. */
-const char *ffs_version(void);
+FFS_API const char *ffs_version(void);
 
 typedef struct ffs_instance ffs_instance;  /* instance data + device copy            */
 typedef struct ffs_state ffs_state;        /* frozen context at RS + staged tables   */
@@ -76,8 +82,8 @@ typedef struct {
 } ffs_instance_desc;
 
 /* Copy host arrays, validate, upload to `cuda_device`. */
-ffs_status ffs_instance_create(const ffs_instance_desc *d, int cuda_device, ffs_instance **out);
-void ffs_instance_destroy(ffs_instance *inst);
+FFS_API ffs_status ffs_instance_create(const ffs_instance_desc *d, int cuda_device, ffs_instance **out);
+FFS_API void ffs_instance_destroy(ffs_instance *inst);
 
 /* ------------------------------------------------------------------------
  * Freeze at the rescheduling point RS (Algorithm 1 frozen branch,
@@ -94,23 +100,23 @@ void ffs_instance_destroy(ffs_instance *inst);
  * (job-major, stage-minor); ffs_state_genes reports it.
  * Errors: FFS_ERR_INVALID_SCHEDULE if the plan violates Eqs. (4)-(7).
  * ---------------------------------------------------------------------- */
-ffs_status ffs_reschedule_state(const ffs_instance *inst, int32_t rs, const int32_t *orig_assign,
+FFS_API ffs_status ffs_reschedule_state(const ffs_instance *inst, int32_t rs, const int32_t *orig_assign,
                                 const int32_t *orig_start, ffs_state **out, int32_t *K_out);
 /* Host [K] arrays: job and stage of each gene (either may be NULL). */
-ffs_status ffs_state_genes(const ffs_state *st, int32_t *gene_job, int32_t *gene_stage);
+FFS_API ffs_status ffs_state_genes(const ffs_state *st, int32_t *gene_job, int32_t *gene_stage);
 /* Host [(n+n')*g]: 0 pending, 1 running, 2 completed. */
-ffs_status ffs_state_cells(const ffs_state *st, int32_t *cell_state);
+FFS_API ffs_status ffs_state_cells(const ffs_state *st, int32_t *cell_state);
 /* Number of cells with row-major position < p, for p in [0, (n+n')*g]:
  * the compact cut of a row-major crossover point (R13).  Host [cells+1]. */
-ffs_status ffs_state_cut_table(const ffs_state *st, int32_t *pending_before);
+FFS_API ffs_status ffs_state_cut_table(const ffs_state *st, int32_t *pending_before);
 /* Horizon capacity (time slots) of the in-SMEM power profile.  A chromosome
  * whose schedule outgrows it is re-decoded by the global-memory overflow
  * path with identical results.  cap <= 0 restores the automatic choice.
  * (Testing/tuning knob.) */
-ffs_status ffs_state_set_horizon_cap(ffs_state *st, int32_t cap);
-ffs_status ffs_state_info(const ffs_state *st, int32_t *K, int32_t *cells, int32_t *horizon_cap,
+FFS_API ffs_status ffs_state_set_horizon_cap(ffs_state *st, int32_t cap);
+FFS_API ffs_status ffs_state_info(const ffs_state *st, int32_t *K, int32_t *cells, int32_t *horizon_cap,
                           int32_t *horizon_bound, int32_t *smem_bytes_per_cta);
-void ffs_state_destroy(ffs_state *st);
+FFS_API void ffs_state_destroy(ffs_state *st);
 
 /* ------------------------------------------------------------------------
  * Decode + evaluate (Algorithm 1; Algorithm 2, P:273-289;
@@ -124,18 +130,18 @@ void ffs_state_destroy(ffs_state *st);
  *   start_out:       device int32 [count*(n+n')*g], S_js of the merged schedule
  *                    (frozen ops keep their plan start)           (may be NULL)
  * ---------------------------------------------------------------------- */
-ffs_status ffs_evaluate(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
+FFS_API ffs_status ffs_evaluate(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
                         int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                         int32_t *start_out, void *cuda_stream);
 /* Same with HOST buffers (pageable or pinned): copies in, evaluates, copies
  * out, synchronises.  Used for end-to-end timing. */
-ffs_status ffs_evaluate_host(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
+FFS_API ffs_status ffs_evaluate_host(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
                              int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                              void *cuda_stream);
 /* Counter-based random chromosomes (the GA's initialisation operator,
  * P:227): chromosome id -> island id>>20, individual id&(2^20-1); device
  * x [count*K], y [count*K]. */
-ffs_status ffs_random_population(const ffs_state *st, int64_t count, uint64_t seed, int64_t first_id,
+FFS_API ffs_status ffs_random_population(const ffs_state *st, int64_t count, uint64_t seed, int64_t first_id,
                                  int8_t *x, int16_t *y, void *cuda_stream);
 
 /* ------------------------------------------------------------------------
@@ -169,28 +175,28 @@ typedef struct {
 
 /* Generation 0: initialise, evaluate, E_max (global via the
  * allreduce hook, R23), fitness (Eq. (13)), per-island history elite. */
-ffs_status ffs_evolve_begin(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
+FFS_API ffs_status ffs_evolve_begin(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
 /* Run `generations` more generations (selection, crossover + correction,
  * mutation, evaluation, elitist replacement, ring migration every
  * migration_interval, trace).  Asynchronous except around hook calls. */
-ffs_status ffs_evolve_step(ffs_run *run, int32_t generations);
+FFS_API ffs_status ffs_evolve_step(ffs_run *run, int32_t generations);
 /* begin + step(cfg->generations) + synchronise.  K == 0: returns a run whose
  * best is the frozen plan and whose trace is empty. */
-ffs_status ffs_evolve(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
+FFS_API ffs_status ffs_evolve(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
 /* Best-in-history of this shard (ties -> lowest island) and its decoded,
  * merged schedule.  Host outputs, any may be NULL:
  *   x [K], y [K], assign/start [(n+n')*g], trace_min/trace_sum [G+1] (local
  *   shard: min objective and sum of objectives per generation). */
-ffs_status ffs_best(ffs_run *run, int8_t *x, int16_t *y, int32_t *assign, int32_t *start,
+FFS_API ffs_status ffs_best(ffs_run *run, int8_t *x, int16_t *y, int32_t *assign, int32_t *start,
                     int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                     int64_t *trace_min, int64_t *trace_sum);
 /* Host copies of the shard population (cells_local*K genes), its
  * objective/fitness, the per-island history elites, E_max and generation. */
-ffs_status ffs_run_population(ffs_run *run, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness);
-ffs_status ffs_run_history(ffs_run *run, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness);
-ffs_status ffs_run_info(const ffs_run *run, int32_t *generation, int64_t *emax, int64_t *evaluations,
+FFS_API ffs_status ffs_run_population(ffs_run *run, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness);
+FFS_API ffs_status ffs_run_history(ffs_run *run, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness);
+FFS_API ffs_status ffs_run_info(const ffs_run *run, int32_t *generation, int64_t *emax, int64_t *evaluations,
                         int32_t *kernel_launches);
-void ffs_run_destroy(ffs_run *run);
+FFS_API void ffs_run_destroy(ffs_run *run);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,472 @@
+// evaluate.cu -- population-wide decode + evaluate on sm_100a.
+//
+// One warp per chromosome (persistent grid, chromosomes strided over warps).
+// Per CTA: the frozen rescheduling state ("image": P/Q table, gene table,
+// machine-free and job-ready times, initial power profile, due dates) is
+// staged into shared memory once with cp.async.bulk (TMA) + mbarrier.
+// Per warp (shared memory):
+//   ord[K]   rank-ordered (gene | machine << 16)      -- Algorithm 1
+//   cnt[K]   per-priority segment counts / rank starts (aliased with below)
+//   level[h] integer power profile Q_t, one slot per tick after RS (Eq. (8))
+//   ready[NJ], mfree[G*O]
+// Algorithm 1 (greedy reading R1) is evaluated as a stable sort
+// by (prefix-min of y over the job's pending stages desc, stage asc):
+// segmented warp scans + a counting sort, O(K/32) warp steps.
+// Algorithm 2 is evaluated as "earliest power-feasible start
+// >= t0" (R5): a 32-slot window of the profile is tested with one ballot,
+// runs of p feasible slots are found with shifts/ands on the ballot mask.
+#include <climits>
+
+#include "ffs_common.cuh"
+
+namespace edffs {
+namespace {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Stage the state image global -> shared with the bulk-copy engine (TMA).
+__device__ __forceinline__ void stage_image(unsigned char *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(dst + off)),
+          "l"((const char *)src + off), "r"(n), "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// bit i of the result is set iff bits i .. i+p-1 of b are all set (p <= 32,
+// bits above 31 count as clear)
+__device__ __forceinline__ uint32_t runs_ge(uint32_t b, int p) {
+  int k = 1;
+  while (2 * k <= p) {
+    b &= b >> k;
+    k <<= 1;
+  }
+  if (k < p) b &= b >> (p - k);
+  return b;
+}
+
+template <typename LVL>
+struct WarpMem {
+  uint32_t *ord;
+  uint32_t *lbits;
+  uint16_t *cnt;
+  LVL *level;
+  int32_t *ready;
+  int32_t *mfree;
+};
+
+// per-warp region layout (must match State::build_image's size computation)
+template <typename LVL>
+__device__ __forceinline__ WarpMem<LVL> carve(unsigned char *base, const ImageHdr &h, bool level_in_smem,
+                                              int32_t hcap) {
+  auto r16 = [](uint32_t v) { return (v + 15u) & ~15u; };
+  WarpMem<LVL> w;
+  uint32_t K = (uint32_t)h.K, nt = (K + 31u) / 32u;
+  w.ord = (uint32_t *)base;
+  base += r16(4u * K);
+  w.lbits = (uint32_t *)base;
+  base += r16(4u * nt);
+  w.cnt = (uint16_t *)base;  // union U
+  unsigned char *u = base;
+  if (level_in_smem) {
+    w.level = (LVL *)u;
+    u += r16((uint32_t)hcap * sizeof(LVL));
+  } else {
+    w.level = nullptr;
+  }
+  w.ready = (int32_t *)u;
+  u += r16(4u * (uint32_t)h.NJ);
+  w.mfree = (int32_t *)u;
+  return w;
+}
+
+// Segmented inclusive min-scan over the 32 lanes (segments start at `head`),
+// continued from `carry` when no head precedes the lane in this tile.
+__device__ __forceinline__ int seg_min_scan(int v, bool head, int carry, int lane) {
+  uint32_t f = head;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int vn = __shfl_up_sync(FULL, v, d);
+    uint32_t fn = __shfl_up_sync(FULL, f, d);
+    if (lane >= d) {
+      if (!f) v = min(v, vn);
+      f |= fn;
+    }
+  }
+  if (!f) v = min(v, carry);
+  return v;
+}
+
+// Algorithm 1 for one chromosome: fills w.ord[0..K) with (gene | x << 16)
+// in rank order.
+template <typename LVL>
+__device__ __forceinline__ void build_order(const ImageHdr &h, const unsigned char *img, WarpMem<LVL> &w,
+                                            const int8_t *__restrict__ xr, const int16_t *__restrict__ yr,
+                                            int lane) {
+  const int K = h.K, nt = (K + 31) >> 5;
+  const uint32_t *head = (const uint32_t *)(img + h.off_head);
+  // Pass A: pm(g) = min y over the job's pending stages <= s; leaders are the
+  // genes with pm(g) == y(g) (new prefix minima: the eligible op with the
+  // largest y among its job's remaining ops starts a run).
+  int carry = INT_MAX;
+  for (int t = 0; t < nt; ++t) {
+    int g = (t << 5) + lane;
+    bool valid = g < K;
+    int yv = valid ? (int)__ldg(yr + g) : INT_MAX;
+    bool hd = !valid || ((head[t] >> lane) & 1u);
+    int pm = seg_min_scan(yv, hd, carry, lane);
+    uint32_t lb = __ballot_sync(FULL, valid && pm == yv);
+    if (lane == 0) w.lbits[t] = lb;
+    carry = __shfl_sync(FULL, pm, 31);
+  }
+  __syncwarp();
+  // Pass B: cnt[y(l) - 1] = length of leader l's run (genes until the next
+  // leader in gene order); 0 for non-leaders.  y is a permutation of 1..K,
+  // so every slot is written exactly once.
+  for (int t = 0; t < nt; ++t) {
+    int g = (t << 5) + lane;
+    if (g < K) {
+      int yv = (int)__ldg(yr + g);
+      uint32_t lb = w.lbits[t];
+      int cv = 0;
+      if ((lb >> lane) & 1u) {
+        uint32_t m = lane == 31 ? 0u : (lb & (FULL << (lane + 1)));
+        int tt = t;
+        while (m == 0u && ++tt < nt) m = w.lbits[tt];
+        int next = m == 0u ? K : (tt << 5) + __ffs(m) - 1;
+        cv = next - g;
+      }
+      unsigned yi = (unsigned)(yv - 1);
+      if (yi < (unsigned)K) w.cnt[yi] = (uint16_t)cv;
+    }
+  }
+  __syncwarp();
+  // Pass C: exclusive suffix sum over priorities: cnt[v] <- #genes with pm > v+1
+  int acc = 0;
+  for (int t = 0; t < nt; ++t) {
+    int v = K - 1 - ((t << 5) + lane);
+    bool valid = v >= 0;
+    int cv = valid ? (int)w.cnt[v] : 0;
+    int incl = cv;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int n = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += n;
+    }
+    if (valid) w.cnt[v] = (uint16_t)(acc + incl - cv);
+    acc += __shfl_sync(FULL, incl, 31);
+  }
+  __syncwarp();
+  // Pass D: rank(g) = start[pm(g)] + (g - leader(g)); scatter.
+  carry = INT_MAX;
+  int carry_lp = -1;
+  for (int t = 0; t < nt; ++t) {
+    int g = (t << 5) + lane;
+    bool valid = g < K;
+    int yv = valid ? (int)__ldg(yr + g) : INT_MAX;
+    int xv = valid ? (int)__ldg(xr + g) : 0;
+    bool hd = !valid || ((head[t] >> lane) & 1u);
+    int pm = seg_min_scan(yv, hd, carry, lane);
+    int lp = ((w.lbits[t] >> lane) & 1u) ? g : -1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int n = __shfl_up_sync(FULL, lp, d);
+      if (lane >= d) lp = max(lp, n);
+    }
+    lp = max(lp, carry_lp);
+    if (valid) {
+      unsigned pi = (unsigned)(pm - 1);
+      int rank = (pi < (unsigned)K ? (int)w.cnt[pi] : 0) + (g - lp);
+      if ((unsigned)rank < (unsigned)K) w.ord[rank] = (uint32_t)g | ((uint32_t)(xv & 0xFF) << 16);
+    }
+    carry = __shfl_sync(FULL, pm, 31);
+    carry_lp = __shfl_sync(FULL, lp, 31);
+  }
+  __syncwarp();
+}
+
+// Algorithm 2 for one chromosome.  Returns false when the schedule outgrows
+// the profile capacity (the chromosome is then re-decoded by the overflow
+// path).  Times are relative to RS.
+template <typename LVL, bool SCHED>
+__device__ __forceinline__ bool decode(const ImageHdr &h, const unsigned char *img, WarpMem<LVL> &w,
+                                       int32_t hcap, int lane, int32_t *__restrict__ start_row) {
+  const int K = h.K, G = h.G, O = h.O, NJ = h.NJ, qmax = h.q_max;
+  const uint32_t *pq = (const uint32_t *)(img + h.off_pq);
+  const uint32_t *ginfo = (const uint32_t *)(img + h.off_ginfo);
+  // initial profile (RUNNING ops, R3), ready and machine-free times
+  {
+    const uint32_t *l0 = (const uint32_t *)(img + h.off_lvl0);
+    uint32_t *lw = (uint32_t *)w.level;
+    int words = (int)(((int64_t)hcap * (int64_t)sizeof(LVL)) >> 2);
+    for (int i = lane; i < words; i += 32) lw[i] = i < h.lvl_words0 ? l0[i] : 0u;
+    const int32_t *r0 = (const int32_t *)(img + h.off_ready0);
+    const int32_t *m0 = (const int32_t *)(img + h.off_mfree0);
+    for (int i = lane; i < NJ; i += 32) w.ready[i] = r0[i];
+    for (int i = lane; i < G * O; i += 32) w.mfree[i] = m0[i];
+  }
+  __syncwarp();
+  for (int r = 0; r < K; ++r) {
+    uint32_t e = w.ord[r];
+    int g = (int)(e & 0xFFFFu);
+    int m = (int)((e >> 16) & 0xFFu);
+    m = m < O ? m : O - 1;                       // unvalidated input: stay in bounds
+    uint32_t gi = ginfo[g < K ? g : 0];
+    int j = (int)(gi & 0xFFFFu), s = (int)(gi >> 16);
+    uint32_t pqv = pq[(j * G + s) * O + m];
+    int p = (int)(pqv & 0xFFFFu), q = (int)(pqv >> 16);
+    int mi = s * O + m;
+    // t0 = max(RS, release / predecessor completion, machine free) (Eqs. (4),
+    // (5), (10); append-only machine sequencing R6)
+    int t0 = max(w.ready[j], w.mfree[mi]);
+    int thr = qmax - q;
+    // earliest t >= t0 with Q_tau + q <= Q_max for all tau in [t, t+p) (R2, R5)
+    int c = t0, run = 0, S;
+    for (;;) {
+      int idx = c + lane;
+      int lv = idx < hcap ? (int)w.level[idx] : 0;
+      uint32_t b = __ballot_sync(FULL, lv <= thr);
+      int first0 = __clz(__brev(~b));
+      if (run + first0 >= p) {
+        S = c - run;
+        break;
+      }
+      if (p <= 32) {
+        uint32_t f = runs_ge(b, p);
+        if (f) {
+          S = c + __ffs(f) - 1;
+          break;
+        }
+      }
+      run = b == FULL ? run + 32 : __clz(~b);
+      c += 32;
+    }
+    int C = S + p;
+    if (C > hcap) return false;
+    for (int k = lane; k < p; k += 32) w.level[S + k] = (LVL)(w.level[S + k] + q);
+    w.ready[j] = C;  // every lane stores the same value: no cross-lane hazard
+    w.mfree[mi] = C;
+    if (SCHED && lane == 0) start_row[j * G + s] = S + h.rs;
+    __syncwarp();
+  }
+  return true;
+}
+
+template <typename LVL, bool SCHED, bool FALLBACK>
+__global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t img_bytes = ((const ImageHdr *)a.image)->image_bytes;
+  stage_image(smem, a.image, img_bytes, &bar);
+  const ImageHdr &h = *(const ImageHdr *)smem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  WarpMem<LVL> w = carve<LVL>(smem + img_bytes + (size_t)warp * a.per_warp_bytes, h, !FALLBACK, a.h_cap);
+  if (FALLBACK) w.level = (LVL *)a.lvl_global + (size_t)gw * (size_t)a.h_cap;
+  const int64_t count = FALLBACK ? (int64_t)a.ovf[0] : a.count;
+  const int K = h.K;
+  for (int64_t i = gw; i < count; i += nw) {
+    const int64_t c = FALLBACK ? (int64_t)a.ovf[1 + i] : i;
+    const int8_t *xr = a.x + c * K;
+    const int16_t *yr = a.y + c * K;
+    int32_t *srow = SCHED ? a.start_out + c * h.cells : nullptr;
+    if (SCHED)
+      for (int k = lane; k < h.cells; k += 32) srow[k] = a.fstart[k];
+    build_order<LVL>(h, smem, w, xr, yr, lane);
+    bool ok = decode<LVL, SCHED>(h, smem, w, a.h_cap, lane, srow);
+    if (!ok) {
+      if (lane == 0) {
+        int pos = atomicAdd(&a.ovf[0], 1);
+        a.ovf[1 + pos] = (int32_t)c;
+      }
+      __syncwarp();
+      continue;
+    }
+    // Eqs. (1)-(3) over every job (R9): frozen jobs are constants of the state
+    int64_t T = 0;
+    int cm = h.frozen_cmax;
+    const int32_t *pj = (const int32_t *)(smem + h.off_pjob);
+    const int32_t *pd = (const int32_t *)(smem + h.off_pdue);
+    for (int k = lane; k < h.n_pjobs; k += 32) {
+      int Cr = w.ready[pj[k]];
+      int tj = Cr - pd[k];
+      if (tj > 0) T += tj;
+      cm = max(cm, Cr + h.rs);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      T += __shfl_xor_sync(FULL, T, d);
+      cm = max(cm, __shfl_xor_sync(FULL, cm, d));
+    }
+    T += h.frozen_T;
+    if (lane == 0) {
+      int64_t obj = h.wt * T + (int64_t)cm;
+      if (a.obj) a.obj[c] = obj;
+      if (a.tard) a.tard[c] = T;
+      if (a.cmax) a.cmax[c] = cm;
+      if (a.fit) {                                 // Eq. (13)
+        int64_t f = *a.emax - obj;
+        a.fit[c] = f > 0 ? f : 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Counter-based random chromosomes: x ~ U{0..o-1}, y = 1 + rank of a random
+// key (ties by gene index).  Warp per chromosome; keys in shared memory.
+__global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32_t O, int64_t count,
+                                                                uint64_t seed, int64_t first_id,
+                                                                int8_t *x, int16_t *y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *keys = (uint32_t *)smem + (size_t)warp * K;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < count; c += nw) {
+    const int64_t id = first_id + c;
+    const uint32_t island = (uint32_t)(id >> 20), indiv = (uint32_t)(id & 0xFFFFF);
+    for (int g = lane; g < K; g += 32) {
+      u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
+      u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
+      x[c * K + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
+      keys[g] = word_of(ry, g & 3);
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < K; g0 += 128) {
+      uint32_t mk[4];
+      int rk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int gg = g0 + lane + 32 * u;
+        mk[u] = gg < K ? keys[gg] : 0u;
+        rk[u] = 0;
+      }
+      for (int hh = 0; hh < K; ++hh) {
+        uint32_t kh = keys[hh];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int gg = g0 + lane + 32 * u;
+          rk[u] += (kh < mk[u]) | ((kh == mk[u]) & (hh < gg));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int gg = g0 + lane + 32 * u;
+        if (gg < K) y[c * K + gg] = (int16_t)(rk[u] + 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename LVL, bool SCHED, bool FB>
+ffs_status set_smem_attr(size_t bytes) {
+  static size_t done = 0;
+  if (bytes > done) {
+    FFS_CUDA(cudaFuncSetAttribute(evaluate_kernel<LVL, SCHED, FB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done = bytes;
+  }
+  return FFS_OK;
+}
+
+template <typename LVL, bool SCHED>
+ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cudaStream_t s,
+                        int *launches) {
+  EvalArgs a = a0;
+  a.ovf = scr.list;
+  FFS_CUDA(cudaMemsetAsync(scr.list, 0, sizeof(int32_t), s));
+  if (a.count > 0) {
+    int64_t need_ctas = (a.count + st.warps_per_cta - 1) / st.warps_per_cta;
+    int64_t grid = (int64_t)st.num_sms * st.ctas_per_sm;
+    if (need_ctas < grid) grid = need_ctas;
+    a.h_cap = st.h_cap;
+    a.per_warp_bytes = (int32_t)st.per_warp_bytes;
+    ffs_status e = set_smem_attr<LVL, SCHED, false>(st.smem_bytes);
+    if (e != FFS_OK) return e;
+    evaluate_kernel<LVL, SCHED, false><<<(unsigned)grid, st.warps_per_cta * 32, st.smem_bytes, s>>>(a);
+    FFS_CUDA(cudaGetLastError());
+    if (launches) ++*launches;
+  }
+  if (st.h_cap < st.h_bound && a.count > 0) {
+    // overflow path: global-memory profile of full horizon
+    a.h_cap = st.h_bound;
+    a.per_warp_bytes = (int32_t)st.fb_per_warp_bytes;
+    a.lvl_global = scr.level;
+    ffs_status e = set_smem_attr<LVL, SCHED, true>(st.fb_smem_bytes);
+    if (e != FFS_OK) return e;
+    evaluate_kernel<LVL, SCHED, true><<<(unsigned)st.num_sms, st.fb_warps_per_cta * 32, st.fb_smem_bytes, s>>>(a);
+    FFS_CUDA(cudaGetLastError());
+    if (launches) ++*launches;
+  }
+  return FFS_OK;
+}
+
+}  // namespace
+
+ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
+                           int *launches) {
+  int64_t fb_warps = (int64_t)st.num_sms * st.fb_warps_per_cta;
+  ffs_status e = scr.ensure(a.count, st.h_cap < st.h_bound ? fb_warps * st.h_bound * st.lvl_bytes : 0);
+  if (e != FFS_OK) return e;
+  const bool sched = a.start_out != nullptr;
+  if (st.lvl_bytes == 1)
+    return sched ? launch_typed<uint8_t, true>(st, a, scr, s, launches)
+                 : launch_typed<uint8_t, false>(st, a, scr, s, launches);
+  return sched ? launch_typed<uint16_t, true>(st, a, scr, s, launches)
+               : launch_typed<uint16_t, false>(st, a, scr, s, launches);
+}
+
+ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id,
+                                    int8_t *x, int16_t *y, cudaStream_t s) {
+  if (count <= 0 || st.K == 0) return FFS_OK;
+  const int warps = 8;
+  size_t smem = (size_t)warps * st.K * sizeof(uint32_t);
+  if (smem > (size_t)kSmemLimit) return fail(FFS_ERR_INVALID_ARG, "K too large for random_population");
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    FFS_CUDA(cudaFuncSetAttribute(random_population_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = smem;
+  }
+  int64_t grid = (count + warps - 1) / warps;
+  int64_t cap = (int64_t)st.num_sms * 8;
+  if (grid > cap) grid = cap;
+  random_population_kernel<<<(unsigned)grid, warps * 32, smem, s>>>(st.K, st.inst->o, count, seed, first_id,
+                                                                    x, y);
+  FFS_CUDA(cudaGetLastError());
+  return FFS_OK;
+}
+
+}  // namespace edffs

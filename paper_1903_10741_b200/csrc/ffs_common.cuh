@@ -1,0 +1,154 @@
+// ffs_common.cuh -- shared device/host definitions of the sm_100a library.
+// Product code: independent of oracle/ (no shared code, tables or helpers).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ffs.h"
+
+namespace edffs {
+
+// ---------------------------------------------------------------------------
+// Error plumbing (thread-local last error, status returns only)
+// ---------------------------------------------------------------------------
+void set_error(const std::string &msg);
+ffs_status fail(ffs_status st, const std::string &msg);
+ffs_status cuda_fail(cudaError_t e, const char *what);
+#define FFS_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return ::edffs::cuda_fail(_e, #call); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Host-side objects behind the opaque handles
+// ---------------------------------------------------------------------------
+constexpr int kMaxWarpsPerCta = 32;
+constexpr int kSmemLimit = 227 * 1024;
+
+// The device state "image": one 16-byte aligned blob in global memory that
+// every CTA stages into shared memory with cp.async.bulk (TMA) in its
+// prologue.  Header followed by the arrays at the recorded offsets.
+struct ImageHdr {
+  int32_t K, NJ, G, O;
+  int32_t rs, q_max;
+  int32_t n_pjobs, lvl_words0;   // jobs with pending ops; 32-bit words of the initial profile
+  int64_t wt;
+  int64_t frozen_T;              // sum of T_j over jobs with no pending op (Eq. (2))
+  int32_t frozen_cmax;           // max completion over those jobs (Eq. (3))
+  int32_t cells;
+  uint32_t off_pq;               // u32 [NJ*G*O]  p | q << 16
+  uint32_t off_ginfo;            // u32 [K]       j | s << 16
+  uint32_t off_head;             // u32 [ceil(K/32)] first pending gene of each job
+  uint32_t off_ready0;           // i32 [NJ]      earliest start of the job's next op, rel. to RS
+  uint32_t off_mfree0;           // i32 [G*O]     machine free time, rel. to RS
+  uint32_t off_lvl0;             // u32 [lvl_words0] initial power profile (RUNNING ops), LVL-typed
+  uint32_t off_pjob;             // i32 [n_pjobs] job index
+  uint32_t off_pdue;             // i32 [n_pjobs] D_j - RS
+  uint32_t image_bytes;          // multiple of 16
+  uint32_t pad_;
+};
+
+struct Instance {
+  int dev = 0;
+  int32_t n = 0, np = 0, g = 0, o = 0, NJ = 0;
+  int32_t q_max = 0;
+  int64_t wt = 0;
+  std::vector<int32_t> P, Q, R, D;   // host copies [NJ*g*o], [NJ]
+};
+
+// Scratch of the overflow path (chromosomes whose schedule outgrows the
+// in-SMEM profile are re-decoded with a global-memory profile).
+struct OvfScratch {
+  int32_t *list = nullptr;       // [1 + cap]: count, then chromosome ids
+  int64_t cap = 0;
+  void *level = nullptr;         // [fallback warps * hfull * sizeof(LVL)]
+  int64_t level_bytes = 0;
+  ffs_status ensure(int64_t count, int64_t level_bytes_needed);
+  void release();
+};
+
+struct State {
+  const Instance *inst = nullptr;
+  int32_t rs = 0, K = 0, cells = 0;
+  std::vector<int32_t> cell_state;   // 0 pending, 1 running, 2 completed
+  std::vector<int32_t> fassign, fstart;
+  std::vector<int32_t> gene_job, gene_stage, gene_cell;
+  std::vector<int32_t> pend_before;  // [cells+1]
+  int32_t h_bound = 0;               // slots needed for any schedule (rel. to RS)
+  int32_t h_cap = 0;                 // slots of the in-SMEM profile
+  int32_t h_cap_user = 0;
+  int lvl_bytes = 1;                 // 1: u8 profile (Q_max <= 255), 2: u16
+  std::vector<uint8_t> image_host;   // built for the current h_cap
+  void *image_dev = nullptr;
+  int32_t *fstart_dev = nullptr;     // [cells] frozen starts (abs), -1 pending
+  int32_t *cut_dev = nullptr;        // [cells+1] pend_before on device
+  // launch geometry of the evaluate kernel
+  int warps_per_cta = 0, ctas_per_sm = 0, num_sms = 0;
+  size_t smem_bytes = 0, per_warp_bytes = 0;
+  size_t fb_smem_bytes = 0, fb_per_warp_bytes = 0;
+  int fb_warps_per_cta = 4;
+  OvfScratch scratch;
+  ffs_status build_image();
+};
+
+// Arguments of one evaluate launch (device pointers).
+struct EvalArgs {
+  const void *image;
+  int64_t count;
+  const int8_t *x;
+  const int16_t *y;
+  int64_t *obj;
+  int64_t *tard;
+  int32_t *cmax;
+  int32_t *start_out;            // optional full schedule
+  const int32_t *fstart;         // frozen starts for start_out
+  const int64_t *emax;           // optional: fitness = max(*emax - obj, 0)
+  int64_t *fit;
+  int32_t *ovf;                  // overflow list (count at [0])
+  void *lvl_global;              // fallback: global profiles
+  int32_t h_cap;                 // slots in the profile used by this launch
+  int32_t per_warp_bytes;
+};
+
+ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
+                           int *launches);
+ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id,
+                                    int8_t *x, int16_t *y, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (device), DESIGN.md "RNG"
+// ---------------------------------------------------------------------------
+struct u32x4 { uint32_t x, y, z, w; };
+__host__ __device__ __forceinline__ u32x4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                  uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+#else
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return {c0, c1, c2, c3};
+}
+enum : uint32_t { RNG_INIT_X = 1, RNG_INIT_Y = 2, RNG_XO = 3, RNG_MUT = 4, RNG_MUT_X = 5 };
+__host__ __device__ __forceinline__ uint32_t word_of(const u32x4 &v, int w) {
+  return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+__host__ __device__ __forceinline__ uint32_t bounded(uint32_t u, uint32_t n) {
+  return (uint32_t)(((uint64_t)u * n) >> 32);
+}
+
+}  // namespace edffs
+
+struct ffs_instance { edffs::Instance v; };
+struct ffs_state { edffs::State v; };

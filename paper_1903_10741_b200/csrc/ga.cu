@@ -1,0 +1,774 @@
+// ga.cu -- island GA of one rescheduling point on sm_100a.
+//
+// Population: global island I owns cells I*tile + i (i row-major in the
+// island tile, tile = island_w * island_h); SoA device buffers x int8[cell][K],
+// y int16[cell][K], obj/fit int64[cell], double-buffered across generations
+// (synchronous update from the previous generation's snapshot, R18).
+// Per generation (operator order R20):
+//   generation_kernel  warp per horizontal pair: asteroid selection,
+//                      neighbouring paired crossover + correction,
+//                      mutation                     -> next buffer
+//   evaluate           decode + objective + fitness (Eq. (13))
+//   replace_kernel     CTA per island: elitist replacement
+//   donor/import       ring migration every migration_interval,
+//                      allgather hook across processes
+//   trace_kernel       min objective and sum of objectives
+// Random draws: Philox4x32-10 keyed by the seed, counter
+// (purpose << 24 | block, individual, generation, island) -- DESIGN.md "RNG".
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "ffs_common.cuh"
+
+namespace edffs {
+
+struct Run {
+  State *st = nullptr;
+  ffs_ga_config cfg{};
+  cudaStream_t s = nullptr;
+  int tile = 0, nisl = 0, K = 0, cells = 0;
+  int64_t nloc = 0;
+  int gen = -1;
+  int cur = 0;
+  int8_t *x[2] = {nullptr, nullptr};
+  int16_t *y[2] = {nullptr, nullptr};
+  int64_t *obj[2] = {nullptr, nullptr};
+  int64_t *fit[2] = {nullptr, nullptr};
+  int8_t *hx = nullptr;
+  int16_t *hy = nullptr;
+  int64_t *hobj = nullptr, *hfit = nullptr;
+  int32_t *worst_idx = nullptr;
+  unsigned char *donor = nullptr, *recv = nullptr;
+  size_t rec = 0;
+  int64_t *scal = nullptr;          // [0] emax, [1] max objective
+  int64_t *tmin = nullptr, *tsum = nullptr;
+  OvfScratch scr;
+  int64_t evaluations = 0;
+  int launches = 0;
+  std::vector<void *> allocs;
+  ~Run() {
+    for (void *p : allocs) cudaFree(p);
+    scr.release();
+  }
+  template <typename T>
+  ffs_status alloc(T **p, size_t n) {
+    void *q = nullptr;
+    FFS_CUDA(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)));
+    allocs.push_back(q);
+    *p = (T *)q;
+    return FFS_OK;
+  }
+};
+
+namespace {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+
+// ---- initialisation: x ~ U{0..o-1}, y = 1 + rank of a random key
+__global__ void __launch_bounds__(256) init_kernel(int32_t K, int32_t O, int64_t count, int32_t tile,
+                                                   int32_t island0, uint64_t seed, int8_t *x, int16_t *y) {
+  extern __shared__ __align__(16) uint32_t keys_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *keys = keys_all + (size_t)warp * K;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < count; c += nw) {
+    const uint32_t island = (uint32_t)(island0 + c / tile), indiv = (uint32_t)(c % tile);
+    for (int g = lane; g < K; g += 32) {
+      u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
+      u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
+      x[c * K + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
+      keys[g] = word_of(ry, g & 3);
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < K; g0 += 128) {
+      uint32_t mk[4];
+      int rk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int gg = g0 + lane + 32 * u;
+        mk[u] = gg < K ? keys[gg] : 0u;
+        rk[u] = 0;
+      }
+      for (int hh = 0; hh < K; ++hh) {
+        uint32_t kh = keys[hh];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rk[u] += (kh < mk[u]) | ((kh == mk[u]) & (hh < g0 + lane + 32 * u));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int gg = g0 + lane + 32 * u;
+        if (gg < K) y[c * K + gg] = (int16_t)(rk[u] + 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- E_max = 10^a, a >= 1, smallest with every initial objective < E_max
+__global__ void max_kernel(const int64_t *obj, int64_t n, int64_t *out) {
+  __shared__ long long sm[32];
+  long long m = LLONG_MIN;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = max(m, (long long)obj[i]);
+  for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(FULL, m, d));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : LLONG_MIN;
+    for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(FULL, m, d));
+    if (threadIdx.x == 0) *out = m;
+  }
+}
+
+__global__ void emax_fitness_kernel(int64_t *scal, const int64_t *obj, int64_t *fit, int64_t n) {
+  int64_t mx = scal[1];
+  int64_t E = 10;
+  while (E <= mx) E *= 10;
+  if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = E;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = E - obj[i];
+    fit[i] = f > 0 ? f : 0;                       // Eq. (13)
+  }
+}
+
+// ---- block helpers: argmax / argmin of fitness inside one island (ties -> lowest index)
+__device__ __forceinline__ void better_max(int64_t &f, int &i, int64_t f2, int i2) {
+  if (f2 > f || (f2 == f && i2 < i)) { f = f2; i = i2; }
+}
+__device__ __forceinline__ void better_min(int64_t &f, int &i, int64_t f2, int i2) {
+  if (f2 < f || (f2 == f && i2 < i)) { f = f2; i = i2; }
+}
+__device__ void island_best_worst(const int64_t *fit, int tile, int &best, int &worst) {
+  __shared__ long long sfb[32], sfw[32];
+  __shared__ int sib[32], siw[32];
+  int64_t fb = LLONG_MIN, fw = LLONG_MAX;
+  int ib = INT_MAX, iw = INT_MAX;
+  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+    better_max(fb, ib, fit[i], i);
+    better_min(fw, iw, fit[i], i);
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    better_max(fb, ib, __shfl_xor_sync(FULL, fb, d), __shfl_xor_sync(FULL, ib, d));
+    better_min(fw, iw, __shfl_xor_sync(FULL, fw, d), __shfl_xor_sync(FULL, iw, d));
+  }
+  int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sfb[w] = fb; sib[w] = ib; sfw[w] = fw; siw[w] = iw; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int nw = blockDim.x >> 5;
+    fb = threadIdx.x < nw ? sfb[threadIdx.x] : LLONG_MIN;
+    ib = threadIdx.x < nw ? sib[threadIdx.x] : INT_MAX;
+    fw = threadIdx.x < nw ? sfw[threadIdx.x] : LLONG_MAX;
+    iw = threadIdx.x < nw ? siw[threadIdx.x] : INT_MAX;
+    for (int d = 16; d > 0; d >>= 1) {
+      better_max(fb, ib, __shfl_xor_sync(FULL, fb, d), __shfl_xor_sync(FULL, ib, d));
+      better_min(fw, iw, __shfl_xor_sync(FULL, fw, d), __shfl_xor_sync(FULL, iw, d));
+    }
+    if (threadIdx.x == 0) { sib[0] = ib; siw[0] = iw; }
+  }
+  __syncthreads();
+  best = sib[0];
+  worst = siw[0];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void copy_bytes(unsigned char *dst, const unsigned char *src, size_t n) {
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// history elite record per island; generation 0 sets it unconditionally
+__global__ void history_init_kernel(int K, int tile, const int8_t *x, const int16_t *y, const int64_t *obj,
+                                    const int64_t *fit, int8_t *hx, int16_t *hy, int64_t *hobj, int64_t *hfit) {
+  const int li = blockIdx.x;
+  const int64_t base = (int64_t)li * tile;
+  int b, w;
+  island_best_worst(fit + base, tile, b, w);
+  const int64_t c = base + b;
+  copy_bytes((unsigned char *)(hx + (int64_t)li * K), (const unsigned char *)(x + c * K), (size_t)K);
+  copy_bytes((unsigned char *)(hy + (int64_t)li * K), (const unsigned char *)(y + c * K), (size_t)K * 2);
+  if (threadIdx.x == 0) { hobj[li] = obj[c]; hfit[li] = fit[c]; }
+}
+
+// elitist replacement (R21): strict improvement updates the history;
+// the island's worst cell is overwritten by the history elite.
+__global__ void replace_kernel(int K, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
+                               int16_t *hy, int64_t *hobj, int64_t *hfit) {
+  const int li = blockIdx.x;
+  const int64_t base = (int64_t)li * tile;
+  int b, w;
+  island_best_worst(fit + base, tile, b, w);
+  const int64_t cb = base + b, cw = base + w;
+  int8_t *hxr = hx + (int64_t)li * K;
+  int16_t *hyr = hy + (int64_t)li * K;
+  const bool upd = fit[cb] > hfit[li];
+  __syncthreads();
+  if (upd) {
+    copy_bytes((unsigned char *)hxr, (const unsigned char *)(x + cb * K), (size_t)K);
+    copy_bytes((unsigned char *)hyr, (const unsigned char *)(y + cb * K), (size_t)K * 2);
+    if (threadIdx.x == 0) { hobj[li] = obj[cb]; hfit[li] = fit[cb]; }
+  }
+  __syncthreads();
+  copy_bytes((unsigned char *)(x + cw * K), (const unsigned char *)hxr, (size_t)K);
+  copy_bytes((unsigned char *)(y + cw * K), (const unsigned char *)hyr, (size_t)K * 2);
+  if (threadIdx.x == 0) { obj[cw] = hobj[li]; fit[cw] = hfit[li]; }
+}
+
+// ring migration, part 1: snapshot every island's best (after replacement)
+// and remember its worst cell (R22)
+__global__ void donor_kernel(int K, int tile, size_t rec, const int8_t *x, const int16_t *y, const int64_t *obj,
+                             const int64_t *fit, unsigned char *donor, int32_t *worst_idx) {
+  const int li = blockIdx.x;
+  const int64_t base = (int64_t)li * tile;
+  int b, w;
+  island_best_worst(fit + base, tile, b, w);
+  const int64_t cb = base + b;
+  unsigned char *d = donor + (size_t)li * rec;
+  copy_bytes(d, (const unsigned char *)(x + cb * K), (size_t)K);
+  copy_bytes(d + K, (const unsigned char *)(y + cb * K), (size_t)K * 2);
+  if (threadIdx.x == 0) {
+    int64_t o = obj[cb], f = fit[cb];
+    memcpy(d + 3 * (size_t)K, &o, 8);
+    memcpy(d + 3 * (size_t)K + 8, &f, 8);
+    worst_idx[li] = (int32_t)(base + w);
+  }
+}
+
+// part 2: island li's worst cell <- best of island li-1; island 0 of the shard
+// <- `incoming` (the last island of the previous shard, or of this shard)
+__global__ void import_kernel(int K, size_t rec, const unsigned char *donor, const unsigned char *incoming,
+                              const int32_t *worst_idx, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+  const int li = blockIdx.x;
+  const unsigned char *src = li == 0 ? incoming : donor + (size_t)(li - 1) * rec;
+  const int64_t cw = worst_idx[li];
+  copy_bytes((unsigned char *)(x + cw * K), src, (size_t)K);
+  copy_bytes((unsigned char *)(y + cw * K), src + K, (size_t)K * 2);
+  if (threadIdx.x == 0) {
+    int64_t o, f;
+    memcpy(&o, src + 3 * (size_t)K, 8);
+    memcpy(&f, src + 3 * (size_t)K + 8, 8);
+    obj[cw] = o;
+    fit[cw] = f;
+  }
+}
+
+__global__ void trace_kernel(const int64_t *obj, int64_t n, int64_t *tmin, int64_t *tsum, int k) {
+  __shared__ long long smin[32];
+  __shared__ long long ssum[32];
+  long long mn = LLONG_MAX, sm = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    mn = min(mn, (long long)obj[i]);
+    sm += obj[i];
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+    sm += __shfl_xor_sync(FULL, sm, d);
+  }
+  if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = mn; ssum[threadIdx.x >> 5] = sm; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int nw = blockDim.x >> 5;
+    mn = threadIdx.x < nw ? smin[threadIdx.x] : LLONG_MAX;
+    sm = threadIdx.x < nw ? ssum[threadIdx.x] : 0;
+    for (int d = 16; d > 0; d >>= 1) {
+      mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+      sm += __shfl_xor_sync(FULL, sm, d);
+    }
+    if (threadIdx.x == 0) { tmin[k] = mn; tsum[k] = sm; }
+  }
+}
+
+// ---- one generation's breeding for one horizontal pair (a, b = a + 1)
+struct GenArgs {
+  int32_t K, O, cells, w, h, tile, island0, k;
+  uint32_t xo_thr, mut_thr;
+  uint64_t seed;
+  int64_t npairs;
+  const int32_t *cut;                          // pending cells before row-major position p
+  const int8_t *xp; const int16_t *yp; const int64_t *fp;   // previous generation
+  int8_t *xn; int16_t *yn;                     // next generation
+};
+
+__device__ __forceinline__ void argmax5(int lane, int sub, const int64_t *fitI, int cell, int w, int h,
+                                        int &winner) {
+  // lanes sub*16 + k, k < 5: candidate k of `cell` in the order self, N, S, E, W
+  int row = cell / w, col = cell % w;
+  int k = lane - sub * 16;
+  int nb = cell;
+  if (k == 1) nb = ((row + h - 1) % h) * w + col;
+  else if (k == 2) nb = ((row + 1) % h) * w + col;
+  else if (k == 3) nb = row * w + (col + 1) % w;
+  else if (k == 4) nb = row * w + (col + w - 1) % w;
+  long long f = (k >= 0 && k < 5) ? (long long)fitI[nb] : -1;  // fitness >= 0
+  int kk = (k >= 0 && k < 5) ? k : 99;
+#pragma unroll
+  for (int d = 8; d > 0; d >>= 1) {
+    long long f2 = __shfl_xor_sync(FULL, f, d);
+    int k2 = __shfl_xor_sync(FULL, kk, d);
+    int nb2 = __shfl_xor_sync(FULL, nb, d);
+    if (f2 > f || (f2 == f && k2 < kk)) { f = f2; kk = k2; nb = nb2; }
+  }
+  winner = __shfl_sync(FULL, nb, sub * 16);
+}
+
+__global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.K, nwd = (K + 31) >> 5;
+  const size_t per_warp = (size_t)2 * nwd * 4 + (size_t)2 * ((K * 2 + 15) & ~15);
+  uint32_t *PA = (uint32_t *)(gsm + warp * per_warp);
+  uint32_t *PB = PA + nwd;
+  uint16_t *LA = (uint16_t *)(PB + nwd);
+  uint16_t *LB = LA + ((K * 2 + 15) & ~15) / 2;
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int half = a.tile >> 1, wh = a.w >> 1;
+  for (int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; pi < a.npairs; pi += nw) {
+    const int64_t li = pi / half;
+    const int pr = (int)(pi % half);
+    const int ca = (pr / wh) * a.w + 2 * (pr % wh), cb = ca + 1;
+    const uint32_t I = (uint32_t)(a.island0 + li), kg = (uint32_t)a.k;
+    const int64_t base = li * a.tile;
+    // a6: asteroid selection on the previous generation's fitness
+    int wa, wb;
+    argmax5(lane, 0, a.fp + base, ca, a.w, a.h, wa);
+    argmax5(lane, 1, a.fp + base, cb, a.w, a.h, wb);
+    const int8_t *XA = a.xp + (base + wa) * K, *XB = a.xp + (base + wb) * K;
+    const int16_t *YA = a.yp + (base + wa) * K, *YB = a.yp + (base + wb) * K;
+    int8_t *xa = a.xn + (base + ca) * K, *xb = a.xn + (base + cb) * K;
+    int16_t *ya = a.yn + (base + ca) * K, *yb = a.yn + (base + cb) * K;
+    // a7: crossover fires with p_c; one row-major cut shared by X and Y (R13)
+    u32x4 rxo = philox((RNG_XO << 24), (uint32_t)ca, kg, I, k0, k1);
+    int kc = K;
+    if (rxo.x < a.xo_thr) {
+      int p = 1 + (int)bounded(rxo.y, (uint32_t)(a.cells - 1));
+      kc = a.cut[p];
+    }
+    // a8 draws for both children
+    u32x4 rma = philox((RNG_MUT << 24), (uint32_t)ca, kg, I, k0, k1);
+    u32x4 rmb = philox((RNG_MUT << 24), (uint32_t)cb, kg, I, k0, k1);
+    const bool ma = rma.x < a.mut_thr, mb = rmb.x < a.mut_thr;
+    const bool repair = kc > 0 && kc < K;
+    if (repair) {
+      // correction (R14): duplicates of child a are the suffix genes of B
+      // whose value occurs in A's prefix; missing values = in B's prefix, not
+      // in A's prefix; assigned in ascending order to duplicates in gene order.
+      for (int i = lane; i < nwd; i += 32) { PA[i] = 0u; PB[i] = 0u; }
+      __syncwarp();
+      for (int g = lane; g < kc; g += 32) {
+        int va = YA[g] - 1, vb = YB[g] - 1;
+        if ((unsigned)va < (unsigned)K) atomicOr(&PA[va >> 5], 1u << (va & 31));
+        if ((unsigned)vb < (unsigned)K) atomicOr(&PB[vb >> 5], 1u << (vb & 31));
+      }
+      __syncwarp();
+      int offa = 0, offb = 0;
+      for (int i0 = 0; i0 < nwd; i0 += 32) {
+        int i = i0 + lane;
+        uint32_t wa_ = i < nwd ? (PB[i] & ~PA[i]) : 0u;
+        uint32_t wb_ = i < nwd ? (PA[i] & ~PB[i]) : 0u;
+        int na = __popc(wa_), nb = __popc(wb_);
+        int ia = na, ib = nb;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          int t1 = __shfl_up_sync(FULL, ia, d), t2 = __shfl_up_sync(FULL, ib, d);
+          if (lane >= d) { ia += t1; ib += t2; }
+        }
+        int pa = offa + ia - na, pb = offb + ib - nb;
+        while (wa_) { int bit = __ffs(wa_) - 1; wa_ &= wa_ - 1; LA[pa++] = (uint16_t)(i * 32 + bit + 1); }
+        while (wb_) { int bit = __ffs(wb_) - 1; wb_ &= wb_ - 1; LB[pb++] = (uint16_t)(i * 32 + bit + 1); }
+        offa += __shfl_sync(FULL, ia, 31);
+        offb += __shfl_sync(FULL, ib, 31);
+      }
+      __syncwarp();
+    }
+    // write children: prefix from own parent, suffix from the other (corrected)
+    int da = 0, db = 0;  // duplicates seen so far (gene order)
+    const int o1 = a.O - 1;
+    for (int g0 = 0; g0 < K; g0 += 32) {
+      int g = g0 + lane;
+      bool v = g < K;
+      bool pre = g < kc;
+      int xav = 0, xbv = 0, yav = 0, ybv = 0;
+      bool dupa = false, dupb = false;
+      if (v) {
+        xav = pre ? XA[g] : XB[g];
+        xbv = pre ? XB[g] : XA[g];
+        yav = pre ? YA[g] : YB[g];
+        ybv = pre ? YB[g] : YA[g];
+        if (repair && !pre) {
+          int ta = yav - 1, tb = ybv - 1;
+          dupa = (unsigned)ta < (unsigned)K && ((PA[ta >> 5] >> (ta & 31)) & 1u);
+          dupb = (unsigned)tb < (unsigned)K && ((PB[tb >> 5] >> (tb & 31)) & 1u);
+        }
+      }
+      uint32_t ba = __ballot_sync(FULL, dupa), bb = __ballot_sync(FULL, dupb);
+      uint32_t lt = (1u << lane) - 1u;
+      if (dupa) yav = LA[da + __popc(ba & lt)];
+      if (dupb) ybv = LB[db + __popc(bb & lt)];
+      da += __popc(ba);
+      db += __popc(bb);
+      if (v) {
+        // a8: every gene's machine resampled among the other o-1 (R15)
+        if ((ma || mb) && o1 >= 1) {
+          if (ma) {
+            u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)ca, kg, I, k0, k1);
+            xav = (xav + 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1)) % a.O;
+          }
+          if (mb) {
+            u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)cb, kg, I, k0, k1);
+            xbv = (xbv + 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1)) % a.O;
+          }
+        }
+        xa[g] = (int8_t)xav;
+        xb[g] = (int8_t)xbv;
+        ya[g] = (int16_t)yav;
+        yb[g] = (int16_t)ybv;
+      }
+    }
+    __syncwarp();
+    // a8: swap two priorities
+    if (K >= 2 && lane < 2) {
+      const u32x4 &rm = lane == 0 ? rma : rmb;
+      const bool fire = lane == 0 ? ma : mb;
+      int16_t *yy = lane == 0 ? ya : yb;
+      if (fire) {
+        int g1 = (int)bounded(rm.y, (uint32_t)K);
+        int g2 = (int)bounded(rm.z, (uint32_t)(K - 1));
+        g2 += g2 >= g1;
+        int16_t t = yy[g1];
+        yy[g1] = yy[g2];
+        yy[g2] = t;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t gen_smem_per_warp(int K) {
+  int nwd = (K + 31) >> 5;
+  return (size_t)2 * nwd * 4 + (size_t)2 * ((K * 2 + 15) & ~15);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static ffs_status evaluate_population(Run &r, int buf, bool with_fitness) {
+  EvalArgs a{};
+  a.image = r.st->image_dev;
+  a.count = r.nloc;
+  a.x = r.x[buf];
+  a.y = r.y[buf];
+  a.obj = r.obj[buf];
+  a.fstart = r.st->fstart_dev;
+  if (with_fitness) {
+    a.emax = r.scal;
+    a.fit = r.fit[buf];
+  }
+  r.evaluations += r.nloc;
+  return launch_evaluate(*r.st, a, r.scr, r.s, &r.launches);
+}
+
+static ffs_status ga_init(Run &r) {
+  const State &st = *r.st;
+  const int warps = 8;
+  size_t smem = (size_t)warps * r.K * 4;
+  if (smem > (size_t)kSmemLimit) return fail(FFS_ERR_INVALID_ARG, "K too large for initialisation");
+  FFS_CUDA(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t grid = std::min<int64_t>((r.nloc + warps - 1) / warps, (int64_t)st.num_sms * 8);
+  init_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(r.K, st.inst->o, r.nloc, r.tile, r.cfg.island_begin,
+                                                         r.cfg.seed, r.x[0], r.y[0]);
+  FFS_CUDA(cudaGetLastError());
+  r.launches++;
+  ffs_status e = evaluate_population(r, 0, false);
+  if (e != FFS_OK) return e;
+  max_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.scal + 1);
+  FFS_CUDA(cudaGetLastError());
+  r.launches++;
+  if (r.cfg.allreduce_max_i64 && r.cfg.world > 1) {
+    // E_max over the global initial population (R23)
+    if (r.cfg.allreduce_max_i64(r.cfg.user, r.scal + 1, (void *)r.s) != 0)
+      return fail(FFS_ERR_COMM, "allreduce_max_i64 hook failed");
+  }
+  emax_fitness_kernel<<<(unsigned)std::min<int64_t>((r.nloc + 255) / 256, 1024), 256, 0, r.s>>>(
+      r.scal, r.obj[0], r.fit[0], r.nloc);
+  FFS_CUDA(cudaGetLastError());
+  history_init_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.x[0], r.y[0], r.obj[0], r.fit[0], r.hx, r.hy, r.hobj,
+                                               r.hfit);
+  FFS_CUDA(cudaGetLastError());
+  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.tmin, r.tsum, 0);
+  FFS_CUDA(cudaGetLastError());
+  r.launches += 3;
+  r.cur = 0;
+  r.gen = 0;
+  return FFS_OK;
+}
+
+static ffs_status ga_generation(Run &r) {
+  const State &st = *r.st;
+  const int k = r.gen + 1;
+  const int nb = 1 - r.cur;
+  GenArgs g{};
+  g.K = r.K; g.O = st.inst->o; g.cells = st.cells; g.w = r.cfg.island_w; g.h = r.cfg.island_h;
+  g.tile = r.tile; g.island0 = r.cfg.island_begin; g.k = k;
+  g.xo_thr = r.cfg.xo_threshold; g.mut_thr = r.cfg.mut_threshold; g.seed = r.cfg.seed;
+  g.npairs = r.nloc / 2;
+  g.cut = st.cut_dev;
+  g.xp = r.x[r.cur]; g.yp = r.y[r.cur]; g.fp = r.fit[r.cur];
+  g.xn = r.x[nb]; g.yn = r.y[nb];
+  const int warps = 8;
+  size_t smem = (size_t)warps * gen_smem_per_warp(r.K);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    FFS_CUDA(cudaFuncSetAttribute(generation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int64_t grid = std::min<int64_t>((g.npairs + warps - 1) / warps, (int64_t)st.num_sms * 8);
+  generation_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(g);
+  FFS_CUDA(cudaGetLastError());
+  r.launches++;
+  ffs_status e = evaluate_population(r, nb, true);
+  if (e != FFS_OK) return e;
+  replace_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.hx, r.hy, r.hobj,
+                                          r.hfit);
+  FFS_CUDA(cudaGetLastError());
+  r.launches++;
+  if (k % r.cfg.migration_interval == 0 && r.cfg.islands_total >= 2) {
+    donor_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.rec, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.donor,
+                                          r.worst_idx);
+    FFS_CUDA(cudaGetLastError());
+    r.launches++;
+    const unsigned char *incoming = r.donor + (size_t)(r.nisl - 1) * r.rec;
+    if (r.cfg.world > 1) {
+      if (!r.cfg.allgather) return fail(FFS_ERR_INVALID_ARG, "world > 1 needs the allgather hook");
+      if (r.cfg.allgather(r.cfg.user, r.donor + (size_t)(r.nisl - 1) * r.rec, r.recv, r.rec, (void *)r.s) != 0)
+        return fail(FFS_ERR_COMM, "allgather hook failed");
+      incoming = r.recv + (size_t)((r.cfg.rank + r.cfg.world - 1) % r.cfg.world) * r.rec;
+    }
+    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.rec, r.donor, incoming, r.worst_idx, r.x[nb], r.y[nb], r.obj[nb],
+                                           r.fit[nb]);
+    FFS_CUDA(cudaGetLastError());
+    r.launches++;
+  }
+  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[nb], r.nloc, r.tmin, r.tsum, k);
+  FFS_CUDA(cudaGetLastError());
+  r.launches++;
+  r.cur = nb;
+  r.gen = k;
+  return FFS_OK;
+}
+
+}  // namespace edffs
+
+struct ffs_run { edffs::Run v; };
+
+using namespace edffs;
+
+extern "C" {
+
+ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *stream, ffs_run **out) {
+  if (!sh || !cfg || !out) return fail(FFS_ERR_INVALID_ARG, "null argument");
+  if (cfg->island_w < 2 || (cfg->island_w & 1) || cfg->island_h < 1)
+    return fail(FFS_ERR_INVALID_ARG, "island_w must be even and >= 2, island_h >= 1");
+  if ((int64_t)cfg->island_w * cfg->island_h > (1 << 20)) return fail(FFS_ERR_INVALID_ARG, "island tile > 2^20 cells");
+  if (cfg->islands_total < 1 || cfg->island_begin < 0 || cfg->island_end > cfg->islands_total ||
+      cfg->island_begin >= cfg->island_end)
+    return fail(FFS_ERR_INVALID_ARG, "bad island shard");
+  if (cfg->generations < 0 || cfg->migration_interval < 1) return fail(FFS_ERR_INVALID_ARG, "bad generations");
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail(FFS_ERR_INVALID_ARG, "bad rank/world");
+  State &st = sh->v;
+  cudaSetDevice(st.inst->dev);
+  ffs_run *h = new ffs_run();
+  Run &r = h->v;
+  r.st = &st;
+  r.cfg = *cfg;
+  r.s = (cudaStream_t)stream;
+  r.tile = cfg->island_w * cfg->island_h;
+  r.nisl = cfg->island_end - cfg->island_begin;
+  r.nloc = (int64_t)r.nisl * r.tile;
+  r.K = st.K;
+  r.cells = st.cells;
+  r.rec = ((size_t)3 * r.K + 16 + 15) & ~(size_t)15;
+  const size_t genes = (size_t)r.nloc * std::max(r.K, 1);
+  ffs_status e = FFS_OK;
+  for (int b = 0; b < 2 && e == FFS_OK; ++b) {
+    if (e == FFS_OK) e = r.alloc(&r.x[b], genes);
+    if (e == FFS_OK) e = r.alloc(&r.y[b], genes);
+    if (e == FFS_OK) e = r.alloc(&r.obj[b], (size_t)r.nloc);
+    if (e == FFS_OK) e = r.alloc(&r.fit[b], (size_t)r.nloc);
+  }
+  if (e == FFS_OK) e = r.alloc(&r.hx, (size_t)r.nisl * std::max(r.K, 1));
+  if (e == FFS_OK) e = r.alloc(&r.hy, (size_t)r.nisl * std::max(r.K, 1));
+  if (e == FFS_OK) e = r.alloc(&r.hobj, (size_t)r.nisl);
+  if (e == FFS_OK) e = r.alloc(&r.hfit, (size_t)r.nisl);
+  if (e == FFS_OK) e = r.alloc(&r.worst_idx, (size_t)r.nisl);
+  if (e == FFS_OK) e = r.alloc(&r.donor, (size_t)r.nisl * r.rec);
+  if (e == FFS_OK) e = r.alloc(&r.recv, (size_t)cfg->world * r.rec);
+  if (e == FFS_OK) e = r.alloc(&r.scal, 2);
+  if (e == FFS_OK) e = r.alloc(&r.tmin, (size_t)cfg->generations + 1);
+  if (e == FFS_OK) e = r.alloc(&r.tsum, (size_t)cfg->generations + 1);
+  if (e == FFS_OK && r.K > 0) e = ga_init(r);
+  if (e != FFS_OK) {
+    delete h;
+    return e;
+  }
+  *out = h;
+  return FFS_OK;
+}
+
+ffs_status ffs_evolve_step(ffs_run *h, int32_t generations) {
+  if (!h || generations < 0) return fail(FFS_ERR_INVALID_ARG, "bad arguments");
+  Run &r = h->v;
+  if (r.K == 0) return FFS_OK;
+  if (r.gen + generations > r.cfg.generations)
+    return fail(FFS_ERR_INVALID_ARG, "more generations than configured");
+  cudaSetDevice(r.st->inst->dev);
+  for (int i = 0; i < generations; ++i) {
+    ffs_status e = ga_generation(r);
+    if (e != FFS_OK) return e;
+  }
+  return FFS_OK;
+}
+
+ffs_status ffs_evolve(ffs_state *sh, const ffs_ga_config *cfg, void *stream, ffs_run **out) {
+  ffs_run *h = nullptr;
+  ffs_status e = ffs_evolve_begin(sh, cfg, stream, &h);
+  if (e != FFS_OK) return e;
+  e = ffs_evolve_step(h, cfg->generations);
+  if (e == FFS_OK) {
+    cudaError_t ce = cudaStreamSynchronize((cudaStream_t)stream);
+    if (ce != cudaSuccess) e = cuda_fail(ce, "ffs_evolve sync");
+  }
+  if (e != FFS_OK) {
+    ffs_run_destroy(h);
+    return e;
+  }
+  *out = h;
+  return FFS_OK;
+}
+
+ffs_status ffs_best(ffs_run *h, int8_t *x, int16_t *y, int32_t *assign, int32_t *start, int64_t *objective,
+                    int64_t *total_tardiness, int32_t *makespan, int64_t *trace_min, int64_t *trace_sum) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
+  Run &r = h->v;
+  State &st = *r.st;
+  cudaSetDevice(st.inst->dev);
+  FFS_CUDA(cudaStreamSynchronize(r.s));
+  const int K = r.K;
+  std::vector<int8_t> bx(std::max(K, 1), 0);
+  std::vector<int16_t> by(std::max(K, 1), 1);
+  if (K > 0) {
+    std::vector<int64_t> hf(r.nisl);
+    FFS_CUDA(cudaMemcpy(hf.data(), r.hfit, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
+    int b = 0;
+    for (int i = 1; i < r.nisl; ++i)
+      if (hf[i] > hf[b]) b = i;  // ties -> lowest island
+    FFS_CUDA(cudaMemcpy(bx.data(), r.hx + (size_t)b * K, (size_t)K, cudaMemcpyDeviceToHost));
+    FFS_CUDA(cudaMemcpy(by.data(), r.hy + (size_t)b * K, (size_t)K * 2, cudaMemcpyDeviceToHost));
+  }
+  // decode the elite once more to emit its schedule
+  int8_t *dx = nullptr;
+  int16_t *dy = nullptr;
+  int64_t *dv = nullptr;
+  int32_t *di = nullptr;
+  FFS_CUDA(cudaMalloc(&dx, bx.size()));
+  FFS_CUDA(cudaMalloc(&dy, by.size() * 2));
+  FFS_CUDA(cudaMalloc(&dv, 16));
+  FFS_CUDA(cudaMalloc(&di, (size_t)(st.cells + 1) * 4));
+  cudaMemcpy(dx, bx.data(), bx.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dy, by.data(), by.size() * 2, cudaMemcpyHostToDevice);
+  EvalArgs a{};
+  a.image = st.image_dev;
+  a.count = 1;
+  a.x = dx;
+  a.y = dy;
+  a.obj = dv;
+  a.tard = dv + 1;
+  a.cmax = di + st.cells;
+  a.start_out = di;
+  a.fstart = st.fstart_dev;
+  ffs_status e = launch_evaluate(st, a, r.scr, r.s, nullptr);
+  std::vector<int32_t> hs(st.cells + 1);
+  int64_t hv[2] = {0, 0};
+  if (e == FFS_OK) {
+    cudaError_t ce = cudaMemcpyAsync(hs.data(), di, (size_t)(st.cells + 1) * 4, cudaMemcpyDeviceToHost, r.s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(hv, dv, 16, cudaMemcpyDeviceToHost, r.s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(r.s);
+    if (ce != cudaSuccess) e = cuda_fail(ce, "ffs_best copy-out");
+  }
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(dv);
+  cudaFree(di);
+  if (e != FFS_OK) return e;
+  if (x && K) std::memcpy(x, bx.data(), (size_t)K);
+  if (y && K) std::memcpy(y, by.data(), (size_t)K * 2);
+  if (start) std::memcpy(start, hs.data(), (size_t)st.cells * 4);
+  if (assign) {
+    for (int c = 0; c < st.cells; ++c) assign[c] = st.fassign[c];
+    for (int k = 0; k < K; ++k) assign[st.gene_cell[k]] = bx[k];
+  }
+  if (objective) *objective = hv[0];
+  if (total_tardiness) *total_tardiness = hv[1];
+  if (makespan) *makespan = hs[st.cells];
+  if (K > 0 && r.gen >= 0) {
+    if (trace_min) FFS_CUDA(cudaMemcpy(trace_min, r.tmin, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost));
+    if (trace_sum) FFS_CUDA(cudaMemcpy(trace_sum, r.tsum, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost));
+  }
+  return FFS_OK;
+}
+
+ffs_status ffs_run_population(ffs_run *h, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
+  Run &r = h->v;
+  cudaSetDevice(r.st->inst->dev);
+  FFS_CUDA(cudaStreamSynchronize(r.s));
+  if (r.K == 0) return FFS_OK;
+  const size_t genes = (size_t)r.nloc * r.K;
+  if (x) FFS_CUDA(cudaMemcpy(x, r.x[r.cur], genes, cudaMemcpyDeviceToHost));
+  if (y) FFS_CUDA(cudaMemcpy(y, r.y[r.cur], genes * 2, cudaMemcpyDeviceToHost));
+  if (objective) FFS_CUDA(cudaMemcpy(objective, r.obj[r.cur], (size_t)r.nloc * 8, cudaMemcpyDeviceToHost));
+  if (fitness) FFS_CUDA(cudaMemcpy(fitness, r.fit[r.cur], (size_t)r.nloc * 8, cudaMemcpyDeviceToHost));
+  return FFS_OK;
+}
+
+ffs_status ffs_run_history(ffs_run *h, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
+  Run &r = h->v;
+  cudaSetDevice(r.st->inst->dev);
+  FFS_CUDA(cudaStreamSynchronize(r.s));
+  if (r.K == 0) return FFS_OK;
+  if (x) FFS_CUDA(cudaMemcpy(x, r.hx, (size_t)r.nisl * r.K, cudaMemcpyDeviceToHost));
+  if (y) FFS_CUDA(cudaMemcpy(y, r.hy, (size_t)r.nisl * r.K * 2, cudaMemcpyDeviceToHost));
+  if (objective) FFS_CUDA(cudaMemcpy(objective, r.hobj, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
+  if (fitness) FFS_CUDA(cudaMemcpy(fitness, r.hfit, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
+  return FFS_OK;
+}
+
+ffs_status ffs_run_info(const ffs_run *h, int32_t *generation, int64_t *emax, int64_t *evaluations,
+                        int32_t *kernel_launches) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
+  const Run &r = h->v;
+  if (generation) *generation = r.gen;
+  if (emax) {
+    *emax = 0;
+    if (r.K > 0) {
+      cudaStreamSynchronize(r.s);
+      FFS_CUDA(cudaMemcpy(emax, r.scal, 8, cudaMemcpyDeviceToHost));
+    }
+  }
+  if (evaluations) *evaluations = r.evaluations;
+  if (kernel_launches) *kernel_launches = r.launches;
+  return FFS_OK;
+}
+
+void ffs_run_destroy(ffs_run *h) {
+  if (!h) return;
+  cudaSetDevice(h->v.st->inst->dev);
+  cudaStreamSynchronize(h->v.s);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+// state.cu -- instance creation and the freeze at RS (host), device image.
+//
+// Freeze (Algorithm 1 frozen branch): an original op with plan
+// (M, S, C = S + P_jsM) is RUNNING iff S < RS < C, COMPLETED iff C <= RS,
+// else PENDING (reading R7); every op of a new job is PENDING.  RUNNING ops
+// keep their machine busy and draw power until C (R3).
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "ffs_common.cuh"
+
+namespace edffs {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+ffs_status fail(ffs_status st, const std::string &msg) {
+  set_error(msg);
+  return st;
+}
+ffs_status cuda_fail(cudaError_t e, const char *what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? FFS_ERR_OOM : FFS_ERR_CUDA;
+}
+
+ffs_status OvfScratch::ensure(int64_t count, int64_t level_bytes_needed) {
+  if (count + 1 > cap) {
+    if (list) cudaFree(list);
+    list = nullptr;
+    int64_t c = std::max<int64_t>(count + 1, 1024);
+    FFS_CUDA(cudaMalloc(&list, (size_t)c * sizeof(int32_t)));
+    cap = c;
+  }
+  if (level_bytes_needed > level_bytes) {
+    if (level) cudaFree(level);
+    level = nullptr;
+    FFS_CUDA(cudaMalloc(&level, (size_t)level_bytes_needed));
+    level_bytes = level_bytes_needed;
+  }
+  return FFS_OK;
+}
+
+void OvfScratch::release() {
+  if (list) cudaFree(list);
+  if (level) cudaFree(level);
+  list = nullptr;
+  level = nullptr;
+  cap = 0;
+  level_bytes = 0;
+}
+
+static uint32_t r16(uint64_t v) { return (uint32_t)((v + 15) & ~(uint64_t)15); }
+
+// Build the staged image for the current h_cap and choose launch geometry.
+ffs_status State::build_image() {
+  const Instance &in = *inst;
+  const int NJ = in.NJ, G = in.g, O = in.o;
+  // --- per-job pending info
+  std::vector<int32_t> first_pending(NJ, G);
+  for (int j = 0; j < NJ; ++j)
+    for (int s = 0; s < G; ++s)
+      if (cell_state[j * G + s] == 0) {
+        first_pending[j] = s;
+        break;
+      }
+  auto Pof = [&](int j, int s, int m) { return in.P[((size_t)j * G + s) * O + m]; };
+  auto Qof = [&](int j, int s, int m) { return in.Q[((size_t)j * G + s) * O + m]; };
+  auto comp = [&](int j, int s) {  // completion of a frozen op (plan)
+    int cell = j * G + s;
+    return (int64_t)fstart[cell] + Pof(j, s, fassign[cell]);
+  };
+  std::vector<int32_t> ready0(NJ, 0), mfree0((size_t)G * O, 0);
+  std::vector<int32_t> pjob, pdue;
+  int64_t frozen_T = 0;
+  int64_t frozen_cmax = 0;
+  int64_t base = 0;
+  for (int j = 0; j < NJ; ++j) {
+    int s0 = first_pending[j];
+    if (s0 < G) {
+      // earliest start of the job's first pending op: Eq. (10) RS, Eq. (4) R_j or
+      // Eq. (5) completion of the frozen predecessor (R8)
+      int64_t t = s0 == 0 ? (int64_t)in.R[j] : comp(j, s0 - 1);
+      t = std::max<int64_t>(t, rs);
+      ready0[j] = (int32_t)(t - rs);
+      base = std::max<int64_t>(base, t - rs);
+      pjob.push_back(j);
+      pdue.push_back((int32_t)((int64_t)in.D[j] - rs));
+    } else {
+      int64_t Cj = comp(j, G - 1);  // Eqs. (2)-(3) over J u J' (R9)
+      frozen_T += std::max<int64_t>(Cj - in.D[j], 0);
+      frozen_cmax = std::max(frozen_cmax, Cj);
+    }
+  }
+  // machine free times and the initial profile from RUNNING ops
+  int64_t Lr = 0;
+  std::vector<std::pair<int64_t, int32_t>> running;  // (C - RS, q)
+  for (int j = 0; j < NJ; ++j)
+    for (int s = 0; s < G; ++s) {
+      int cell = j * G + s;
+      if (cell_state[cell] != 1) continue;
+      int m = fassign[cell];
+      int64_t Crel = comp(j, s) - rs;
+      mfree0[(size_t)s * O + m] = (int32_t)std::max<int64_t>(mfree0[(size_t)s * O + m], Crel);
+      base = std::max(base, Crel);
+      running.push_back({Crel, Qof(j, s, m)});
+      Lr = std::max(Lr, Crel);
+    }
+  int64_t sum_p = 0;
+  for (int k = 0; k < K; ++k) {
+    int j = gene_job[k], s = gene_stage[k];
+    int mx = 0;
+    for (int m = 0; m < O; ++m) mx = std::max(mx, Pof(j, s, m));
+    sum_p += mx;
+  }
+  // every completion is <= base + sum of the pending ops' longest P
+  int64_t hb = base + sum_p + 1;
+  hb = (hb + 31) / 32 * 32;
+  if (hb >= (int64_t)1 << 30) return fail(FFS_ERR_INVALID_ARG, "time horizon exceeds 2^30 ticks");
+  h_bound = (int32_t)hb;
+
+  // --- image layout
+  const int nt = (K + 31) / 32;
+  uint32_t off = r16(sizeof(ImageHdr));
+  ImageHdr H;
+  std::memset(&H, 0, sizeof(H));
+  H.K = K; H.NJ = NJ; H.G = G; H.O = O; H.rs = rs; H.q_max = in.q_max;
+  H.n_pjobs = (int32_t)pjob.size();
+  H.wt = in.wt; H.frozen_T = frozen_T; H.frozen_cmax = (int32_t)frozen_cmax; H.cells = cells;
+  H.off_pq = off; off += r16((uint64_t)NJ * G * O * 4);
+  H.off_ginfo = off; off += r16((uint64_t)K * 4);
+  H.off_head = off; off += r16((uint64_t)nt * 4);
+  H.off_ready0 = off; off += r16((uint64_t)NJ * 4);
+  H.off_mfree0 = off; off += r16((uint64_t)G * O * 4);
+  int64_t lvl_bytes0 = Lr * lvl_bytes;
+  H.lvl_words0 = (int32_t)((lvl_bytes0 + 3) / 4);
+  H.off_lvl0 = off; off += r16((uint64_t)H.lvl_words0 * 4);
+  H.off_pjob = off; off += r16((uint64_t)pjob.size() * 4);
+  H.off_pdue = off; off += r16((uint64_t)pjob.size() * 4);
+  H.image_bytes = off;
+  image_host.assign(off, 0);
+  uint8_t *img = image_host.data();
+  std::memcpy(img, &H, sizeof(H));
+  uint32_t *pq = (uint32_t *)(img + H.off_pq);
+  for (size_t i = 0; i < (size_t)NJ * G * O; ++i) pq[i] = (uint32_t)in.P[i] | ((uint32_t)in.Q[i] << 16);
+  uint32_t *gi = (uint32_t *)(img + H.off_ginfo);
+  uint32_t *hd = (uint32_t *)(img + H.off_head);
+  for (int k = 0; k < K; ++k) {
+    gi[k] = (uint32_t)gene_job[k] | ((uint32_t)gene_stage[k] << 16);
+    if (k == 0 || gene_job[k - 1] != gene_job[k]) hd[k >> 5] |= 1u << (k & 31);
+  }
+  std::memcpy(img + H.off_ready0, ready0.data(), (size_t)NJ * 4);
+  std::memcpy(img + H.off_mfree0, mfree0.data(), (size_t)G * O * 4);
+  for (int64_t t = 0; t < Lr; ++t) {
+    int64_t L = 0;
+    for (auto &rq : running)
+      if (t < rq.first) L += rq.second;
+    if (lvl_bytes == 1) img[H.off_lvl0 + t] = (uint8_t)L;
+    else ((uint16_t *)(img + H.off_lvl0))[t] = (uint16_t)L;
+  }
+  if (!pjob.empty()) {
+    std::memcpy(img + H.off_pjob, pjob.data(), pjob.size() * 4);
+    std::memcpy(img + H.off_pdue, pdue.data(), pdue.size() * 4);
+  }
+
+  // --- geometry: profile capacity and warps per CTA
+  auto per_warp = [&](int64_t hcap, bool lvl_smem) -> uint64_t {
+    uint64_t u_level = (lvl_smem ? r16((uint64_t)hcap * lvl_bytes) : 0) + r16((uint64_t)NJ * 4) +
+                       r16((uint64_t)G * O * 4);
+    uint64_t u = std::max<uint64_t>(r16((uint64_t)K * 2), u_level);
+    return r16((uint64_t)K * 4) + r16((uint64_t)nt * 4) + u;
+  };
+  const int64_t budget = kSmemLimit - (int64_t)H.image_bytes - 256;
+  if (budget < (int64_t)per_warp(32, true))
+    return fail(FFS_ERR_INVALID_ARG, "instance too large: state image + one warp exceed shared memory");
+  int64_t hcap;
+  if (h_cap_user > 0) {
+    hcap = std::min<int64_t>(((int64_t)h_cap_user + 31) / 32 * 32, h_bound);
+  } else {
+    // largest capacity that keeps 32 resident warps, at least 512 slots, at
+    // most the proven bound h_bound
+    int64_t fixed = (int64_t)per_warp(0, true);
+    int64_t h32 = (budget / kMaxWarpsPerCta - fixed) / lvl_bytes;
+    h32 = h32 / 32 * 32;
+    hcap = std::min<int64_t>(h_bound, std::max<int64_t>(h32, 512));
+  }
+  while (hcap > 32 && (int64_t)per_warp(hcap, true) > budget) hcap -= 32;
+  h_cap = (int32_t)hcap;
+  per_warp_bytes = per_warp(hcap, true);
+  warps_per_cta = (int)std::min<int64_t>(kMaxWarpsPerCta, budget / (int64_t)per_warp_bytes);
+  smem_bytes = H.image_bytes + (size_t)warps_per_cta * per_warp_bytes;
+  fb_per_warp_bytes = per_warp(0, false);
+  fb_warps_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(4, budget / (int64_t)fb_per_warp_bytes));
+  fb_smem_bytes = H.image_bytes + (size_t)fb_warps_per_cta * fb_per_warp_bytes;
+
+  // --- upload
+  cudaSetDevice(in.dev);
+  if (image_dev) cudaFree(image_dev);
+  image_dev = nullptr;
+  FFS_CUDA(cudaMalloc(&image_dev, image_host.size()));
+  FFS_CUDA(cudaMemcpy(image_dev, image_host.data(), image_host.size(), cudaMemcpyHostToDevice));
+  int dev = in.dev;
+  FFS_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  // one CTA of up to 32 warps per SM, or more CTAs if they fit
+  ctas_per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(64 / warps_per_cta,
+                                                           (int64_t)(kSmemLimit + 1024) / (int64_t)(smem_bytes + 1024)));
+  return FFS_OK;
+}
+
+}  // namespace edffs
+
+using namespace edffs;
+
+extern "C" {
+
+const char *ffs_last_error(void) { return g_last_error.c_str(); }
+const char *ffs_version(void) { return "ffs-b200 0.1 (sm_100a)"; }
+
+ffs_status ffs_instance_create(const ffs_instance_desc *d, int cuda_device, ffs_instance **out) {
+  if (!d || !out) return fail(FFS_ERR_INVALID_ARG, "null argument");
+  if (d->n < 0 || d->n_prime < 0 || d->n + d->n_prime < 1 || d->g < 1 || d->o < 1)
+    return fail(FFS_ERR_INVALID_ARG, "sizes: need n, n' >= 0, n + n' >= 1, g >= 1, o >= 1");
+  if (d->n + d->n_prime > 65535 || d->o > 127 || (int64_t)d->g * d->o > 4096)
+    return fail(FFS_ERR_INVALID_ARG, "limits: n + n' <= 65535, o <= 127, g*o <= 4096");
+  if (!d->proc_time || !d->power || !d->release || !d->due) return fail(FFS_ERR_INVALID_ARG, "null array");
+  if (d->wt < 0) return fail(FFS_ERR_INVALID_ARG, "WT must be >= 0");
+  if (d->q_max < 0 || d->q_max > 65535) return fail(FFS_ERR_INVALID_ARG, "Q_max must be in [0, 65535]");
+  const int NJ = d->n + d->n_prime;
+  const size_t tab = (size_t)NJ * d->g * d->o;
+  for (size_t i = 0; i < tab; ++i) {
+    if (d->proc_time[i] < 1 || d->proc_time[i] > 65535)
+      return fail(FFS_ERR_INVALID_ARG, "P_jsm must be in [1, 65535]");
+    if (d->power[i] < 0 || d->power[i] > 65535) return fail(FFS_ERR_INVALID_ARG, "Q_jsm must be in [0, 65535]");
+  }
+  for (int j = 0; j < NJ; ++j)
+    if (d->release[j] < 0 || d->due[j] < d->release[j])
+      return fail(FFS_ERR_INVALID_ARG, "need 0 <= R_j <= D_j");
+  for (size_t i = 0; i < tab; ++i)
+    if (d->power[i] > d->q_max)
+      return fail(FFS_ERR_INFEASIBLE, "some Q_jsm > Q_max: no start satisfies Eq. (7)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+    return fail(FFS_ERR_CUDA, "no such CUDA device");
+  ffs_instance *h = new ffs_instance();
+  Instance &in = h->v;
+  in.dev = cuda_device;
+  in.n = d->n; in.np = d->n_prime; in.g = d->g; in.o = d->o; in.NJ = NJ;
+  in.q_max = d->q_max; in.wt = d->wt;
+  in.P.assign(d->proc_time, d->proc_time + tab);
+  in.Q.assign(d->power, d->power + tab);
+  in.R.assign(d->release, d->release + NJ);
+  in.D.assign(d->due, d->due + NJ);
+  *out = h;
+  return FFS_OK;
+}
+
+void ffs_instance_destroy(ffs_instance *inst) { delete inst; }
+
+ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_t *orig_assign,
+                                const int32_t *orig_start, ffs_state **out, int32_t *K_out) {
+  if (!ih || !out) return fail(FFS_ERR_INVALID_ARG, "null argument");
+  if (rs < 0) return fail(FFS_ERR_INVALID_ARG, "RS must be >= 0");
+  if ((orig_assign == nullptr) != (orig_start == nullptr))
+    return fail(FFS_ERR_INVALID_ARG, "orig_assign and orig_start must both be given or both NULL");
+  const Instance &in = ih->v;
+  const int G = in.g, O = in.o, n = in.n, NJ = in.NJ;
+  auto Pof = [&](int j, int s, int m) { return (int64_t)in.P[((size_t)j * G + s) * O + m]; };
+  auto Qof = [&](int j, int s, int m) { return (int64_t)in.Q[((size_t)j * G + s) * O + m]; };
+  if (orig_assign) {
+    // the plan of the original jobs must satisfy Eqs. (4)-(7)
+    for (int c = 0; c < n * G; ++c)
+      if (orig_assign[c] < 0 || orig_assign[c] >= O || orig_start[c] < 0)
+        return fail(FFS_ERR_INVALID_SCHEDULE, "original plan: machine out of range or negative start");
+    std::vector<std::pair<int64_t, int64_t>> ev;  // per-(s,m) intervals check via sort
+    for (int j = 0; j < n; ++j) {
+      if (orig_start[j * G] < in.R[j]) return fail(FFS_ERR_INVALID_SCHEDULE, "original plan violates Eq. (4)");
+      for (int s = 1; s < G; ++s)
+        if (orig_start[j * G + s] < orig_start[j * G + s - 1] + Pof(j, s - 1, orig_assign[j * G + s - 1]))
+          return fail(FFS_ERR_INVALID_SCHEDULE, "original plan violates Eq. (5)");
+    }
+    for (int s = 0; s < G; ++s)
+      for (int m = 0; m < O; ++m) {
+        std::vector<std::pair<int64_t, int64_t>> iv;
+        for (int j = 0; j < n; ++j)
+          if (orig_assign[j * G + s] == m)
+            iv.push_back({orig_start[j * G + s], orig_start[j * G + s] + Pof(j, s, m)});
+        std::sort(iv.begin(), iv.end());
+        for (size_t k = 1; k < iv.size(); ++k)
+          if (iv[k].first < iv[k - 1].second)
+            return fail(FFS_ERR_INVALID_SCHEDULE, "original plan violates Eq. (6)");
+      }
+    // Eq. (7): sweep of +q at starts, -q at completions (completions first)
+    std::vector<std::pair<int64_t, int64_t>> sweep;
+    for (int j = 0; j < n; ++j)
+      for (int s = 0; s < G; ++s) {
+        int m = orig_assign[j * G + s];
+        int64_t S = orig_start[j * G + s];
+        sweep.push_back({S, Qof(j, s, m)});
+        sweep.push_back({S + Pof(j, s, m), -Qof(j, s, m)});
+      }
+    std::sort(sweep.begin(), sweep.end());
+    int64_t L = 0;
+    for (auto &e : sweep) {
+      L += e.second;
+      if (L > in.q_max) return fail(FFS_ERR_INVALID_SCHEDULE, "original plan violates Eq. (7)");
+    }
+  }
+  ffs_state *h = new ffs_state();
+  State &st = h->v;
+  st.inst = &in;
+  st.rs = rs;
+  st.cells = NJ * G;
+  st.cell_state.assign(st.cells, 0);
+  st.fassign.assign(st.cells, -1);
+  st.fstart.assign(st.cells, -1);
+  int64_t running_q = 0;
+  for (int j = 0; j < n && orig_assign; ++j)
+    for (int s = 0; s < G; ++s) {
+      int c = j * G + s, m = orig_assign[c];
+      int64_t S = orig_start[c], C = S + Pof(j, s, m);
+      int stt = (S < rs && rs < C) ? 1 : (C <= rs ? 2 : 0);
+      st.cell_state[c] = stt;
+      if (stt) {
+        st.fassign[c] = m;
+        st.fstart[c] = (int32_t)S;
+      }
+      if (stt == 1) running_q += Qof(j, s, m);
+    }
+  if (running_q > in.q_max) {
+    delete h;
+    return fail(FFS_ERR_INFEASIBLE, "RUNNING operations at RS exceed Q_max");
+  }
+  st.pend_before.assign(st.cells + 1, 0);
+  for (int c = 0; c < st.cells; ++c) {
+    st.pend_before[c + 1] = st.pend_before[c] + (st.cell_state[c] == 0);
+    if (st.cell_state[c] == 0) {
+      st.gene_cell.push_back(c);
+      st.gene_job.push_back(c / G);
+      st.gene_stage.push_back(c % G);
+    }
+  }
+  st.K = (int32_t)st.gene_cell.size();
+  if (st.K > 32767) {
+    delete h;
+    return fail(FFS_ERR_INVALID_ARG, "K (pending ops) must be <= 32767 (int16 priorities)");
+  }
+  st.lvl_bytes = in.q_max <= 255 ? 1 : 2;
+  cudaSetDevice(in.dev);
+  ffs_status e = st.build_image();
+  if (e != FFS_OK) {
+    delete h;
+    return e;
+  }
+  cudaError_t ce = cudaMalloc(&st.fstart_dev, (size_t)st.cells * 4);
+  if (ce == cudaSuccess) ce = cudaMemcpy(st.fstart_dev, st.fstart.data(), (size_t)st.cells * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMalloc(&st.cut_dev, (size_t)(st.cells + 1) * 4);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(st.cut_dev, st.pend_before.data(), (size_t)(st.cells + 1) * 4, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    ffs_state_destroy(h);
+    return cuda_fail(ce, "state upload");
+  }
+  *out = h;
+  if (K_out) *K_out = st.K;
+  return FFS_OK;
+}
+
+ffs_status ffs_state_genes(const ffs_state *h, int32_t *gene_job, int32_t *gene_stage) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
+  if (gene_job) std::copy(h->v.gene_job.begin(), h->v.gene_job.end(), gene_job);
+  if (gene_stage) std::copy(h->v.gene_stage.begin(), h->v.gene_stage.end(), gene_stage);
+  return FFS_OK;
+}
+
+ffs_status ffs_state_cells(const ffs_state *h, int32_t *cell_state) {
+  if (!h || !cell_state) return fail(FFS_ERR_INVALID_ARG, "null argument");
+  std::copy(h->v.cell_state.begin(), h->v.cell_state.end(), cell_state);
+  return FFS_OK;
+}
+
+ffs_status ffs_state_cut_table(const ffs_state *h, int32_t *pb) {
+  if (!h || !pb) return fail(FFS_ERR_INVALID_ARG, "null argument");
+  std::copy(h->v.pend_before.begin(), h->v.pend_before.end(), pb);
+  return FFS_OK;
+}
+
+ffs_status ffs_state_set_horizon_cap(ffs_state *h, int32_t cap) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
+  h->v.h_cap_user = cap > 0 ? cap : 0;
+  cudaSetDevice(h->v.inst->dev);
+  return h->v.build_image();
+}
+
+ffs_status ffs_state_info(const ffs_state *h, int32_t *K, int32_t *cells, int32_t *hcap, int32_t *hb,
+                          int32_t *smem) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
+  if (K) *K = h->v.K;
+  if (cells) *cells = h->v.cells;
+  if (hcap) *hcap = h->v.h_cap;
+  if (hb) *hb = h->v.h_bound;
+  if (smem) *smem = (int32_t)h->v.smem_bytes;
+  return FFS_OK;
+}
+
+void ffs_state_destroy(ffs_state *h) {
+  if (!h) return;
+  State &st = h->v;
+  if (st.image_dev) cudaFree(st.image_dev);
+  if (st.fstart_dev) cudaFree(st.fstart_dev);
+  if (st.cut_dev) cudaFree(st.cut_dev);
+  st.scratch.release();
+  delete h;
+}
+
+ffs_status ffs_evaluate(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y, int64_t *objective,
+                        int64_t *total_tardiness, int32_t *makespan, int32_t *start_out, void *stream) {
+  if (!h || count < 0) return fail(FFS_ERR_INVALID_ARG, "bad state or count");
+  if (count > 0 && h->v.K > 0 && (!x || !y)) return fail(FFS_ERR_INVALID_ARG, "null chromosome arrays");
+  if (count > ((int64_t)1 << 31) - 2) return fail(FFS_ERR_INVALID_ARG, "count must be < 2^31");
+  State &st = const_cast<State &>(h->v);
+  cudaSetDevice(st.inst->dev);
+  EvalArgs a{};
+  a.image = st.image_dev;
+  a.count = count;
+  a.x = x;
+  a.y = y;
+  a.obj = objective;
+  a.tard = total_tardiness;
+  a.cmax = makespan;
+  a.start_out = start_out;
+  a.fstart = st.fstart_dev;
+  return launch_evaluate(st, a, st.scratch, (cudaStream_t)stream, nullptr);
+}
+
+ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y,
+                             int64_t *objective, int64_t *total_tardiness, int32_t *makespan, void *stream) {
+  if (!h || count < 0) return fail(FFS_ERR_INVALID_ARG, "bad state or count");
+  const State &st = h->v;
+  cudaSetDevice(st.inst->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t gb = (size_t)count * st.K;
+  int8_t *dx = nullptr;
+  int16_t *dy = nullptr;
+  int64_t *dobj = nullptr, *dT = nullptr;
+  int32_t *dM = nullptr;
+  ffs_status rc = FFS_OK;
+  cudaError_t e = cudaMallocAsync(&dx, gb + 1, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dy, gb * 2 + 2, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dobj, (size_t)count * 8 + 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dT, (size_t)count * 8 + 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dM, (size_t)count * 4 + 4, s);
+  if (e == cudaSuccess && gb) e = cudaMemcpyAsync(dx, x, gb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && gb) e = cudaMemcpyAsync(dy, y, gb * 2, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = cuda_fail(e, "evaluate_host staging");
+  if (rc == FFS_OK) rc = ffs_evaluate(h, count, dx, dy, dobj, dT, dM, nullptr, stream);
+  if (rc == FFS_OK) {
+    e = cudaSuccess;
+    if (objective) e = cudaMemcpyAsync(objective, dobj, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && total_tardiness)
+      e = cudaMemcpyAsync(total_tardiness, dT, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && makespan) e = cudaMemcpyAsync(makespan, dM, (size_t)count * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "evaluate_host copy-out");
+  }
+  cudaFreeAsync(dx, s);
+  cudaFreeAsync(dy, s);
+  cudaFreeAsync(dobj, s);
+  cudaFreeAsync(dT, s);
+  cudaFreeAsync(dM, s);
+  e = cudaStreamSynchronize(s);
+  if (rc == FFS_OK && e != cudaSuccess) rc = cuda_fail(e, "evaluate_host sync");
+  return rc;
+}
+
+ffs_status ffs_random_population(const ffs_state *h, int64_t count, uint64_t seed, int64_t first_id, int8_t *x,
+                                 int16_t *y, void *stream) {
+  if (!h || count < 0 || first_id < 0) return fail(FFS_ERR_INVALID_ARG, "bad arguments");
+  if (count > 0 && h->v.K > 0 && (!x || !y)) return fail(FFS_ERR_INVALID_ARG, "null output arrays");
+  cudaSetDevice(h->v.inst->dev);
+  return launch_random_population(h->v, count, seed, first_id, x, y, (cudaStream_t)stream);
+}
+
+}  // extern "C"

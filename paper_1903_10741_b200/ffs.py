@@ -1,0 +1,365 @@
+"""Thin Python binding of the C-ABI (include/ffs.h) -- argument marshalling only.
+
+Every step of the hot path runs in libffs.so's sm_100a kernels.  PyTorch is
+used only for device memory and streams.  There is no fallback: importing
+works without a GPU (for the build check), but every call requires the
+compiled library and a CUDA device and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+OK = 0
+STATUS = {0: "FFS_OK", 1: "FFS_ERR_INVALID_ARG", 2: "FFS_ERR_INFEASIBLE", 3: "FFS_ERR_INVALID_SCHEDULE",
+          4: "FFS_ERR_CUDA", 5: "FFS_ERR_OOM", 6: "FFS_ERR_COMM"}
+
+XO_090 = 3865470566   # floor(0.9 * 2^32), crossover rate of P:395
+MUT_010 = 429496729   # floor(0.1 * 2^32), mutation rate of P:395
+
+# every entry point declared in include/ffs.h
+EXPORTS = [
+    "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
+    "ffs_reschedule_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
+    "ffs_state_set_horizon_cap", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
+    "ffs_evaluate_host", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
+    "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
+    "ffs_run_destroy",
+]
+
+
+class FFSError(RuntimeError):
+    def __init__(self, status, what, msg):
+        super().__init__(f"{what}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Desc(C.Structure):
+    _fields_ = [("n", C.c_int32), ("n_prime", C.c_int32), ("g", C.c_int32), ("o", C.c_int32),
+                ("proc_time", C.POINTER(C.c_int32)), ("power", C.POINTER(C.c_int32)),
+                ("release", C.POINTER(C.c_int32)), ("due", C.POINTER(C.c_int32)),
+                ("q_max", C.c_int32), ("wt", C.c_int64)]
+
+
+ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class GAConfig(C.Structure):
+    _fields_ = [("island_w", C.c_int32), ("island_h", C.c_int32), ("islands_total", C.c_int32),
+                ("island_begin", C.c_int32), ("island_end", C.c_int32),
+                ("xo_threshold", C.c_uint32), ("mut_threshold", C.c_uint32),
+                ("migration_interval", C.c_int32), ("generations", C.c_int32),
+                ("seed", C.c_uint64), ("rank", C.c_int32), ("world", C.c_int32),
+                ("allreduce_max_i64", ALLRED), ("allgather", ALLGATHER), ("user", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libffs.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"{_build.LIB} is missing: the sm_100a library must be built "
+                              "(python -m paper_1903_10741_b200.build); there is no CPU fallback")
+        L = C.CDLL(_build.LIB)
+        P = C.c_void_p
+        sig = {
+            "ffs_last_error": ([], C.c_char_p), "ffs_version": ([], C.c_char_p),
+            "ffs_instance_create": ([C.POINTER(_Desc), C.c_int, P], C.c_int),
+            "ffs_instance_destroy": ([P], None),
+            "ffs_reschedule_state": ([P, C.c_int32, P, P, P, P], C.c_int),
+            "ffs_state_genes": ([P, P, P], C.c_int), "ffs_state_cells": ([P, P], C.c_int),
+            "ffs_state_cut_table": ([P, P], C.c_int),
+            "ffs_state_set_horizon_cap": ([P, C.c_int32], C.c_int),
+            "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
+            "ffs_evaluate": ([P, C.c_int64, P, P, P, P, P, P, P], C.c_int),
+            "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
+            "ffs_random_population": ([P, C.c_int64, C.c_uint64, C.c_int64, P, P, P], C.c_int),
+            "ffs_evolve_begin": ([P, C.POINTER(GAConfig), P, P], C.c_int),
+            "ffs_evolve_step": ([P, C.c_int32], C.c_int),
+            "ffs_evolve": ([P, C.POINTER(GAConfig), P, P], C.c_int),
+            "ffs_best": ([P, P, P, P, P, P, P, P, P, P], C.c_int),
+            "ffs_run_population": ([P, P, P, P, P], C.c_int),
+            "ffs_run_history": ([P, P, P, P, P], C.c_int),
+            "ffs_run_info": ([P, P, P, P, P], C.c_int), "ffs_run_destroy": ([P], None),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(st, what):
+    if st != OK:
+        raise FFSError(st, what, lib().ffs_last_error().decode())
+
+
+def _np_ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _dev_ptr(t, dtype, numel, what):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what}: expected a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous() or t.numel() < numel:
+        raise TypeError(f"{what}: expected contiguous {dtype} with >= {numel} elements")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+class Instance:
+    """EDFFS instance (Table 2) in integer ticks, uploaded to `device`."""
+
+    def __init__(self, n, n_prime, g, o, P, Q, R, D, q_max, wt, device=0):
+        self._a = [np.ascontiguousarray(np.asarray(v, dtype=np.int32)).ravel() for v in (P, Q, R, D)]
+        ptr = [a.ctypes.data_as(C.POINTER(C.c_int32)) for a in self._a]
+        desc = _Desc(int(n), int(n_prime), int(g), int(o), ptr[0], ptr[1], ptr[2], ptr[3], int(q_max), int(wt))
+        h = C.c_void_p()
+        _check(lib().ffs_instance_create(C.byref(desc), int(device), C.byref(h)), "ffs_instance_create")
+        self.h = h
+        self.n, self.n_prime, self.g, self.o = int(n), int(n_prime), int(g), int(o)
+        self.NJ = self.n + self.n_prime
+        self.q_max, self.wt, self.device = int(q_max), int(wt), int(device)
+
+    @classmethod
+    def from_arrays(cls, a: dict, device=0):
+        return cls(a["n"], a["n_prime"], a["g"], a["o"], a["P"], a["Q"], a["R"], a["D"], a["q_max"], a["wt"],
+                   device=device)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ffs_instance_destroy(self.h)
+            self.h = None
+
+
+class State:
+    """Frozen rescheduling context at RS (ffs_reschedule_state)."""
+
+    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None):
+        self.inst = inst
+        oa = None if orig_assign is None else np.ascontiguousarray(np.asarray(orig_assign, np.int32)).ravel()
+        os_ = None if orig_start is None else np.ascontiguousarray(np.asarray(orig_start, np.int32)).ravel()
+        h = C.c_void_p()
+        K = C.c_int32()
+        _check(lib().ffs_reschedule_state(inst.h, int(rs), _np_ptr(oa), _np_ptr(os_), C.byref(h), C.byref(K)),
+               "ffs_reschedule_state")
+        self.h = h
+        self.K = K.value
+        self.rs = int(rs)
+        self.cells = inst.NJ * inst.g
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ffs_state_destroy(self.h)
+            self.h = None
+
+    def genes(self):
+        j = np.zeros(max(self.K, 1), np.int32)
+        s = np.zeros(max(self.K, 1), np.int32)
+        _check(lib().ffs_state_genes(self.h, _np_ptr(j), _np_ptr(s)), "ffs_state_genes")
+        return j[:self.K], s[:self.K]
+
+    def cell_states(self):
+        c = np.zeros(self.cells, np.int32)
+        _check(lib().ffs_state_cells(self.h, _np_ptr(c)), "ffs_state_cells")
+        return c
+
+    def cut_table(self):
+        c = np.zeros(self.cells + 1, np.int32)
+        _check(lib().ffs_state_cut_table(self.h, _np_ptr(c)), "ffs_state_cut_table")
+        return c
+
+    def set_horizon_cap(self, cap: int):
+        _check(lib().ffs_state_set_horizon_cap(self.h, int(cap)), "ffs_state_set_horizon_cap")
+
+    def info(self):
+        v = [C.c_int32() for _ in range(5)]
+        _check(lib().ffs_state_info(self.h, *[C.byref(x) for x in v]), "ffs_state_info")
+        return dict(K=v[0].value, cells=v[1].value, horizon_cap=v[2].value, horizon_bound=v[3].value,
+                    smem_bytes=v[4].value)
+
+
+def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=None, start_out=None,
+             with_schedule=False, stream=None):
+    """Decode + evaluate device chromosomes x:int8[count,K], y:int16[count,K]."""
+    import torch
+    count = x.shape[0] if x.dim() == 2 else (x.numel() // max(state.K, 1))
+    dev = x.device
+    if objective is None:
+        objective = torch.empty(count, dtype=torch.int64, device=dev)
+    if total_tardiness is None:
+        total_tardiness = torch.empty(count, dtype=torch.int64, device=dev)
+    if makespan is None:
+        makespan = torch.empty(count, dtype=torch.int32, device=dev)
+    if with_schedule and start_out is None:
+        start_out = torch.empty((count, state.cells), dtype=torch.int32, device=dev)
+    n = count * state.K
+    _check(lib().ffs_evaluate(state.h, count, _dev_ptr(x, torch.int8, n, "x"), _dev_ptr(y, torch.int16, n, "y"),
+                              _dev_ptr(objective, torch.int64, count, "objective"),
+                              _dev_ptr(total_tardiness, torch.int64, count, "total_tardiness"),
+                              _dev_ptr(makespan, torch.int32, count, "makespan"),
+                              _dev_ptr(start_out, torch.int32, count * state.cells, "start_out"),
+                              _stream(stream)), "ffs_evaluate")
+    return objective, total_tardiness, makespan, start_out
+
+
+def evaluate_host(state: State, x: np.ndarray, y: np.ndarray, stream=None):
+    """Same as evaluate() with host buffers (copies inside the call)."""
+    x = np.ascontiguousarray(x, dtype=np.int8)
+    y = np.ascontiguousarray(y, dtype=np.int16)
+    count = x.shape[0]
+    obj = np.zeros(count, np.int64)
+    T = np.zeros(count, np.int64)
+    M = np.zeros(count, np.int32)
+    _check(lib().ffs_evaluate_host(state.h, count, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(T), _np_ptr(M),
+                                   _stream(stream)), "ffs_evaluate_host")
+    return obj, T, M
+
+
+def evaluate_host_into(state: State, x: np.ndarray, y: np.ndarray, obj: np.ndarray, T: np.ndarray,
+                       M: np.ndarray, stream=None):
+    """evaluate_host() into caller-provided (e.g. pinned) host buffers."""
+    _check(lib().ffs_evaluate_host(state.h, x.shape[0], _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(T),
+                                   _np_ptr(M), _stream(stream)), "ffs_evaluate_host")
+
+
+def random_population(state: State, count: int, seed: int, first_id: int = 0, device=None, stream=None):
+    """Counter-based random chromosomes on the device."""
+    import torch
+    dev = torch.device("cuda", state.inst.device) if device is None else device
+    x = torch.empty((count, state.K), dtype=torch.int8, device=dev)
+    y = torch.empty((count, state.K), dtype=torch.int16, device=dev)
+    _check(lib().ffs_random_population(state.h, count, int(seed), int(first_id),
+                                       C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), _stream(stream)),
+           "ffs_random_population")
+    return x, y
+
+
+def decode_schedule(state: State, x_genes, y_genes):
+    """Decode ONE chromosome on the GPU and return its merged schedule (host):
+    assign/start [(n+n')*g], objective, sum T, C_max."""
+    import torch
+    dev = torch.device("cuda", state.inst.device)
+    x = torch.as_tensor(np.asarray(x_genes, np.int8).reshape(1, -1)).to(dev)
+    y = torch.as_tensor(np.asarray(y_genes, np.int16).reshape(1, -1)).to(dev)
+    if state.K == 0:
+        x = torch.zeros((1, 1), dtype=torch.int8, device=dev)
+        y = torch.ones((1, 1), dtype=torch.int16, device=dev)
+    obj, T, M, st = evaluate(state, x, y, with_schedule=True)
+    torch.cuda.synchronize(dev)
+    start = st[0].cpu().numpy()
+    cs = state.cell_states()
+    assign = -np.ones(state.cells, np.int32)
+    jj, ss = state.genes()
+    g = state.inst.g
+    frozen = getattr(state, "frozen_assign", None)
+    if frozen is not None:
+        assign[cs != 0] = frozen[cs != 0]
+    for k in range(state.K):
+        assign[jj[k] * g + ss[k]] = int(np.asarray(x_genes).ravel()[k])
+    return assign, start, int(obj.item()), int(T.item()), int(M.item())
+
+
+def make_state(inst: Instance, rs: int, orig_assign=None, orig_start=None) -> State:
+    """State plus the frozen assignment kept for merged-schedule assembly."""
+    st = State(inst, rs, orig_assign, orig_start)
+    fa = -np.ones(st.cells, np.int32)
+    if orig_assign is not None:
+        oa = np.asarray(orig_assign, np.int32).ravel()
+        fa[: oa.size] = oa
+    st.frozen_assign = fa
+    return st
+
+
+class Run:
+    """Island GA of one rescheduling point (ffs_evolve_begin / _step / ffs_best).
+
+    hooks: optional (allreduce_max_i64, allgather) Python callables with the
+    C signatures of ffs_ga_config (see paper_1903_10741_b200.dist).
+    """
+
+    def __init__(self, state: State, island_w: int, island_h: int, islands_total: int, generations: int,
+                 seed: int, island_begin: int = 0, island_end: int | None = None, xo_threshold: int = XO_090,
+                 mut_threshold: int = MUT_010, migration_interval: int = 10, rank: int = 0, world: int = 1,
+                 hooks=None, stream=None):
+        self.state = state
+        island_end = islands_total if island_end is None else island_end
+        ar, ag = (ALLRED(), ALLGATHER()) if hooks is None else (ALLRED(hooks[0]), ALLGATHER(hooks[1]))
+        self._keep = (ar, ag)
+        self.cfg = GAConfig(island_w, island_h, islands_total, island_begin, island_end, xo_threshold,
+                            mut_threshold, migration_interval, generations, seed, rank, world, ar, ag, None)
+        self.generations = generations
+        self.tile = island_w * island_h
+        self.nisl = island_end - island_begin
+        self.nloc = self.nisl * self.tile
+        self._stream = stream
+        h = C.c_void_p()
+        _check(lib().ffs_evolve_begin(state.h, C.byref(self.cfg), _stream(stream), C.byref(h)), "ffs_evolve_begin")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ffs_run_destroy(self.h)
+            self.h = None
+
+    def step(self, generations: int = 1):
+        _check(lib().ffs_evolve_step(self.h, int(generations)), "ffs_evolve_step")
+
+    def info(self):
+        g = C.c_int32()
+        e = C.c_int64()
+        ev = C.c_int64()
+        nl = C.c_int32()
+        _check(lib().ffs_run_info(self.h, C.byref(g), C.byref(e), C.byref(ev), C.byref(nl)), "ffs_run_info")
+        return dict(generation=g.value, emax=e.value, evaluations=ev.value, launches=nl.value)
+
+    def population(self):
+        K = self.state.K
+        x = np.zeros((self.nloc, K), np.int8)
+        y = np.zeros((self.nloc, K), np.int16)
+        obj = np.zeros(self.nloc, np.int64)
+        fit = np.zeros(self.nloc, np.int64)
+        _check(lib().ffs_run_population(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)),
+               "ffs_run_population")
+        return x, y, obj, fit
+
+    def history(self):
+        K = self.state.K
+        x = np.zeros((self.nisl, K), np.int8)
+        y = np.zeros((self.nisl, K), np.int16)
+        obj = np.zeros(self.nisl, np.int64)
+        fit = np.zeros(self.nisl, np.int64)
+        _check(lib().ffs_run_history(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)), "ffs_run_history")
+        return x, y, obj, fit
+
+    def best(self):
+        K, cells = self.state.K, self.state.cells
+        x = np.zeros(max(K, 1), np.int8)
+        y = np.zeros(max(K, 1), np.int16)
+        assign = np.zeros(cells, np.int32)
+        start = np.zeros(cells, np.int32)
+        obj, T, M = C.c_int64(), C.c_int64(), C.c_int32()
+        g = self.info()["generation"]
+        tmin = np.zeros(max(g + 1, 1), np.int64)
+        tsum = np.zeros(max(g + 1, 1), np.int64)
+        _check(lib().ffs_best(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(assign), _np_ptr(start), C.byref(obj),
+                              C.byref(T), C.byref(M), _np_ptr(tmin), _np_ptr(tsum)), "ffs_best")
+        return dict(x=x[:K], y=y[:K], assign=assign, start=start, objective=obj.value, sum_tardiness=T.value,
+                    makespan=M.value, trace_min=tmin[:g + 1], trace_sum=tsum[:g + 1])

@@ -1,0 +1,194 @@
+"""Bit-exact parity of the CUDA decode/evaluate (through the C-ABI) with the oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as orc
+from paper_1903_10741_b200 import ffs
+from paper_1903_10741_b200 import workload as wlmod
+from tests import fixtures as fx
+from tests.gpu_util import both_event_ctx, check_gene_order, gpu_state
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def gpu_eval(st, x, y, sched=False):
+    xd = torch.as_tensor(np.ascontiguousarray(x)).to(DEV)
+    yd = torch.as_tensor(np.ascontiguousarray(y)).to(DEV)
+    obj, T, M, S = ffs.evaluate(st, xd, yd, with_schedule=sched)
+    torch.cuda.synchronize()
+    return obj.cpu().numpy(), T.cpu().numpy(), M.cpu().numpy(), (S.cpu().numpy() if sched else None)
+
+
+def compare(octx, st, x, y, n_sched=None):
+    obj, T, M, S = gpu_eval(st, x, y, sched=True)
+    oo, oT, oM, _ = octx.evaluate_batch(x, y, nthreads=8)
+    assert (obj == oo).all(), np.flatnonzero(obj != oo)[:10]
+    assert (T == oT).all()
+    assert (M == oM).all()
+    n_sched = len(x) if n_sched is None else n_sched
+    for i in range(min(n_sched, len(x))):
+        r = octx.decode_genes(x[i], y[i])
+        assert (S[i] == r["start"]).all(), i
+
+
+def test_table4_printed_chromosome():
+    d, inst, octx = fx.table4_ctx()
+    _, a = fx.table4_arrays()
+    st = gpu_state(a, d["rs"], np.array(d["orig_assign"]), np.array(d["orig_start"]))
+    check_gene_order(octx, st)
+    x, y = octx.to_genes(np.array(d["X"]), np.array(d["Y"]))
+    obj, T, M, S = gpu_eval(st, x[None], y[None], sched=True)
+    assert M[0] == 2042                                       # Fig. 8 caption
+    compare(octx, st, x[None], y[None])
+
+
+def test_h3():
+    d, inst, octx = fx.h3()
+    a = dict(n=3, n_prime=0, g=2, o=2, P=np.array(d["P"]), Q=np.ones((3, 2, 2), np.int32),
+             R=np.array(d["release"]), D=np.array(d["due"]), q_max=2, wt=10)
+    st = gpu_state(a, 0)
+    x, y = octx.to_genes(np.array(d["X"]), np.array(d["Y"]))
+    obj, T, M, S = gpu_eval(st, x[None], y[None], sched=True)
+    assert obj[0] == 27 and T[0] == 2 and M[0] == 7
+    assert (S[0].reshape(3, 2) == np.array(d["expected_start"])).all()
+
+
+@pytest.mark.parametrize("cfg,count,nsched", [("A2", 3000, 200), ("B", 1000, 50), ("C", 300, 10)])
+def test_random_chromosomes_configs(cfg, count, nsched):
+    wl = {"A2": wlmod.config_A2, "B": wlmod.config_B, "C": wlmod.config_C}[cfg]()
+    octx, st, arr = both_event_ctx(wl)
+    check_gene_order(octx, st)
+    x, y = wlmod.random_chromosomes(count, st.K, wl.o, seed=7)
+    compare(octx, st, x, y, n_sched=nsched)
+
+
+def test_general_power_path():
+    wl = wlmod.gen_v1("Cq", 30, 6, 3, 6, arrivals_per_event=[8], ratios=[0.3], power="u13", seed=5)
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(500, st.K, wl.o, seed=8)
+    compare(octx, st, x, y, n_sched=20)
+
+
+def test_overflow_path_is_exact():
+    """A tiny in-SMEM horizon forces the global-memory overflow path."""
+    wl = wlmod.config_B()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(400, st.K, wl.o, seed=9)
+    ref = gpu_eval(st, x, y, sched=True)
+    st.set_horizon_cap(64)
+    assert st.info()["horizon_cap"] == 64 < st.info()["horizon_bound"]
+    got = gpu_eval(st, x, y, sched=True)
+    for u, v in zip(ref, got):
+        assert (u == v).all()
+    compare(octx, st, x[:100], y[:100], n_sched=20)
+    st.set_horizon_cap(0)
+
+
+def test_u16_profile_path():
+    """Q_max > 255 selects the 16-bit power profile."""
+    rng = np.random.default_rng(4)
+    n, g, o = 12, 3, 3
+    P = rng.integers(1, 6, size=(n, g, o)).astype(np.int32)
+    Q = rng.integers(50, 200, size=(n, g, o)).astype(np.int32)
+    R = rng.integers(0, 5, size=n).astype(np.int32)
+    a = dict(n=n, n_prime=0, g=g, o=o, P=P, Q=Q, R=R, D=R + 10, q_max=400, wt=3)
+    octx = orc.Ctx(fx.workload_instance(a), 0)
+    st = gpu_state(a, 0)
+    x, y = wlmod.random_chromosomes(300, st.K, o, seed=3)
+    compare(octx, st, x, y, n_sched=30)
+
+
+@pytest.mark.parametrize("case", ["K1", "o1", "g1", "qinf", "q0", "rs_end", "static_ties"])
+def test_edge_cases(case):
+    rng = np.random.default_rng(abs(hash(case)) % 1000)
+    n, g, o, qmax = 6, 3, 2, 2
+    P = rng.integers(1, 4, size=(n, g, o)).astype(np.int32)
+    Q = np.ones((n, g, o), np.int32)
+    R = rng.integers(0, 4, size=n).astype(np.int32)
+    D = R + 5
+    if case == "o1":
+        o, P, Q = 1, P[:, :, :1].copy(), Q[:, :, :1].copy()
+    if case == "g1":
+        g, P, Q = 1, P[:, :1].copy(), Q[:, :1].copy()
+    if case == "qinf":
+        qmax = 1000
+    if case == "q0":
+        Q = rng.integers(0, 2, size=P.shape).astype(np.int32)
+    if case == "static_ties":
+        P = np.ones_like(P)
+        R = np.zeros(n, np.int32)
+    a = dict(n=n, n_prime=0, g=g, o=o, P=P, Q=Q, R=R, D=D, q_max=qmax, wt=7)
+    octx0 = orc.Ctx(fx.workload_instance(a), 0)
+    xp, yp = wlmod.random_chromosomes(1, octx0.K, o, seed=1)
+    plan = octx0.decode_genes(xp[0], yp[0])
+    if case == "K1":
+        # freeze late enough that exactly one op remains pending
+        ends = sorted(set((plan["start"] + P.reshape(-1, o)[np.arange(n * g), plan["assign"]]).tolist()))
+        rs = None
+        for t in range(max(ends), -1, -1):
+            c = orc.Ctx(fx.workload_instance(a), t, plan["assign"], plan["start"])
+            if c.K == 1:
+                rs = t
+                break
+        assert rs is not None
+    elif case == "rs_end":
+        rs = plan["makespan"] + 3
+    else:
+        rs = plan["makespan"] // 3
+    octx = orc.Ctx(fx.workload_instance(a), rs, plan["assign"], plan["start"])
+    st = gpu_state(a, rs, plan["assign"], plan["start"])
+    check_gene_order(octx, st)
+    if octx.K == 0:
+        x = np.zeros((4, 1), np.int8)
+        y = np.ones((4, 1), np.int16)
+        obj, T, M, S = gpu_eval(st, x[:, :0].copy(), y[:, :0].copy(), sched=True)
+        r = octx.decode(-np.ones(octx.cells, np.int32), -np.ones(octx.cells, np.int32))
+        assert (obj == r["objective"]).all() and (M == r["makespan"]).all()
+        assert (S == r["start"]).all()
+        return
+    x, y = wlmod.random_chromosomes(200, st.K, o, seed=2)
+    compare(octx, st, x, y, n_sched=50)
+
+
+def test_random_population_matches_oracle_init():
+    wl = wlmod.config_A2()
+    octx, st, arr = both_event_ctx(wl)
+    ga = orc.GA(octx, 4, 2, 3, 1, seed=10741)
+    ga.step()
+    ox, oy, oobj, _ = ga.population()
+    xs, ys = [], []
+    for I in range(3):
+        x, y = ffs.random_population(st, 8, seed=10741, first_id=I << 20)
+        xs.append(x.cpu().numpy())
+        ys.append(y.cpu().numpy())
+    assert (np.concatenate(xs) == ox).all() and (np.concatenate(ys) == oy).all()
+
+
+def test_evaluate_host_matches_device():
+    wl = wlmod.config_B()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(256, st.K, wl.o, seed=11)
+    obj, T, M = ffs.evaluate_host(st, x, y)
+    ref = gpu_eval(st, x, y)
+    assert (obj == ref[0]).all() and (T == ref[1]).all() and (M == ref[2]).all()
+
+
+def test_full_size_sampled_parity():
+    """Config C at the bench's launch configuration (65,536 Philox chromosomes
+    generated on the device); the oracle checks a sample one by one."""
+    wl = wlmod.config_C()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = ffs.random_population(st, 65536, seed=10741)
+    obj, T, M, _ = ffs.evaluate(st, x, y)
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(0).choice(65536, 48, replace=False)
+    xs, ys = x.cpu().numpy()[idx], y.cpu().numpy()[idx]
+    oo, oT, oM, _ = octx.evaluate_batch(xs, ys, nthreads=8)
+    assert (obj.cpu().numpy()[idx] == oo).all()
+    assert (T.cpu().numpy()[idx] == oT).all() and (M.cpu().numpy()[idx] == oM).all()
+    # every chromosome is a valid permutation (device generator property)
+    ysort = torch.sort(y.to(torch.int32), dim=1).values
+    assert bool((ysort == torch.arange(1, st.K + 1, device=y.device, dtype=torch.int32)).all())
