@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the EDFFS decode/evaluate + island GA hot path on B200.
+
+One "step" = one GA generation of the whole hot path (SURVEY 8(a) rows a2-a11:
+selection, crossover + correction, mutation, decode + evaluate, elitist
+replacement, ring migration every 10 generations, trace) over config C's
+population: the 100-job instance (80 originals + 20 arrivals at RS = 25% of the
+original plan's makespan, 10 stages x 4 machines, Q_max = 10, gen-v1 recipe),
+256 islands x 256 individuals (16x16 tiles) per GPU.  N GPUs hold 256*N
+islands (weak scaling; N = 8 is config D) and exchange boundary elites with an
+NCCL allgather every 10 generations.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
+(oracle/, plain C) on a bounded sample of the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chromosome evaluations/sec and GA generations/sec per GPU at 1/2/4/8 B200"
+ISLAND_W, ISLAND_H, ISLANDS_PER_GPU = 16, 16, 256
+SEED = 10741
+# issue-rate roofline: 148 SMs x 4 SMSPs x 1 warp-instruction/clk x 1.965 GHz
+ISSUE_PEAK = 148 * 4 * 1.965e9
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def workload_desc(n_gpus):
+    return {
+        "workload": "C: gen-v1 100 jobs (80 + 20 arrivals at RS=25% of plan C_max) x 10 stages x 4 machines, "
+                    "Q_max=10 (tight), WT=100; 256 islands x 256 (16x16) per GPU; 1 generation per step",
+        "islands_total": ISLANDS_PER_GPU * n_gpus,
+        "population_total": ISLANDS_PER_GPU * ISLAND_W * ISLAND_H * n_gpus,
+        "generations_per_step": 1,
+        "migration": "every 10 generations, NCCL allgather of boundary elites" if n_gpus > 1
+                     else "every 10 generations, intra-GPU ring",
+        "l2": "inputs larger than L2: two 170 MB population buffers per GPU",
+        "seed_instance": 1903, "seed_ga": SEED,
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [v.strip() for v in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except Exception:
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# the reference arm: the CPU oracle as it stands
+# ---------------------------------------------------------------------------
+def oracle_ctx():
+    from tests import fixtures as fx
+    from paper_1903_10741_b200 import workload as wlmod
+    wl = wlmod.config_C()
+    octx, arr, plan, rs = fx.oracle_event_ctx(wl)
+    return wl, octx
+
+
+def cpu_baseline_eval(seconds):
+    """Oracle decode+evaluate of Philox-independent random chromosomes of
+    config C on every host core, for about `seconds`.  Returns (evals/s,
+    cores, sample, algorithmic ops per evaluation)."""
+    from paper_1903_10741_b200 import workload as wlmod
+    wl, octx = oracle_ctx()
+    cores = len(os.sched_getaffinity(0))
+    n = 0
+    cnt = {"dispatches": 0, "checks": 0, "jumps": 0, "updates": 0}
+    t0 = time.perf_counter()
+    batch = max(32, 16 * cores)
+    while time.perf_counter() - t0 < seconds:
+        x, y = wlmod.random_chromosomes(batch, octx.K, wl.o, seed=1000 + n)
+        _, _, _, c = octx.evaluate_batch(x, y, nthreads=cores)
+        for k in cnt:
+            cnt[k] += c[k]
+        n += batch
+    dt = time.perf_counter() - t0
+    ops = sum(cnt.values()) / n
+    return n / dt, cores, f"{n} random config-C chromosomes (K={octx.K}), oracle evaluate, {dt:.1f} s", ops, cnt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    wl, octx = oracle_ctx()
+    cores = len(os.sched_getaffinity(0))
+    islands = 2  # bounded sample: 2 islands x 256 individuals per step
+    G = args.warmup + args.steps
+    ga = orc.GA(octx, ISLAND_W, ISLAND_H, islands, G, SEED, nthreads=cores)
+    ga.step()
+    for _ in range(args.warmup):
+        ga.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ga.step()
+    dt = time.perf_counter() - t0
+    pop = islands * ISLAND_W * ISLAND_H
+    v = pop * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": dict(workload_desc(1), sample=f"{islands} islands x 256 per step"),
+        "gens_per_s": args.steps / dt,
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                         "sample": f"oracle island GA, {islands} islands x 256 (16x16) of config C, "
+                                   f"{args.steps} generations"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1903_10741_b200 import dist as fdist
+    from paper_1903_10741_b200 import ffs
+    from paper_1903_10741_b200 import workload as wlmod
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    # ---- workload: plan decoded on the GPU at RS = 0, freeze at RS
+    wl = wlmod.config_C()
+    base = ffs.Instance.from_arrays(wl.original_instance(), device=local)
+    st0 = ffs.make_state(base, 0)
+    _, pstart, _, _, pcmax = ffs.decode_schedule(st0, wl.plan_x, wl.plan_y)
+    passign = wl.plan_x.astype(np.int32)
+    rs = wl.rs_from_makespan(wl.ratios[0], pcmax)
+    inst = ffs.Instance.from_arrays(wl.instance_at(0, [rs]), device=local)
+    st = ffs.make_state(inst, rs, passign, pstart[: wl.n * wl.g])
+    K = st.K
+
+    islands_total = ISLANDS_PER_GPU * world
+    b, e = fdist.shard(islands_total, rank, world)
+    G = args.warmup + args.steps
+    stream = torch.cuda.Stream(device=dev)
+    hooks = fdist.make_hooks(device_memory=True) if world > 1 else None
+    with torch.cuda.stream(stream):
+        run = ffs.Run(st, ISLAND_W, ISLAND_H, islands_total, G, SEED, island_begin=b, island_end=e,
+                      rank=rank, world=world, hooks=hooks, stream=stream)
+        for _ in range(args.warmup):
+            run.step(1)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    pop_local = (e - b) * ISLAND_W * ISLAND_H
+
+    l0 = run.info()["launches"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            run.step(args.steps)
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    launches = run.info()["launches"] - l0
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    evals_total = pop_local * world * args.steps
+    value = evals_total / t_max
+    best = run.best()
+
+    # ---- dominant kernel alone (decode + evaluate of the same 65,536 population,
+    # same launch configuration), CUDA events on its stream
+    x, y = ffs.random_population(st, pop_local, SEED, first_id=b << 20, stream=stream)
+    obj = torch.empty(pop_local, dtype=torch.int64, device=dev)
+    T = torch.empty(pop_local, dtype=torch.int64, device=dev)
+    M = torch.empty(pop_local, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        ffs.evaluate(st, x, y, obj, T, M, stream=stream)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    torch.cuda.synchronize(dev)
+    for a_, b_ in k_ev:
+        a_.record(stream)
+        ffs.evaluate(st, x, y, obj, T, M, stream=stream)
+        b_.record(stream)
+    torch.cuda.synchronize(dev)
+    k_times = [a_.elapsed_time(b_) / 1e3 for a_, b_ in k_ev]
+    t_kernel = statistics.mean(k_times)
+    eval_only = pop_local / t_kernel
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside
+    xh = torch.empty((pop_local, K), dtype=torch.int8, pin_memory=True)
+    yh = torch.empty((pop_local, K), dtype=torch.int16, pin_memory=True)
+    xh.copy_(x.cpu())
+    yh.copy_(y.cpu())
+    oh = torch.empty(pop_local, dtype=torch.int64, pin_memory=True).numpy()
+    th = torch.empty(pop_local, dtype=torch.int64, pin_memory=True).numpy()
+    mh = torch.empty(pop_local, dtype=torch.int32, pin_memory=True).numpy()
+    xn, yn = xh.numpy(), yh.numpy()
+    ffs.evaluate_host_into(st, xn, yn, oh, th, mh, stream=stream)
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ffs.evaluate_host_into(st, xn, yn, oh, th, mh, stream=stream)
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = pop_local * world / float(te.item())
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": dict(workload_desc(world), K=K, rs=rs, parallelism=f"islands x{world}"),
+            "gens_per_s": args.steps / t_max,
+            "evals_per_s_per_gpu": value / world,
+            "eval_only": {"value": eval_only * world, "unit": "evals/s", "ms_per_launch": 1e3 * t_kernel,
+                          "population": pop_local},
+            "gpu_launches": launches,
+            "best_objective": best["objective"],
+            "clocks": clk.summary(),
+        }
+        alg_ops = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample, alg_ops, cnt = cpu_baseline_eval(args.cpu_seconds)
+            out["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                                   "sample": sample}
+            out["alg_ops_per_eval"] = alg_ops
+        if alg_ops is None:
+            alg_ops = 7.1 * K  # per-dispatch average measured by the instrumented oracle
+        achieved = eval_only * alg_ops
+        out["roofline"] = {"bound": "alu", "achieved": achieved / 1e9, "peak": ISSUE_PEAK / 1e9,
+                           "unit": "Gop/s", "frac": achieved / ISSUE_PEAK, "traffic": None,
+                           "note": "algorithmic ops (oracle-counted dispatches + power checks + delay jumps + "
+                                   "profile updates per evaluation) / evaluate-kernel time, against the issue "
+                                   "rate 148 SM x 4 SMSP x 1.965 GHz (one warp-instruction per op)",
+                           "kernel": "evaluate_kernel", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
+        out["e2e"] = {"value": e2e_value, "unit": "evals/s",
+                      "h2d_bytes_per_step": int(pop_local * K * 3),
+                      "d2h_bytes_per_step": int(pop_local * (8 + 8 + 4)),
+                      "what": "ffs_evaluate_host over the 65,536-chromosome population from pinned host memory"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
