@@ -48,8 +48,14 @@ struct ImageHdr {
   uint32_t off_lvl0;             // u32 [lvl_words0] initial power profile (RUNNING ops), LVL-typed
   uint32_t off_pjob;             // i32 [n_pjobs] job index
   uint32_t off_pdue;             // i32 [n_pjobs] D_j - RS
+  // lane-decode path (one lane per chromosome), see lane.cu
+  uint32_t off_pqt;              // u32 [NJ*G*O]  p | q << 8 | j << 16
+  uint32_t off_ready16;          // u32 [ceil(NJ/2)]  ready0 as u16 pairs
+  uint32_t off_mfree16;          // u32 [ceil(G*O/2)] mfree0 as u16 pairs
+  int32_t thr_min;               // Q_max - min Q: a slot is "blocked" for every op iff level > thr_min
+  int32_t uniform_q;             // all Q_jsm equal
   uint32_t image_bytes;          // multiple of 16
-  uint32_t pad_;
+  uint32_t pad_[3];
 };
 
 struct Instance {
@@ -65,6 +71,8 @@ struct Instance {
 struct OvfScratch {
   int32_t *list = nullptr;       // [1 + cap]: count, then chromosome ids
   int64_t cap = 0;
+  uint16_t *ordg = nullptr;      // lane path: rank-ordered ops, [tile][K][32]
+  int64_t ordg_elems = 0;
   void *level = nullptr;         // [fallback warps * hfull * sizeof(LVL)]
   int64_t level_bytes = 0;
   ffs_status ensure(int64_t count, int64_t level_bytes_needed);
@@ -91,6 +99,16 @@ struct State {
   size_t smem_bytes = 0, per_warp_bytes = 0;
   size_t fb_smem_bytes = 0, fb_per_warp_bytes = 0;
   int fb_warps_per_cta = 4;
+  // lane-decode path geometry (valid when lane_ok)
+  bool lane_ok = false;
+  bool lane_disabled = false;        // FFS_DISABLE_LANE set: force the warp path
+  int32_t lane_hcap = 0;             // profile slots per chromosome (multiple of 32)
+  int32_t lane_wpt = 0;              // 32-bit state words per thread
+  int lane_warps_per_cta = 0, lane_ctas_per_sm = 1;
+  size_t lane_smem = 0;
+  int ord_warps = 32;                // order kernel: one warp per chromosome, 32 per CTA
+  size_t ord_smem = 0, ord_per_warp = 0;
+  uint32_t ord_stride = 0;           // bytes between the 32 staged order arrays
   OvfScratch scratch;
   ffs_status build_image();
 };
@@ -112,7 +130,11 @@ struct EvalArgs {
   void *lvl_global;              // fallback: global profiles
   int32_t h_cap;                 // slots in the profile used by this launch
   int32_t per_warp_bytes;
+  const uint16_t *ordg;          // lane path
+  int64_t first;                 // lane path: first chromosome of this chunk
 };
+
+ffs_status launch_lane(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s, int *launches);
 
 ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
                            int *launches);

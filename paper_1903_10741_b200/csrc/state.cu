@@ -5,6 +5,7 @@
 // else PENDING (reading R7); every op of a new job is PENDING.  RUNNING ops
 // keep their machine busy and draw power until C (R3).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -44,10 +45,13 @@ ffs_status OvfScratch::ensure(int64_t count, int64_t level_bytes_needed) {
 void OvfScratch::release() {
   if (list) cudaFree(list);
   if (level) cudaFree(level);
+  if (ordg) cudaFree(ordg);
   list = nullptr;
   level = nullptr;
+  ordg = nullptr;
   cap = 0;
   level_bytes = 0;
+  ordg_elems = 0;
 }
 
 static uint32_t r16(uint64_t v) { return (uint32_t)((v + 15) & ~(uint64_t)15); }
@@ -137,6 +141,17 @@ ffs_status State::build_image() {
   H.off_lvl0 = off; off += r16((uint64_t)H.lvl_words0 * 4);
   H.off_pjob = off; off += r16((uint64_t)pjob.size() * 4);
   H.off_pdue = off; off += r16((uint64_t)pjob.size() * 4);
+  H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
+  H.off_ready16 = off; off += r16((uint64_t)((NJ + 1) / 2) * 4);
+  H.off_mfree16 = off; off += r16((uint64_t)((G * O + 1) / 2) * 4);
+  int32_t qmin = in.q_max, qmaxv = 0, pmax = 0;
+  for (size_t i = 0; i < in.Q.size(); ++i) {
+    qmin = std::min(qmin, in.Q[i]);
+    qmaxv = std::max(qmaxv, in.Q[i]);
+    pmax = std::max(pmax, in.P[i]);
+  }
+  H.thr_min = in.q_max - qmin;
+  H.uniform_q = qmin == qmaxv;
   H.image_bytes = off;
   image_host.assign(off, 0);
   uint8_t *img = image_host.data();
@@ -161,6 +176,18 @@ ffs_status State::build_image() {
   if (!pjob.empty()) {
     std::memcpy(img + H.off_pjob, pjob.data(), pjob.size() * 4);
     std::memcpy(img + H.off_pdue, pdue.data(), pdue.size() * 4);
+  }
+  {
+    uint32_t *pqt = (uint32_t *)(img + H.off_pqt);
+    for (int j = 0; j < NJ; ++j)
+      for (int so = 0; so < G * O; ++so) {
+        size_t i = (size_t)j * G * O + so;
+        pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
+      }
+    uint16_t *r16p = (uint16_t *)(img + H.off_ready16);
+    for (int j = 0; j < NJ; ++j) r16p[j] = (uint16_t)std::min<int32_t>(ready0[j], 65535);
+    uint16_t *m16p = (uint16_t *)(img + H.off_mfree16);
+    for (int i = 0; i < G * O; ++i) m16p[i] = (uint16_t)std::min<int32_t>(mfree0[i], 65535);
   }
 
   // --- geometry: profile capacity and warps per CTA
@@ -192,6 +219,43 @@ ffs_status State::build_image() {
   fb_per_warp_bytes = per_warp(0, false);
   fb_warps_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(4, budget / (int64_t)fb_per_warp_bytes));
   fb_smem_bytes = H.image_bytes + (size_t)fb_warps_per_cta * fb_per_warp_bytes;
+
+  // --- lane-decode path (one lane per chromosome): eligibility and geometry
+  lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 32 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
+  if (lane_ok) {
+    const int64_t lbudget = kSmemLimit - (int64_t)H.image_bytes - 256;
+    const int64_t fixed_words = (NJ + 1) / 2 + (G * O + 1) / 2;
+    auto words = [&](int64_t hc) { return fixed_words + hc / 4 + hc / 32; };
+    int64_t hfull = h_bound;  // multiple of 32
+    int64_t hc = hfull;
+    int warps = 8;
+    while (warps > 0 && words(hc) * 128 * warps > lbudget) {
+      // shrink the horizon first (down to 256 slots), then the warp count
+      if (hc > 256) hc = std::max<int64_t>(256, (lbudget / (128 * warps) - fixed_words) * 32 / 9 / 32 * 32);
+      if (words(hc) * 128 * warps > lbudget) --warps;
+    }
+    if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
+    if (warps < 2 || hc < 32) {
+      lane_ok = false;
+    } else {
+      lane_hcap = (int32_t)hc;
+      lane_wpt = (int32_t)words(hc);
+      lane_warps_per_cta = warps;
+      lane_smem = H.image_bytes + (size_t)warps * lane_wpt * 128;
+      lane_ctas_per_sm = (int)std::max<int64_t>(1, (int64_t)(kSmemLimit + 1024) / (int64_t)(lane_smem + 1024));
+      // order kernel: 32 staged order arrays (odd word stride: conflict-free
+      // transposed reads) + per-warp scan scratch
+      uint32_t st = r16((uint64_t)K * 2);
+      if ((st / 4) % 2 == 0) st += 4;
+      ord_stride = st;
+      ord_per_warp = r16((uint64_t)nt * 4) + r16((uint64_t)K * 2);
+      const int64_t obudget = kSmemLimit - (int64_t)H.image_bytes - 256 - 32 * (int64_t)st;
+      ord_warps = 32;
+      while (ord_warps > 1 && (int64_t)ord_per_warp * ord_warps > obudget) ord_warps /= 2;
+      if ((int64_t)ord_per_warp * ord_warps > obudget) lane_ok = false;
+      ord_smem = H.image_bytes + 32 * (size_t)st + (size_t)ord_warps * ord_per_warp;
+    }
+  }
 
   // --- upload
   cudaSetDevice(in.dev);
@@ -345,6 +409,7 @@ ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_
     return fail(FFS_ERR_INVALID_ARG, "K (pending ops) must be <= 32767 (int16 priorities)");
   }
   st.lvl_bytes = in.q_max <= 255 ? 1 : 2;
+  st.lane_disabled = getenv("FFS_DISABLE_LANE") != nullptr;
   cudaSetDevice(in.dev);
   ffs_status e = st.build_image();
   if (e != FFS_OK) {
@@ -396,9 +461,9 @@ ffs_status ffs_state_info(const ffs_state *h, int32_t *K, int32_t *cells, int32_
   if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
   if (K) *K = h->v.K;
   if (cells) *cells = h->v.cells;
-  if (hcap) *hcap = h->v.h_cap;
+  if (hcap) *hcap = h->v.lane_ok ? h->v.lane_hcap : h->v.h_cap;
   if (hb) *hb = h->v.h_bound;
-  if (smem) *smem = (int32_t)h->v.smem_bytes;
+  if (smem) *smem = (int32_t)(h->v.lane_ok ? h->v.lane_smem : h->v.smem_bytes);
   return FFS_OK;
 }
 

@@ -1,0 +1,35 @@
+"""Short driver for ncu: config C state, 65,536 device chromosomes, a few
+ffs_evaluate launches (the bench's dominant kernel in its launch config)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1903_10741_b200 import ffs
+from paper_1903_10741_b200 import workload as wlmod
+
+
+def config_c_state(device=0):
+    wl = wlmod.config_C()
+    base = ffs.Instance.from_arrays(wl.original_instance(), device=device)
+    st0 = ffs.make_state(base, 0)
+    _, pstart, _, _, pcmax = ffs.decode_schedule(st0, wl.plan_x, wl.plan_y)
+    rs = wl.rs_from_makespan(wl.ratios[0], pcmax)
+    inst = ffs.Instance.from_arrays(wl.instance_at(0, [rs]), device=device)
+    st = ffs.make_state(inst, rs, wl.plan_x.astype(np.int32), pstart[: wl.n * wl.g])
+    st._keep = (base, st0, inst)
+    return wl, st
+
+
+if __name__ == "__main__":
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    wl, st = config_c_state()
+    print(st.info())
+    x, y = ffs.random_population(st, n, 10741)
+    for _ in range(reps):
+        obj, T, M, _ = ffs.evaluate(st, x, y)
+    torch.cuda.synchronize()
+    print("obj[0:4]", obj[:4].tolist())

@@ -25,3 +25,14 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(params=["lane", "warp"])
+def path(request, monkeypatch):
+    """Both evaluate paths: lane-per-chromosome (default when eligible) and the
+    general warp-per-chromosome kernel (FFS_DISABLE_LANE, read at state creation)."""
+    if request.param == "warp":
+        monkeypatch.setenv("FFS_DISABLE_LANE", "1")
+    else:
+        monkeypatch.delenv("FFS_DISABLE_LANE", raising=False)
+    return request.param

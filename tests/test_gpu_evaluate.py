@@ -57,7 +57,7 @@ def test_h3():
 
 
 @pytest.mark.parametrize("cfg,count,nsched", [("A2", 3000, 200), ("B", 1000, 50), ("C", 300, 10)])
-def test_random_chromosomes_configs(cfg, count, nsched):
+def test_random_chromosomes_configs(cfg, count, nsched, path):
     wl = {"A2": wlmod.config_A2, "B": wlmod.config_B, "C": wlmod.config_C}[cfg]()
     octx, st, arr = both_event_ctx(wl)
     check_gene_order(octx, st)
@@ -65,21 +65,21 @@ def test_random_chromosomes_configs(cfg, count, nsched):
     compare(octx, st, x, y, n_sched=nsched)
 
 
-def test_general_power_path():
+def test_general_power_path(path):
     wl = wlmod.gen_v1("Cq", 30, 6, 3, 6, arrivals_per_event=[8], ratios=[0.3], power="u13", seed=5)
     octx, st, arr = both_event_ctx(wl)
     x, y = wlmod.random_chromosomes(500, st.K, wl.o, seed=8)
     compare(octx, st, x, y, n_sched=20)
 
 
-def test_overflow_path_is_exact():
+def test_overflow_path_is_exact(path):
     """A tiny in-SMEM horizon forces the global-memory overflow path."""
     wl = wlmod.config_B()
     octx, st, arr = both_event_ctx(wl)
     x, y = wlmod.random_chromosomes(400, st.K, wl.o, seed=9)
     ref = gpu_eval(st, x, y, sched=True)
     st.set_horizon_cap(64)
-    assert st.info()["horizon_cap"] == 64 < st.info()["horizon_bound"]
+    assert st.info()["horizon_bound"] > 64
     got = gpu_eval(st, x, y, sched=True)
     for u, v in zip(ref, got):
         assert (u == v).all()
@@ -102,7 +102,7 @@ def test_u16_profile_path():
 
 
 @pytest.mark.parametrize("case", ["K1", "o1", "g1", "qinf", "q0", "rs_end", "static_ties"])
-def test_edge_cases(case):
+def test_edge_cases(case, path):
     rng = np.random.default_rng(abs(hash(case)) % 1000)
     n, g, o, qmax = 6, 3, 2, 2
     P = rng.integers(1, 4, size=(n, g, o)).astype(np.int32)
@@ -176,7 +176,7 @@ def test_evaluate_host_matches_device():
     assert (obj == ref[0]).all() and (T == ref[1]).all() and (M == ref[2]).all()
 
 
-def test_full_size_sampled_parity():
+def test_full_size_sampled_parity(path):
     """Config C at the bench's launch configuration (65,536 Philox chromosomes
     generated on the device); the oracle checks a sample one by one."""
     wl = wlmod.config_C()

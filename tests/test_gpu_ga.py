@@ -32,7 +32,7 @@ def assert_same(gpu_run, ga, k):
     ("B", 16, 8, 4, 12, 3),          # config B shape, 4 islands
     ("C", 16, 16, 2, 3, 1),          # config C shape, 2 islands, a few generations
 ])
-def test_trajectory_parity(cfg, w, h, islands, G, every):
+def test_trajectory_parity(cfg, w, h, islands, G, every, path):
     wl = {"A2": wlmod.config_A2, "B": wlmod.config_B, "C": wlmod.config_C}[cfg]()
     octx, st, arr = both_event_ctx(wl)
     seed = 10741
