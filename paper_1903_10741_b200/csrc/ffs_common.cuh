@@ -55,7 +55,8 @@ struct ImageHdr {
   int32_t thr_min;               // Q_max - min Q: a slot is "blocked" for every op iff level > thr_min
   int32_t uniform_q;             // all Q_jsm equal
   uint32_t image_bytes;          // multiple of 16
-  uint32_t pad_[3];
+  uint32_t lane_image_bytes;     // prefix staged by the lane-decode kernel
+  uint32_t pad_[2];
 };
 
 struct Instance {
@@ -94,6 +95,7 @@ struct State {
   void *image_dev = nullptr;
   int32_t *fstart_dev = nullptr;     // [cells] frozen starts (abs), -1 pending
   int32_t *cut_dev = nullptr;        // [cells+1] pend_before on device
+  uint32_t *gbase_dev = nullptr;     // [K] (j*G + s)*O of each gene
   // launch geometry of the evaluate kernel
   int warps_per_cta = 0, ctas_per_sm = 0, num_sms = 0;
   size_t smem_bytes = 0, per_warp_bytes = 0;
@@ -106,9 +108,8 @@ struct State {
   int32_t lane_wpt = 0;              // 32-bit state words per thread
   int lane_warps_per_cta = 0, lane_ctas_per_sm = 1;
   size_t lane_smem = 0;
-  int ord_warps = 32;                // order kernel: one warp per chromosome, 32 per CTA
-  size_t ord_smem = 0, ord_per_warp = 0;
-  uint32_t ord_stride = 0;           // bytes between the 32 staged order arrays
+  size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0;   // order kernel (32 warps per CTA)
+  int ord_ctas_per_sm = 1;
   OvfScratch scratch;
   ffs_status build_image();
 };

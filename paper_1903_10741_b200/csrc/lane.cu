@@ -1,27 +1,32 @@
-// lane.cu -- the fast evaluate path: Algorithm 1 by a warp per chromosome
-// (order_kernel), then Algorithm 2 by ONE LANE per chromosome
-// (lane_decode_kernel), 32 chromosomes per warp.
+// lane.cu -- the fast evaluate path: ONE LANE PER CHROMOSOME, 32 chromosomes
+// per warp, for Algorithm 1 (order_lane_kernel) and Algorithm 2
+// (lane_decode_kernel).
 //
-// Why: Algorithm 2 is a dependent chain of K dispatches per chromosome whose
-// per-dispatch work is scalar (t0 lookups, a window test, a commit).  With a
-// warp per chromosome 31 lanes duplicate that scalar work (measured: 96 warp
-// instructions per dispatch, 87% issue-active).  Here every lane decodes its
-// own chromosome, so one warp instruction advances 32 chromosomes.
+// Why: both algorithms are dependent chains per chromosome whose per-step
+// work is scalar.  With a warp per chromosome 31 lanes duplicate that work
+// (measured: 96 warp instructions per dispatched op, 87% issue-active).  Here
+// one warp instruction advances 32 chromosomes.
 //
-// Data layout
-//   ordg  (global) [tile][ceil(K/4)][32 lanes][4]  u16 P/Q-table index of the
-//         op at each rank, 4 ranks per lane per 8-byte load (coalesced 256 B)
-//   per-thread state in shared memory, LANE-INTERLEAVED 32-bit words (word w
-//   of lane l at (w*32 + l)*4: data-dependent accesses never bank-conflict):
+// Layouts
+//   per-thread arrays live in shared memory LANE-INTERLEAVED: 32-bit word w of
+//   lane l sits at (w*32 + l)*4, so data-dependent indices never bank-conflict.
+//   ordg (global) [tile][ceil(K/4)][32 lanes][4] u16: P/Q-table index of the op
+//   at each rank (4 ranks per lane per 8-byte load, 256 B per warp, coalesced).
+// Algorithm 1 (greedy reading R1) = stable sort by (prefix-min of y
+// over the job's pending stages desc, stage asc): per lane a sequential pass
+// marks runs ("leaders" = new prefix minima) and writes each run length at its
+// leader's priority, a suffix sum over priorities gives run starts, and a
+// second pass scatters every gene to start + offset.
+// Algorithm 2 (R2, R5): per lane state
 //     ready[j]  u16 pairs  earliest start of job j's next op (rel. to RS)
 //     mfree[m]  u16 pairs  machine free time (append-only sequencing, R6)
-//     level[t]  u8 x4      Q_t per tick after RS (Eq. (8))
-//     blocked   1 bit/tick level > Q_max - min Q: no op fits (exact)
-// Feasibility (R2, R5): the earliest t >= t0 with p consecutive un-blocked
-// ticks is found on a 32-tick window of the blocked bitmap (shift/and run
-// test); ops with q > min Q also verify the window's bytes.  Commit adds q to
-// p level bytes (byte-SIMD, no carries: Q_max <= 127) and refreshes the
-// blocked bits of the touched words.
+//     level[t]  u8 x4      Q_t per tick + bias, bias = 0x7F - (Q_max - min Q):
+//                          bit 7 of a byte  <=>  Q_t > Q_max - min Q
+//     blocked   1 bit/tick copy of those bits: no op fits at that tick
+//   The earliest t >= t0 with p un-blocked ticks is found on a 32-tick window
+//   of `blocked` (run test by shifts/ands); ops with q > min Q verify the bytes.
+//   Commit adds q to p bytes (byte SIMD, no carries since Q_max <= 127) and
+//   ORs their bit-7 flags into `blocked`.
 #include "device_util.cuh"
 
 namespace edffs {
@@ -37,6 +42,18 @@ __device__ __forceinline__ uint32_t lds(uint32_t a) {
 __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+// lane-interleaved u16 element v: word v/2, half v%2
+__device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
+  return base + ((v >> 1) << 7) + ((v & 1u) << 1);
+}
 
 // bit i set iff bits i..i+p-1 of b are set, 1 <= p <= 32 (no divergence on p)
 __device__ __forceinline__ uint32_t runs_var(uint32_t b, int p) {
@@ -47,50 +64,159 @@ __device__ __forceinline__ uint32_t runs_var(uint32_t b, int p) {
   return fk & (fk >> (p - (1 << lg)));
 }
 
+// the four bit-7 byte flags of v packed into a nibble
+__device__ __forceinline__ uint32_t flag_nibble(uint32_t v) {
+  return ((v & 0x80808080u) * 0x00204081u) >> 28;
+}
+
+// runs_var for 1 <= p <= 8 without branches: doubling steps masked by p
+__device__ __forceinline__ uint32_t runs_p8(uint32_t b, int p) {
+  b &= (b >> 1) | (uint32_t)((p - 2) >> 31);   // runs >= 2 (skipped when p < 2)
+  b &= (b >> 2) | (uint32_t)((p - 4) >> 31);   // runs >= 4
+  b &= (b >> 4) | (uint32_t)((p - 8) >> 31);   // runs >= 8
+  const int k = 1 << (31 - __clz(p));
+  return b & (b >> (p - k));
+}
+
 // ---------------------------------------------------------------------------
-// Algorithm 1: one warp per chromosome, 32 chromosomes ("tile") per CTA pass;
-// the tile's orders are written transposed (lane-interleaved) to ordg.
+// Algorithm 1: one WARP per chromosome (2 genes per lane per 64-gene tile),
+// 32 chromosomes per CTA; the CTA writes the tile's orders lane-interleaved.
+//   pass A  pm(g) = min y over the job's pending stages <= s (segmented warp
+//           scan, segments start at each job's first pending gene);
+//           hist[pm - 1] += 1  (shared atomics on u16 halves of u32 words)
+//   pass C  start[v] = #genes with pm > v + 1 (exclusive suffix sum)
+//   pass D  rank(g) = start[pm(g) - 1] + (g - position of g's run leader),
+//           leaders being the genes with pm == y (new prefix minima)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024, 1) order_kernel(EvalArgs a, uint32_t ord_stride, uint32_t ord_per_warp,
-                                                        uint16_t *ordg) {
+struct OrdArgs {
+  const int8_t *x;
+  const int16_t *y;
+  int64_t first, count;
+  int32_t K;
+  const uint32_t *head;    // [ceil(K/32)] bit g: first pending gene of its job
+  const uint32_t *gbase;   // [K] (j*G + s)*O
+  uint16_t *ordg;
+  uint32_t hist_bytes;     // per warp
+  uint32_t ord_stride;     // bytes between staged ord arrays (8 * odd)
+};
+
+// (v, f) segmented-min combine of an inclusive scan (f = segment head seen)
+__device__ __forceinline__ void segmin_scan(int &v, uint32_t &f, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int vn = __shfl_up_sync(FULL, v, d);
+    const uint32_t fn = __shfl_up_sync(FULL, f, d);
+    if (lane >= d) {
+      if (!f) v = min(v, vn);
+      f |= fn;
+    }
+  }
+}
+
+// prefix minima of the lane's two genes given the running min before the tile
+__device__ __forceinline__ void pm_pair(int y0, int y1, uint32_t h0, uint32_t h1, int carry, int lane, int &pm0,
+                                        int &pm1) {
+  int v = h1 ? y1 : min(y0, y1);
+  uint32_t f = h0 | h1;
+  segmin_scan(v, f, lane);
+  int vex = __shfl_up_sync(FULL, v, 1);
+  uint32_t fex = __shfl_up_sync(FULL, f, 1);
+  const int pre = lane == 0 ? carry : (fex ? vex : min(vex, carry));
+  pm0 = h0 ? y0 : min(pre, y0);
+  pm1 = h1 ? y1 : min(pm0, y1);
+}
+
+__global__ void __launch_bounds__(1024, 2) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  const uint32_t img_bytes = ((const ImageHdr *)a.image)->image_bytes;
-  stage_image(smem, a.image, img_bytes, &bar);
-  const ImageHdr &h = *(const ImageHdr *)smem;
-  const int K = h.K, nt = (K + 31) >> 5, KQ = (K + 3) >> 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  unsigned char *ordbase = smem + img_bytes;
-  unsigned char *scr = ordbase + 32 * ord_stride + (size_t)warp * ord_per_warp;
-  OrderMem om;
-  om.lbits = (uint32_t *)scr;
-  om.cnt = (uint16_t *)(scr + ((4u * nt + 15u) & ~15u));
+  const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 63) >> 6;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *hist = (uint32_t *)(smem + (size_t)warp * a.hist_bytes);          // u16 pairs
+  unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
+  uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
   const int64_t ntile = (a.count + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-    for (int cc = warp; cc < 32; cc += nwarps) {
-      const int64_t c = tile * 32 + cc;
-      if (c < a.count) {
-        om.ord = ordbase + cc * ord_stride;
-        const int64_t gc = a.first + c;
-        build_order<1>(h, smem, om, a.x + gc * K, a.y + gc * K, lane);
+    const int64_t c = tile * 32 + warp;
+    if (c < a.count) {
+      const int16_t *yr = a.y + (a.first + c) * K;
+      const int8_t *xr = a.x + (a.first + c) * K;
+      for (int i = lane; i < (K + 1) >> 1; i += 32) hist[i] = 0u;
+      __syncwarp();
+      // ---- pass A
+      int carry = INT_MAX;
+      for (int t = 0; t < NT; ++t) {
+        const int g0 = (t << 6) + 2 * lane, g1 = g0 + 1;
+        const int y0 = g0 < K ? (int)__ldg(yr + g0) : INT_MAX;
+        const int y1 = g1 < K ? (int)__ldg(yr + g1) : INT_MAX;
+        const uint32_t hw = __ldg(a.head + (g0 >> 5));
+        const uint32_t h0 = g0 < K ? (hw >> (g0 & 31)) & 1u : 1u, h1 = g1 < K ? (hw >> (g1 & 31)) & 1u : 1u;
+        int pm0, pm1;
+        pm_pair(y0, y1, h0, h1, carry, lane, pm0, pm1);
+        if ((unsigned)(pm0 - 1) < (unsigned)K) atomicAdd(&hist[(pm0 - 1) >> 1], 1u << (((pm0 - 1) & 1) << 4));
+        if (g1 < K && (unsigned)(pm1 - 1) < (unsigned)K)
+          atomicAdd(&hist[(pm1 - 1) >> 1], 1u << (((pm1 - 1) & 1) << 4));
+        carry = __shfl_sync(FULL, pm1, 31);
+      }
+      __syncwarp();
+      // ---- pass C: over u = K-1-v ascending, two values per lane
+      uint32_t acc = 0;
+      uint16_t *h16 = (uint16_t *)hist;
+      for (int t = 0; t < NT; ++t) {
+        const int u0 = (t << 6) + 2 * lane;
+        const int va = K - 1 - u0, vb = va - 1;
+        const uint32_t ca = va >= 0 ? h16[va] : 0u, cb = vb >= 0 ? h16[vb] : 0u;
+        uint32_t incl = ca + cb;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t n = __shfl_up_sync(FULL, incl, d);
+          if (lane >= d) incl += n;
+        }
+        const uint32_t pre = acc + incl - ca - cb;
+        if (va >= 0) h16[va] = (uint16_t)pre;
+        if (vb >= 0) h16[vb] = (uint16_t)(pre + ca);
+        acc += __shfl_sync(FULL, incl, 31);
+      }
+      __syncwarp();
+      // ---- pass D
+      carry = INT_MAX;
+      int carry_lp = -1;
+      for (int t = 0; t < NT; ++t) {
+        const int g0 = (t << 6) + 2 * lane, g1 = g0 + 1;
+        const int y0 = g0 < K ? (int)__ldg(yr + g0) : INT_MAX;
+        const int y1 = g1 < K ? (int)__ldg(yr + g1) : INT_MAX;
+        const uint32_t hw = __ldg(a.head + (g0 >> 5));
+        const uint32_t h0 = g0 < K ? (hw >> (g0 & 31)) & 1u : 1u, h1 = g1 < K ? (hw >> (g1 & 31)) & 1u : 1u;
+        int pm0, pm1;
+        pm_pair(y0, y1, h0, h1, carry, lane, pm0, pm1);
+        const bool l0 = g0 < K && pm0 == y0, l1 = g1 < K && pm1 == y1;
+        int lp = l1 ? g1 : (l0 ? g0 : -1);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int n = __shfl_up_sync(FULL, lp, d);
+          if (lane >= d) lp = max(lp, n);
+        }
+        int lpex = __shfl_up_sync(FULL, lp, 1);
+        lpex = lane == 0 ? carry_lp : max(lpex, carry_lp);
+        const int lp0 = l0 ? g0 : lpex;
+        const int lp1 = l1 ? g1 : lp0;
+        if (g0 < K && (unsigned)(pm0 - 1) < (unsigned)K) {
+          const int r = (int)h16[pm0 - 1] + (g0 - lp0);
+          if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g0) + (uint32_t)(uint8_t)__ldg(xr + g0));
+        }
+        if (g1 < K && (unsigned)(pm1 - 1) < (unsigned)K) {
+          const int r = (int)h16[pm1 - 1] + (g1 - lp1);
+          if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g1) + (uint32_t)(uint8_t)__ldg(xr + g1));
+        }
+        carry = __shfl_sync(FULL, pm1, 31);
+        carry_lp = max(carry_lp, __shfl_sync(FULL, lp, 31));
       }
     }
     __syncthreads();
-    // transposed write: element (q, cc, k) = order of chromosome cc at rank 4q + k
-    uint16_t *dst = ordg + tile * (int64_t)KQ * 128;
+    // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome cc
+    uint2 *dst = (uint2 *)(a.ordg + tile * (int64_t)KQ * 128);
+    const int nrows = (int)min((int64_t)32, a.count - tile * 32);
     for (int idx = threadIdx.x; idx < KQ * 32; idx += blockDim.x) {
       const int qd = idx >> 5, cc = idx & 31;
-      const uint16_t *src = (const uint16_t *)(ordbase + cc * ord_stride);
-      uint16_t v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int r = 4 * qd + k;
-        v[k] = r < K ? src[r] : (uint16_t)0;
-      }
-      uint2 pk;
-      pk.x = (uint32_t)v[0] | ((uint32_t)v[1] << 16);
-      pk.y = (uint32_t)v[2] | ((uint32_t)v[3] << 16);
-      *(uint2 *)(dst + (size_t)idx * 4) = pk;
+      if (cc < nrows) dst[idx] = *(const uint2 *)(ordb + (size_t)cc * a.ord_stride + (size_t)qd * 8);
     }
     __syncthreads();
   }
@@ -106,28 +232,28 @@ struct LaneCtx {
 };
 __device__ __forceinline__ uint32_t waddr(const LaneCtx &L, int w) { return L.base + ((uint32_t)w << 7); }
 
-// earliest start >= t with p free ticks; general==true also checks q > min Q
-// against the level bytes (threshold thr = Q_max - q)
-__device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int thr, bool general) {
+// Slow path (window miss, or q > min Q): earliest start >= t with p ticks
+// that are un-blocked and, for general q, whose biased bytes b satisfy
+// b + (q - qmin) < 0x80  (i.e. Q_t + q <= Q_max).
+__device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int dq, uint32_t bias4) {
   const int LB = L.RW + L.MW, BB = LB + L.LW;
-  const uint32_t KT = (uint32_t)(0x7F - thr) * 0x01010101u;
+  const uint32_t KT = (uint32_t)dq * 0x01010101u;
   for (;;) {
     const int bw = t >> 5;
     uint32_t b0 = bw < L.BW ? lds(waddr(L, BB + bw)) : 0u;
     uint32_t b1 = bw + 1 < L.BW ? lds(waddr(L, BB + bw + 1)) : 0u;
-    uint32_t fr = ~__funnelshift_r(b0, b1, t & 31);
-    uint32_t f = runs_var(fr, p);
+    uint32_t f = runs_var(~__funnelshift_r(b0, b1, t & 31), p);
     if (f == 0u) {
       t += 33 - p;
       continue;
     }
     const int cand = t + __ffs(f) - 1;
-    if (!general) return cand;
+    if (dq == 0) return cand;
     int bad = -1;
     for (int w = cand >> 2; w <= (cand + p - 1) >> 2 && bad < 0; ++w) {
       const int lo = max(cand - 4 * w, 0), hi = min(cand + p - 4 * w, 4);
       const uint32_t bm = (0xFFFFFFFFu << (lo << 3)) & (0xFFFFFFFFu >> ((4 - hi) << 3));
-      const uint32_t v = w < L.LW ? lds(waddr(L, LB + w)) : 0u;
+      const uint32_t v = w < L.LW ? lds(waddr(L, LB + w)) : bias4;
       const uint32_t fl = (v + KT) & 0x80808080u & bm;
       if (fl) bad = 4 * w + ((__ffs(fl) - 1) >> 3);
     }
@@ -137,10 +263,10 @@ __device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int thr, 
 }
 
 template <bool UQ, bool SCHED>
-__global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
+__global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
-  const uint32_t img_bytes = ((const ImageHdr *)a.image)->image_bytes;
+  const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
   const ImageHdr &h = *(const ImageHdr *)smem;
   const int K = h.K, KQ = (K + 3) >> 2, GO = h.G * h.O;
@@ -157,8 +283,9 @@ __global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t
   const uint32_t *r16 = (const uint32_t *)(smem + h.off_ready16);
   const uint32_t *m16 = (const uint32_t *)(smem + h.off_mfree16);
   const uint32_t *lv0 = (const uint32_t *)(smem + h.off_lvl0);
-  const uint32_t KM = (uint32_t)(0x7F - h.thr_min) * 0x01010101u;
-  const int qmin = h.q_max - h.thr_min;
+  const int qmin = h.q_max - h.thr_min, lvw0 = h.lvl_words0;
+  const uint32_t bias4 = (uint32_t)(0x7F - h.thr_min) * 0x01010101u;
+  const int hcap = L.hcap, BW = L.BW;
   const int64_t ntile = (a.count + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
@@ -168,13 +295,10 @@ __global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t
     // --- initial state: ready/machine times, profile of the RUNNING ops
     for (int w = 0; w < L.RW; ++w) sts(waddr(L, w), r16[w]);
     for (int w = 0; w < L.MW; ++w) sts(waddr(L, L.RW + w), m16[w]);
-    for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), w < h.lvl_words0 ? lv0[w] : 0u);
-    for (int w = 0; w < L.BW; ++w) {
+    for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
+    for (int w = 0; w < BW; ++w) {
       uint32_t bits = 0;
-      for (int k = 0; k < 8; ++k) {
-        int lw = 8 * w + k;
-        if (lw < h.lvl_words0) bits |= (((((lv0[lw] + KM) & 0x80808080u) * 0x00204081u) >> 28) << (4 * k));
-      }
+      for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
       sts(waddr(L, BB + w), bits);
     }
     int32_t *srow = nullptr;
@@ -182,17 +306,18 @@ __global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t
       srow = a.start_out + gc * h.cells;
       for (int k = 0; k < h.cells; ++k) srow[k] = a.fstart[k];
     }
+    bool live = active;            // false when inactive or overflowed
     bool ovf = false;
     const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
     for (int qd = 0; qd < KQ; ++qd) {
       uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      const int nk = min(4, K - 4 * qd);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int r = 4 * qd + k;
         const uint32_t e = (k < 2 ? (k == 0 ? cur.x : cur.x >> 16) : (k == 2 ? cur.y : cur.y >> 16)) & 0xFFFFu;
-        if (active && !ovf && r < K) {
+        if (live && k < nk) {
           const uint32_t tv = pqt[e];
           const int p = (int)(tv & 0xFFu), q = (int)((tv >> 8) & 0xFFu), j = (int)(tv >> 16);
           const int mi = (int)e - j * GO;
@@ -201,33 +326,39 @@ __global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t
           const int rsh = (j & 1) << 4, msh = (mi & 1) << 4;
           // t0 = max(RS, release / predecessor completion, machine free)
           const int t0 = max((int)((rw >> rsh) & 0xFFFFu), (int)((mw >> msh) & 0xFFFFu));
+          // first run of p un-blocked ticks in the 32-tick window at t0
           const int bw = t0 >> 5;
-          const uint32_t b0 = bw < L.BW ? lds(waddr(L, BB + bw)) : 0u;
-          const uint32_t b1 = bw + 1 < L.BW ? lds(waddr(L, BB + bw + 1)) : 0u;
-          const uint32_t win = __funnelshift_r(b0, b1, t0 & 31);
-          const uint32_t pm = 0xFFFFFFFFu >> (32 - p);
-          int S = t0;
-          if ((win & pm) != 0u || (!UQ && q != qmin)) S = lane_search(L, t0, p, h.q_max - q, !UQ && q != qmin);
+          const uint32_t b0 = bw < BW ? lds(waddr(L, BB + bw)) : 0u;
+          const uint32_t b1 = bw + 1 < BW ? lds(waddr(L, BB + bw + 1)) : 0u;
+          const uint32_t f = runs_p8(~__funnelshift_r(b0, b1, t0 & 31), p);
+          int S = t0 + __ffs(f) - 1;
+          if (f == 0u || (!UQ && q != qmin)) S = lane_search(L, t0, p, UQ ? 0 : q - qmin, bias4);
           const int C = S + p;
-          if (C > L.hcap) {
+          if (C > hcap) {
             ovf = true;
+            live = false;
           } else {
-            // commit: level += q on [S, C), refresh blocked bits
+            // commit (p <= 8): bytes [S, C) lie in words w0..w0+2; untouched
+            // words get +0 (the words after them are this lane's own state)
             const uint32_t QQ = (uint32_t)q * 0x01010101u;
-            const int w0 = S >> 2, w1 = (C - 1) >> 2, bw0 = S >> 5;
-            uint64_t acc = 0;
-            for (int w = w0; w <= w1; ++w) {
-              const int lo = max(S - 4 * w, 0), hi = min(C - 4 * w, 4);
-              const uint32_t bm = (0xFFFFFFFFu << (lo << 3)) & (0xFFFFFFFFu >> ((4 - hi) << 3));
-              const uint32_t la = waddr(L, LB + w);
-              const uint32_t v = lds(la) + (QQ & bm);
-              sts(la, v);
-              const uint32_t nib = (((v + KM) & 0x80808080u) * 0x00204081u) >> 28;
-              acc |= (uint64_t)nib << ((w - (bw0 << 3)) << 2);
-            }
-            const uint32_t ba = waddr(L, BB + bw0);
-            sts(ba, lds(ba) | (uint32_t)acc);
-            if (acc >> 32) sts(ba + 128, lds(ba + 128) | (uint32_t)(acc >> 32));
+            const int lo = S & 3, w0 = S >> 2, ee = lo + p;
+            const uint32_t m0 = (0xFFFFFFFFu << (lo << 3)) & (0xFFFFFFFFu >> ((4 - min(ee, 4)) << 3));
+            const uint32_t m1 = ee > 4 ? 0xFFFFFFFFu >> ((4 - min(ee - 4, 4)) << 3) : 0u;
+            const uint32_t m2 = ee > 8 ? 0xFFFFFFFFu >> ((12 - ee) << 3) : 0u;
+            const uint32_t a0 = waddr(L, LB + w0);
+            const uint32_t v0 = lds(a0) + (QQ & m0);
+            const uint32_t v1 = lds(a0 + 128) + (QQ & m1);
+            const uint32_t v2 = lds(a0 + 256) + (QQ & m2);
+            sts(a0, v0);
+            sts(a0 + 128, v1);
+            sts(a0 + 256, v2);
+            const uint32_t nib = flag_nibble(v0) | (m1 ? flag_nibble(v1) << 4 : 0u) | (m2 ? flag_nibble(v2) << 8 : 0u);
+            const int sh = (w0 & 7) << 2;
+            const uint32_t ba = waddr(L, BB + (w0 >> 3));
+            const uint32_t spill = sh ? nib >> (32 - sh) : 0u;
+            const uint32_t B0 = lds(ba);
+            sts(ba, B0 | (nib << sh));
+            if ((w0 >> 3) + 1 < BW) sts(ba + 128, lds(ba + 128) | spill);   // stay inside this lane's words
             sts(ra, (rw & ~(0xFFFFu << rsh)) | ((uint32_t)C << rsh));
             sts(ma, (mw & ~(0xFFFFu << msh)) | ((uint32_t)C << msh));
             if (SCHED) srow[e / h.O] = S + h.rs;
@@ -261,8 +392,8 @@ __global__ void __launch_bounds__(256, 1) lane_decode_kernel(EvalArgs a, int32_t
     if (a.tard) a.tard[gc] = T;
     if (a.cmax) a.cmax[gc] = cm;
     if (a.fit) {  // Eq. (13)
-      int64_t f = *a.emax - obj;
-      a.fit[gc] = f > 0 ? f : 0;
+      int64_t fv = *a.emax - obj;
+      a.fit[gc] = fv > 0 ? fv : 0;
     }
   }
 }
@@ -290,7 +421,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     scr.ordg_elems = elems;
   }
   static size_t a_ord = 0, a_l00 = 0, a_l01 = 0, a_l10 = 0, a_l11 = 0;
-  ffs_status e = smem_attr(order_kernel, st.ord_smem, a_ord);
+  ffs_status e = smem_attr(order_warp_kernel, st.ord_smem, a_ord);
   if (e != FFS_OK) return e;
   const bool uq = ((const ImageHdr *)st.image_host.data())->uniform_q != 0;
   const bool sched = a0.start_out != nullptr;
@@ -299,7 +430,6 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   else if (sched) e = smem_attr(lane_decode_kernel<false, true>, st.lane_smem, a_l01);
   else e = smem_attr(lane_decode_kernel<false, false>, st.lane_smem, a_l00);
   if (e != FFS_OK) return e;
-  const int ord_ctas_per_sm = (int)std::max<size_t>(1, (kSmemLimit + 1024) / (st.ord_smem + 1024));
   for (int64_t first = 0; first < a0.count; first += chunk) {
     EvalArgs a = a0;
     a.first = first;
@@ -308,9 +438,20 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     a.h_cap = st.lane_hcap;
     a.ovf = scr.list;
     const int64_t ntile = (a.count + 31) / 32;
-    int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * ord_ctas_per_sm);
-    order_kernel<<<(unsigned)og, st.ord_warps * 32, st.ord_smem, s>>>(a, st.ord_stride, (uint32_t)st.ord_per_warp,
-                                                                      scr.ordg);
+    OrdArgs oa;
+    oa.x = a0.x;
+    oa.y = a0.y;
+    oa.first = first;
+    oa.count = a.count;
+    oa.K = K;
+    oa.head = (const uint32_t *)((const unsigned char *)st.image_dev +
+                                 ((const ImageHdr *)st.image_host.data())->off_head);
+    oa.gbase = st.gbase_dev;
+    oa.ordg = scr.ordg;
+    oa.hist_bytes = (uint32_t)st.ord_hist_bytes;
+    oa.ord_stride = (uint32_t)st.ord_stride;
+    int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
+    order_warp_kernel<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
     FFS_CUDA(cudaGetLastError());
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);

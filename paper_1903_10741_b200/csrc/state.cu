@@ -131,19 +131,21 @@ ffs_status State::build_image() {
   H.K = K; H.NJ = NJ; H.G = G; H.O = O; H.rs = rs; H.q_max = in.q_max;
   H.n_pjobs = (int32_t)pjob.size();
   H.wt = in.wt; H.frozen_T = frozen_T; H.frozen_cmax = (int32_t)frozen_cmax; H.cells = cells;
-  H.off_pq = off; off += r16((uint64_t)NJ * G * O * 4);
-  H.off_ginfo = off; off += r16((uint64_t)K * 4);
-  H.off_head = off; off += r16((uint64_t)nt * 4);
-  H.off_ready0 = off; off += r16((uint64_t)NJ * 4);
-  H.off_mfree0 = off; off += r16((uint64_t)G * O * 4);
+  // lane-decode prefix (staged by the lane kernels), then warp-path tables
+  H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
+  H.off_ready16 = off; off += r16((uint64_t)((NJ + 1) / 2) * 4);
+  H.off_mfree16 = off; off += r16((uint64_t)((G * O + 1) / 2) * 4);
   int64_t lvl_bytes0 = Lr * lvl_bytes;
   H.lvl_words0 = (int32_t)((lvl_bytes0 + 3) / 4);
   H.off_lvl0 = off; off += r16((uint64_t)H.lvl_words0 * 4);
   H.off_pjob = off; off += r16((uint64_t)pjob.size() * 4);
   H.off_pdue = off; off += r16((uint64_t)pjob.size() * 4);
-  H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
-  H.off_ready16 = off; off += r16((uint64_t)((NJ + 1) / 2) * 4);
-  H.off_mfree16 = off; off += r16((uint64_t)((G * O + 1) / 2) * 4);
+  H.lane_image_bytes = off;
+  H.off_head = off; off += r16((uint64_t)nt * 4);
+  H.off_pq = off; off += r16((uint64_t)NJ * G * O * 4);
+  H.off_ginfo = off; off += r16((uint64_t)K * 4);
+  H.off_ready0 = off; off += r16((uint64_t)NJ * 4);
+  H.off_mfree0 = off; off += r16((uint64_t)G * O * 4);
   int32_t qmin = in.q_max, qmaxv = 0, pmax = 0;
   for (size_t i = 0; i < in.Q.size(); ++i) {
     qmin = std::min(qmin, in.Q[i]);
@@ -221,39 +223,34 @@ ffs_status State::build_image() {
   fb_smem_bytes = H.image_bytes + (size_t)fb_warps_per_cta * fb_per_warp_bytes;
 
   // --- lane-decode path (one lane per chromosome): eligibility and geometry
-  lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 32 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
+  lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 8 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
   if (lane_ok) {
-    const int64_t lbudget = kSmemLimit - (int64_t)H.image_bytes - 256;
+    const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 256;
     const int64_t fixed_words = (NJ + 1) / 2 + (G * O + 1) / 2;
     auto words = [&](int64_t hc) { return fixed_words + hc / 4 + hc / 32; };
-    int64_t hfull = h_bound;  // multiple of 32
-    int64_t hc = hfull;
-    int warps = 8;
-    while (warps > 0 && words(hc) * 128 * warps > lbudget) {
-      // shrink the horizon first (down to 256 slots), then the warp count
-      if (hc > 256) hc = std::max<int64_t>(256, (lbudget / (128 * warps) - fixed_words) * 32 / 9 / 32 * 32);
-      if (words(hc) * 128 * warps > lbudget) --warps;
-    }
+    // horizon: the proven bound if it fits, else as large as keeps >= 8
+    // warps (overflowing chromosomes are re-decoded exactly by the fallback)
+    int64_t hc = h_bound;
+    const int target_warps = 8;
+    if (words(hc) * 128 * target_warps > lbudget)
+      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words) * 32 / 9 / 32 * 32);
     if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
-    if (warps < 2 || hc < 32) {
+    hc = std::min<int64_t>(hc, 65504);
+    int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
+    // order kernel: 32 warps, per warp hist[K] u16 + ord[K] u16 (stride 8*odd)
+    ord_hist_bytes = ((size_t)((K + 1) / 2) * 4 + 15) & ~(size_t)15;
+    ord_stride = ((size_t)K * 2 + 7) / 8 * 8;
+    if ((ord_stride / 8) % 2 == 0) ord_stride += 8;
+    ord_smem = 32 * (ord_hist_bytes + ord_stride);
+    ord_ctas_per_sm = ord_smem * 2 + 2048 <= (size_t)kSmemLimit + 1024 ? 2 : 1;
+    if (warps < 2 || hc < 32 || ord_smem > (size_t)kSmemLimit || K > 65535) {
       lane_ok = false;
     } else {
       lane_hcap = (int32_t)hc;
       lane_wpt = (int32_t)words(hc);
       lane_warps_per_cta = warps;
-      lane_smem = H.image_bytes + (size_t)warps * lane_wpt * 128;
-      lane_ctas_per_sm = (int)std::max<int64_t>(1, (int64_t)(kSmemLimit + 1024) / (int64_t)(lane_smem + 1024));
-      // order kernel: 32 staged order arrays (odd word stride: conflict-free
-      // transposed reads) + per-warp scan scratch
-      uint32_t st = r16((uint64_t)K * 2);
-      if ((st / 4) % 2 == 0) st += 4;
-      ord_stride = st;
-      ord_per_warp = r16((uint64_t)nt * 4) + r16((uint64_t)K * 2);
-      const int64_t obudget = kSmemLimit - (int64_t)H.image_bytes - 256 - 32 * (int64_t)st;
-      ord_warps = 32;
-      while (ord_warps > 1 && (int64_t)ord_per_warp * ord_warps > obudget) ord_warps /= 2;
-      if ((int64_t)ord_per_warp * ord_warps > obudget) lane_ok = false;
-      ord_smem = H.image_bytes + 32 * (size_t)st + (size_t)ord_warps * ord_per_warp;
+      lane_smem = H.lane_image_bytes + (size_t)warps * lane_wpt * 128;
+      lane_ctas_per_sm = 1;
     }
   }
 
@@ -416,7 +413,11 @@ ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_
     delete h;
     return e;
   }
-  cudaError_t ce = cudaMalloc(&st.fstart_dev, (size_t)st.cells * 4);
+  std::vector<uint32_t> gbase(std::max(st.K, 1));
+  for (int k = 0; k < st.K; ++k) gbase[k] = (uint32_t)((st.gene_job[k] * G + st.gene_stage[k]) * O);
+  cudaError_t ce = cudaMalloc(&st.gbase_dev, gbase.size() * 4);
+  if (ce == cudaSuccess) ce = cudaMemcpy(st.gbase_dev, gbase.data(), gbase.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMalloc(&st.fstart_dev, (size_t)st.cells * 4);
   if (ce == cudaSuccess) ce = cudaMemcpy(st.fstart_dev, st.fstart.data(), (size_t)st.cells * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess) ce = cudaMalloc(&st.cut_dev, (size_t)(st.cells + 1) * 4);
   if (ce == cudaSuccess)
@@ -473,6 +474,7 @@ void ffs_state_destroy(ffs_state *h) {
   if (st.image_dev) cudaFree(st.image_dev);
   if (st.fstart_dev) cudaFree(st.fstart_dev);
   if (st.cut_dev) cudaFree(st.cut_dev);
+  if (st.gbase_dev) cudaFree(st.gbase_dev);
   st.scratch.release();
   delete h;
 }
