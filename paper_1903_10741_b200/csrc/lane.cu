@@ -42,16 +42,16 @@ __device__ __forceinline__ uint32_t lds(uint32_t a) {
 __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+[[maybe_unused]] __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+[[maybe_unused]] __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 // lane-interleaved u16 element v: word v/2, half v%2
-__device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
+[[maybe_unused]] __device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
   return base + ((v >> 1) << 7) + ((v & 1u) << 1);
 }
 
@@ -98,6 +98,7 @@ struct OrdArgs {
   uint16_t *ordg;
   uint32_t hist_bytes;     // per warp
   uint32_t ord_stride;     // bytes between staged ord arrays (8 * odd)
+  uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
 };
 
 // (v, f) segmented-min combine of an inclusive scan (f = segment head seen)
@@ -113,24 +114,46 @@ __device__ __forceinline__ void segmin_scan(int &v, uint32_t &f, int lane) {
   }
 }
 
-// prefix minima of the lane's two genes given the running min before the tile
-__device__ __forceinline__ void pm_pair(int y0, int y1, uint32_t h0, uint32_t h1, int carry, int lane, int &pm0,
-                                        int &pm1) {
-  int v = h1 ? y1 : min(y0, y1);
-  uint32_t f = h0 | h1;
+// prefix minima of the lane's four genes given the running min before the tile
+__device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, int lane, int pm[4]) {
+  int v = y[0];
+  uint32_t f = h & 1u;
+#pragma unroll
+  for (int k = 1; k < 4; ++k) {
+    const bool hk = (h >> k) & 1u;
+    v = hk ? y[k] : min(v, y[k]);
+    f |= hk;
+  }
   segmin_scan(v, f, lane);
-  int vex = __shfl_up_sync(FULL, v, 1);
-  uint32_t fex = __shfl_up_sync(FULL, f, 1);
-  const int pre = lane == 0 ? carry : (fex ? vex : min(vex, carry));
-  pm0 = h0 ? y0 : min(pre, y0);
-  pm1 = h1 ? y1 : min(pm0, y1);
+  const int vex = __shfl_up_sync(FULL, v, 1);
+  const uint32_t fex = __shfl_up_sync(FULL, f, 1);
+  int run = lane == 0 ? carry : (fex ? vex : min(vex, carry));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    run = ((h >> k) & 1u) ? y[k] : min(run, y[k]);
+    pm[k] = run;
+  }
 }
 
-__global__ void __launch_bounds__(1024, 2) order_warp_kernel(OrdArgs a) {
+__device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *head, int K, int g0, int y[4],
+                                          uint32_t &h) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? (int)__ldg(yr + g0 + k) : INT_MAX;
+  const uint32_t hw = g0 < K ? __ldg(head + (g0 >> 5)) : 0u;
+  h = (hw >> (g0 & 31)) & 0xFu;
+  // genes past the end are their own segments (never merge into valid ones)
+  const int valid = K - g0;
+  if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
+}
+
+__global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 63) >> 6;
+  const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *hist = (uint32_t *)(smem + (size_t)warp * a.hist_bytes);          // u16 pairs
+  uint16_t *h16 = (uint16_t *)hist;
+  uint16_t *pmv = (uint16_t *)(smem + (size_t)32 * a.hist_bytes + (size_t)32 * a.ord_stride +
+                               (size_t)warp * a.pm_bytes);                      // [K] pm-1 | leader<<15
   unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
   const int64_t ntile = (a.count + 31) / 32;
@@ -141,72 +164,82 @@ __global__ void __launch_bounds__(1024, 2) order_warp_kernel(OrdArgs a) {
       const int8_t *xr = a.x + (a.first + c) * K;
       for (int i = lane; i < (K + 1) >> 1; i += 32) hist[i] = 0u;
       __syncwarp();
-      // ---- pass A
+      // ---- pass A: prefix minima (kept with a leader flag in bit 15), histogram
       int carry = INT_MAX;
       for (int t = 0; t < NT; ++t) {
-        const int g0 = (t << 6) + 2 * lane, g1 = g0 + 1;
-        const int y0 = g0 < K ? (int)__ldg(yr + g0) : INT_MAX;
-        const int y1 = g1 < K ? (int)__ldg(yr + g1) : INT_MAX;
-        const uint32_t hw = __ldg(a.head + (g0 >> 5));
-        const uint32_t h0 = g0 < K ? (hw >> (g0 & 31)) & 1u : 1u, h1 = g1 < K ? (hw >> (g1 & 31)) & 1u : 1u;
-        int pm0, pm1;
-        pm_pair(y0, y1, h0, h1, carry, lane, pm0, pm1);
-        if ((unsigned)(pm0 - 1) < (unsigned)K) atomicAdd(&hist[(pm0 - 1) >> 1], 1u << (((pm0 - 1) & 1) << 4));
-        if (g1 < K && (unsigned)(pm1 - 1) < (unsigned)K)
-          atomicAdd(&hist[(pm1 - 1) >> 1], 1u << (((pm1 - 1) & 1) << 4));
-        carry = __shfl_sync(FULL, pm1, 31);
+        const int g0 = (t << 7) + 4 * lane;
+        int y[4], pm[4];
+        uint32_t h;
+        load_quad(yr, a.head, K, g0, y, h);
+        pm_quad(y, h, carry, lane, pm);
+        uint32_t pk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const unsigned v = (unsigned)(pm[k] - 1);
+          const bool ok = g0 + k < K && v < (unsigned)K;
+          if (ok) atomicAdd(&hist[v >> 1], 1u << ((v & 1u) << 4));
+          pk[k] = ok ? (v | (pm[k] == y[k] ? 0x8000u : 0u)) : 0xFFFFu;
+        }
+        if (g0 < K) *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
+        carry = __shfl_sync(FULL, pm[3], 31);
       }
       __syncwarp();
-      // ---- pass C: over u = K-1-v ascending, two values per lane
+      // ---- pass C: start[v] = #genes with pm > v + 1, over u = K-1-v ascending
       uint32_t acc = 0;
-      uint16_t *h16 = (uint16_t *)hist;
       for (int t = 0; t < NT; ++t) {
-        const int u0 = (t << 6) + 2 * lane;
-        const int va = K - 1 - u0, vb = va - 1;
-        const uint32_t ca = va >= 0 ? h16[va] : 0u, cb = vb >= 0 ? h16[vb] : 0u;
-        uint32_t incl = ca + cb;
+        const int vtop = K - 1 - ((t << 7) + 4 * lane);
+        uint32_t cv[4], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          cv[k] = vtop - k >= 0 ? (uint32_t)h16[vtop - k] : 0u;
+          sum += cv[k];
+        }
+        uint32_t incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const uint32_t n = __shfl_up_sync(FULL, incl, d);
           if (lane >= d) incl += n;
         }
-        const uint32_t pre = acc + incl - ca - cb;
-        if (va >= 0) h16[va] = (uint16_t)pre;
-        if (vb >= 0) h16[vb] = (uint16_t)(pre + ca);
+        uint32_t run = acc + incl - sum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (vtop - k >= 0) h16[vtop - k] = (uint16_t)run;
+          run += cv[k];
+        }
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
-      // ---- pass D
-      carry = INT_MAX;
+      // ---- pass D: rank(g) = start[pm - 1] + (g - leader(g)); scatter
       int carry_lp = -1;
       for (int t = 0; t < NT; ++t) {
-        const int g0 = (t << 6) + 2 * lane, g1 = g0 + 1;
-        const int y0 = g0 < K ? (int)__ldg(yr + g0) : INT_MAX;
-        const int y1 = g1 < K ? (int)__ldg(yr + g1) : INT_MAX;
-        const uint32_t hw = __ldg(a.head + (g0 >> 5));
-        const uint32_t h0 = g0 < K ? (hw >> (g0 & 31)) & 1u : 1u, h1 = g1 < K ? (hw >> (g1 & 31)) & 1u : 1u;
-        int pm0, pm1;
-        pm_pair(y0, y1, h0, h1, carry, lane, pm0, pm1);
-        const bool l0 = g0 < K && pm0 == y0, l1 = g1 < K && pm1 == y1;
-        int lp = l1 ? g1 : (l0 ? g0 : -1);
+        const int g0 = (t << 7) + 4 * lane;
+        uint32_t pk[4];
+        if (g0 < K) {
+          const uint2 w = *(const uint2 *)(pmv + g0);
+          pk[0] = w.x & 0xFFFFu; pk[1] = w.x >> 16; pk[2] = w.y & 0xFFFFu; pk[3] = w.y >> 16;
+        } else {
+          pk[0] = pk[1] = pk[2] = pk[3] = 0xFFFFu;
+        }
+        int lp = -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (pk[k] != 0xFFFFu && (pk[k] & 0x8000u)) lp = g0 + k;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const int n = __shfl_up_sync(FULL, lp, d);
           if (lane >= d) lp = max(lp, n);
         }
-        int lpex = __shfl_up_sync(FULL, lp, 1);
-        lpex = lane == 0 ? carry_lp : max(lpex, carry_lp);
-        const int lp0 = l0 ? g0 : lpex;
-        const int lp1 = l1 ? g1 : lp0;
-        if (g0 < K && (unsigned)(pm0 - 1) < (unsigned)K) {
-          const int r = (int)h16[pm0 - 1] + (g0 - lp0);
-          if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g0) + (uint32_t)(uint8_t)__ldg(xr + g0));
+        int run = __shfl_up_sync(FULL, lp, 1);
+        run = lane == 0 ? carry_lp : max(run, carry_lp);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int g = g0 + k;
+          if (pk[k] != 0xFFFFu) {
+            if (pk[k] & 0x8000u) run = g;
+            const int r = (int)h16[pk[k] & 0x7FFFu] + (g - run);
+            if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g) + (uint32_t)(uint8_t)__ldg(xr + g));
+          }
         }
-        if (g1 < K && (unsigned)(pm1 - 1) < (unsigned)K) {
-          const int r = (int)h16[pm1 - 1] + (g1 - lp1);
-          if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g1) + (uint32_t)(uint8_t)__ldg(xr + g1));
-        }
-        carry = __shfl_sync(FULL, pm1, 31);
         carry_lp = max(carry_lp, __shfl_sync(FULL, lp, 31));
       }
     }
@@ -266,6 +299,16 @@ template <bool UQ, bool SCHED>
 __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ uint4 cmask[32];    // byte masks of [S, S+p) over words S/4 .. S/4+2, by (S%4, p-1)
+  if (threadIdx.x < 32) {
+    const int lo = threadIdx.x >> 3, ee = lo + (threadIdx.x & 7) + 1;
+    uint4 m;
+    m.x = (0xFFFFFFFFu << (lo << 3)) & (0xFFFFFFFFu >> ((4 - min(ee, 4)) << 3));
+    m.y = ee > 4 ? 0xFFFFFFFFu >> ((4 - min(ee - 4, 4)) << 3) : 0u;
+    m.z = ee > 8 ? 0xFFFFFFFFu >> ((12 - ee) << 3) : 0u;
+    m.w = 0u;
+    cmask[threadIdx.x] = m;
+  }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
   const ImageHdr &h = *(const ImageHdr *)smem;
@@ -301,6 +344,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
       for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
       sts(waddr(L, BB + w), bits);
     }
+    sts(waddr(L, BB + BW), 0u);
+    sts(waddr(L, BB + BW + 1), 0u);
     int32_t *srow = nullptr;
     if (SCHED && active) {
       srow = a.start_out + gc * h.cells;
@@ -327,10 +372,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
           // t0 = max(RS, release / predecessor completion, machine free)
           const int t0 = max((int)((rw >> rsh) & 0xFFFFu), (int)((mw >> msh) & 0xFFFFu));
           // first run of p un-blocked ticks in the 32-tick window at t0
-          const int bw = t0 >> 5;
-          const uint32_t b0 = bw < BW ? lds(waddr(L, BB + bw)) : 0u;
-          const uint32_t b1 = bw + 1 < BW ? lds(waddr(L, BB + bw + 1)) : 0u;
-          const uint32_t f = runs_p8(~__funnelshift_r(b0, b1, t0 & 31), p);
+          // (blocked words BW, BW+1 are zero sentinels: no bounds test)
+          const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
+          const uint32_t f = runs_p8(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), p);
           int S = t0 + __ffs(f) - 1;
           if (f == 0u || (!UQ && q != qmin)) S = lane_search(L, t0, p, UQ ? 0 : q - qmin, bias4);
           const int C = S + p;
@@ -341,18 +385,17 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             // commit (p <= 8): bytes [S, C) lie in words w0..w0+2; untouched
             // words get +0 (the words after them are this lane's own state)
             const uint32_t QQ = (uint32_t)q * 0x01010101u;
-            const int lo = S & 3, w0 = S >> 2, ee = lo + p;
-            const uint32_t m0 = (0xFFFFFFFFu << (lo << 3)) & (0xFFFFFFFFu >> ((4 - min(ee, 4)) << 3));
-            const uint32_t m1 = ee > 4 ? 0xFFFFFFFFu >> ((4 - min(ee - 4, 4)) << 3) : 0u;
-            const uint32_t m2 = ee > 8 ? 0xFFFFFFFFu >> ((12 - ee) << 3) : 0u;
+            const int w0 = S >> 2;
+            const uint4 mk = cmask[((S & 3) << 3) + p - 1];
             const uint32_t a0 = waddr(L, LB + w0);
-            const uint32_t v0 = lds(a0) + (QQ & m0);
-            const uint32_t v1 = lds(a0 + 128) + (QQ & m1);
-            const uint32_t v2 = lds(a0 + 256) + (QQ & m2);
+            const uint32_t v0 = lds(a0) + (QQ & mk.x);
+            const uint32_t v1 = lds(a0 + 128) + (QQ & mk.y);
+            const uint32_t v2 = lds(a0 + 256) + (QQ & mk.z);
             sts(a0, v0);
             sts(a0 + 128, v1);
             sts(a0 + 256, v2);
-            const uint32_t nib = flag_nibble(v0) | (m1 ? flag_nibble(v1) << 4 : 0u) | (m2 ? flag_nibble(v2) << 8 : 0u);
+            // flags of untouched words are already in `blocked`: OR-ing them is harmless
+            const uint32_t nib = flag_nibble(v0) | (flag_nibble(v1) << 4) | (flag_nibble(v2) << 8);
             const int sh = (w0 & 7) << 2;
             const uint32_t ba = waddr(L, BB + (w0 >> 3));
             const uint32_t spill = sh ? nib >> (32 - sh) : 0u;
@@ -450,6 +493,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ordg = scr.ordg;
     oa.hist_bytes = (uint32_t)st.ord_hist_bytes;
     oa.ord_stride = (uint32_t)st.ord_stride;
+    oa.pm_bytes = (uint32_t)(((size_t)K * 2 + 8 + 15) & ~(size_t)15);
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
     order_warp_kernel<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
     FFS_CUDA(cudaGetLastError());

@@ -227,7 +227,7 @@ ffs_status State::build_image() {
   if (lane_ok) {
     const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 256;
     const int64_t fixed_words = (NJ + 1) / 2 + (G * O + 1) / 2;
-    auto words = [&](int64_t hc) { return fixed_words + hc / 4 + hc / 32; };
+    auto words = [&](int64_t hc) { return fixed_words + hc / 4 + hc / 32 + 2; };   // + 2 sentinel words
     // horizon: the proven bound if it fits, else as large as keeps >= 8
     // warps (overflowing chromosomes are re-decoded exactly by the fallback)
     int64_t hc = h_bound;
@@ -241,8 +241,8 @@ ffs_status State::build_image() {
     ord_hist_bytes = ((size_t)((K + 1) / 2) * 4 + 15) & ~(size_t)15;
     ord_stride = ((size_t)K * 2 + 7) / 8 * 8;
     if ((ord_stride / 8) % 2 == 0) ord_stride += 8;
-    ord_smem = 32 * (ord_hist_bytes + ord_stride);
-    ord_ctas_per_sm = ord_smem * 2 + 2048 <= (size_t)kSmemLimit + 1024 ? 2 : 1;
+    ord_smem = 32 * (ord_hist_bytes + ord_stride + (((size_t)K * 2 + 8 + 15) & ~(size_t)15));
+    ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
     if (warps < 2 || hc < 32 || ord_smem > (size_t)kSmemLimit || K > 65535) {
       lane_ok = false;
     } else {
