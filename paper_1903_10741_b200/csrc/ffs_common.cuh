@@ -80,6 +80,21 @@ struct OvfScratch {
   void release();
 };
 
+// device staging of ffs_evaluate_host (grow-only)
+struct HostStage {
+  int8_t *x = nullptr;
+  int16_t *y = nullptr;
+  int64_t *obj = nullptr, *T = nullptr;
+  int32_t *M = nullptr;
+  int64_t cap = 0;
+  size_t gene_cap = 0;
+  void release() {
+    cudaFree(x); cudaFree(y); cudaFree(obj); cudaFree(T); cudaFree(M);
+    x = nullptr; y = nullptr; obj = nullptr; T = nullptr; M = nullptr;
+    cap = 0; gene_cap = 0;
+  }
+};
+
 struct State {
   const Instance *inst = nullptr;
   int32_t rs = 0, K = 0, cells = 0;
@@ -111,6 +126,7 @@ struct State {
   size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0;   // order kernel (32 warps per CTA)
   int ord_ctas_per_sm = 1;
   OvfScratch scratch;
+  HostStage stage;
   ffs_status build_image();
 };
 

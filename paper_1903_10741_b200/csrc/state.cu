@@ -476,6 +476,7 @@ void ffs_state_destroy(ffs_state *h) {
   if (st.cut_dev) cudaFree(st.cut_dev);
   if (st.gbase_dev) cudaFree(st.gbase_dev);
   st.scratch.release();
+  st.stage.release();
   delete h;
 }
 
@@ -502,40 +503,34 @@ ffs_status ffs_evaluate(const ffs_state *h, int64_t count, const int8_t *x, cons
 ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y,
                              int64_t *objective, int64_t *total_tardiness, int32_t *makespan, void *stream) {
   if (!h || count < 0) return fail(FFS_ERR_INVALID_ARG, "bad state or count");
-  const State &st = h->v;
+  State &st = const_cast<State &>(h->v);
   cudaSetDevice(st.inst->dev);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t gb = (size_t)count * st.K;
-  int8_t *dx = nullptr;
-  int16_t *dy = nullptr;
-  int64_t *dobj = nullptr, *dT = nullptr;
-  int32_t *dM = nullptr;
-  ffs_status rc = FFS_OK;
-  cudaError_t e = cudaMallocAsync(&dx, gb + 1, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dy, gb * 2 + 2, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dobj, (size_t)count * 8 + 8, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dT, (size_t)count * 8 + 8, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dM, (size_t)count * 4 + 4, s);
-  if (e == cudaSuccess && gb) e = cudaMemcpyAsync(dx, x, gb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && gb) e = cudaMemcpyAsync(dy, y, gb * 2, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) rc = cuda_fail(e, "evaluate_host staging");
-  if (rc == FFS_OK) rc = ffs_evaluate(h, count, dx, dy, dobj, dT, dM, nullptr, stream);
-  if (rc == FFS_OK) {
-    e = cudaSuccess;
-    if (objective) e = cudaMemcpyAsync(objective, dobj, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && total_tardiness)
-      e = cudaMemcpyAsync(total_tardiness, dT, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && makespan) e = cudaMemcpyAsync(makespan, dM, (size_t)count * 4, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) rc = cuda_fail(e, "evaluate_host copy-out");
+  // persistent device staging (grow-only), owned by the state
+  HostStage &hs = st.stage;
+  if (count > hs.cap || gb > hs.gene_cap) {
+    hs.release();
+    const size_t c = (size_t)std::max<int64_t>(count, 1), g = std::max<size_t>(gb, 1);
+    FFS_CUDA(cudaMalloc(&hs.x, g));
+    FFS_CUDA(cudaMalloc(&hs.y, g * 2));
+    FFS_CUDA(cudaMalloc(&hs.obj, c * 8));
+    FFS_CUDA(cudaMalloc(&hs.T, c * 8));
+    FFS_CUDA(cudaMalloc(&hs.M, c * 4));
+    hs.cap = (int64_t)c;
+    hs.gene_cap = g;
   }
-  cudaFreeAsync(dx, s);
-  cudaFreeAsync(dy, s);
-  cudaFreeAsync(dobj, s);
-  cudaFreeAsync(dT, s);
-  cudaFreeAsync(dM, s);
-  e = cudaStreamSynchronize(s);
-  if (rc == FFS_OK && e != cudaSuccess) rc = cuda_fail(e, "evaluate_host sync");
-  return rc;
+  if (gb) {
+    FFS_CUDA(cudaMemcpyAsync(hs.x, x, gb, cudaMemcpyHostToDevice, s));
+    FFS_CUDA(cudaMemcpyAsync(hs.y, y, gb * 2, cudaMemcpyHostToDevice, s));
+  }
+  ffs_status rc = ffs_evaluate(h, count, hs.x, hs.y, hs.obj, hs.T, hs.M, nullptr, stream);
+  if (rc != FFS_OK) return rc;
+  if (objective) FFS_CUDA(cudaMemcpyAsync(objective, hs.obj, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
+  if (total_tardiness) FFS_CUDA(cudaMemcpyAsync(total_tardiness, hs.T, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
+  if (makespan) FFS_CUDA(cudaMemcpyAsync(makespan, hs.M, (size_t)count * 4, cudaMemcpyDeviceToHost, s));
+  FFS_CUDA(cudaStreamSynchronize(s));
+  return FFS_OK;
 }
 
 ffs_status ffs_random_population(const ffs_state *h, int64_t count, uint64_t seed, int64_t first_id, int8_t *x,

@@ -58,18 +58,71 @@ def test_trajectory_parity(cfg, w, h, islands, G, every, path):
     assert nv == 0, kinds
 
 
-def test_evolve_sharded_in_process_equals_single():
-    """Two shards in one process exchange through the same ring semantics when
-    driven with islands [0,2) and [2,4) of 4 and world=1 each?  No: shards need
-    the hooks; here we only check that a shard run equals the matching slice of
-    a full run when no migration happens (G < interval)."""
+def test_two_shard_run_equals_single_gpu_run():
+    """Two shards of the product run (islands [0,2) and [2,4) of 4) driven by
+    two host threads whose collective hooks exchange device buffers through a
+    barrier: E_max allreduce + boundary-elite allgather every 10 generations
+    must reproduce the single-run trajectory exactly (the ring crosses the
+    shard boundary twice)."""
+    import threading
+    from paper_1903_10741_b200 import dist as fdist
     wl = wlmod.config_A2()
     octx, st, arr = both_event_ctx(wl)
-    full = ffs.Run(st, 4, 2, 4, 5, 77)
-    full.step(5)
-    part = ffs.Run(st, 4, 2, 4, 5, 77, island_begin=2, island_end=4)
-    part.step(5)
-    fx_, fy, fo, ff = full.population()
-    px, py, po, pf = part.population()
-    # E_max of the shard is its own (no allreduce hook); compare objectives / genes
-    assert (fx_[16:] == px).all() and (fy[16:] == py).all() and (fo[16:] == po).all()
+    G, world = 21, 2
+    full = ffs.Run(st, 4, 2, 4, G, 99)
+    full.step(G)
+    ref = full.population()
+    ref_best = full.best()
+    bar = threading.Barrier(world)
+    slots = [None] * world
+
+    def hooks(rank):
+        def allreduce(user, ptr, stream):
+            torch.cuda.synchronize()
+            t = fdist._dev_view(ptr, 1, "<i8")
+            slots[rank] = t.clone()
+            bar.wait()
+            m = torch.max(torch.stack([s_ for s_ in slots]))
+            bar.wait()
+            t.copy_(m.reshape(1))
+            torch.cuda.synchronize()
+            return 0
+
+        def allgather(user, send, recv, nbytes, stream):
+            torch.cuda.synchronize()
+            slots[rank] = fdist._dev_view(send, nbytes, "|u1").clone()
+            bar.wait()
+            r = fdist._dev_view(recv, nbytes * world, "|u1")
+            for k in range(world):
+                r[k * nbytes:(k + 1) * nbytes].copy_(slots[k])
+            torch.cuda.synchronize()
+            bar.wait()
+            return 0
+        return allreduce, allgather
+
+    out = [None] * world
+    errs = []
+
+    def drive(rank):
+        try:
+            b, e = fdist.shard(4, rank, world)
+            s = torch.cuda.Stream()
+            run = ffs.Run(st, 4, 2, 4, G, 99, island_begin=b, island_end=e, rank=rank, world=world,
+                          hooks=hooks(rank), stream=s)
+            run.step(G)
+            out[rank] = (run.population(), run.best())
+        except Exception as ex:  # pragma: no cover
+            errs.append(ex)
+            bar.abort()
+
+    th = [threading.Thread(target=drive, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(4):
+        assert (np.concatenate([out[0][0][k], out[1][0][k]]) == ref[k]).all(), k
+    tmin = np.minimum(out[0][1]["trace_min"], out[1][1]["trace_min"])
+    assert (tmin == ref_best["trace_min"]).all()
+    assert (out[0][1]["trace_sum"] + out[1][1]["trace_sum"] == ref_best["trace_sum"]).all()
