@@ -69,15 +69,6 @@ __device__ __forceinline__ uint32_t flag_nibble(uint32_t v) {
   return ((v & 0x80808080u) * 0x00204081u) >> 28;
 }
 
-// runs_var for 1 <= p <= 8 without branches: doubling steps masked by p
-__device__ __forceinline__ uint32_t runs_p8(uint32_t b, int p) {
-  b &= (b >> 1) | (uint32_t)((p - 2) >> 31);   // runs >= 2 (skipped when p < 2)
-  b &= (b >> 2) | (uint32_t)((p - 4) >> 31);   // runs >= 4
-  b &= (b >> 4) | (uint32_t)((p - 8) >> 31);   // runs >= 8
-  const int k = 1 << (31 - __clz(p));
-  return b & (b >> (p - k));
-}
-
 // ---------------------------------------------------------------------------
 // Algorithm 1: one WARP per chromosome (2 genes per lane per 64-gene tile),
 // 32 chromosomes per CTA; the CTA writes the tile's orders lane-interleaved.
@@ -162,7 +153,9 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
     if (c < a.count) {
       const int16_t *yr = a.y + (a.first + c) * K;
       const int8_t *xr = a.x + (a.first + c) * K;
-      for (int i = lane; i < (K + 1) >> 1; i += 32) hist[i] = 0u;
+      // hist/start are indexed by u = K - pm (descending prefix minimum), with
+      // a dummy slot u = K for genes past the end (no branches around atomics)
+      for (int i = lane; i < ((K + 2 + 127) >> 7) << 6; i += 32) hist[i] = 0u;
       __syncwarp();
       // ---- pass A: prefix minima (kept with a leader flag in bit 15), histogram
       int carry = INT_MAX;
@@ -177,53 +170,43 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
           const bool ok = g0 + k < K && v < (unsigned)K;
-          if (ok) atomicAdd(&hist[v >> 1], 1u << ((v & 1u) << 4));
-          pk[k] = ok ? (v | (pm[k] == y[k] ? 0x8000u : 0u)) : 0xFFFFu;
+          const unsigned u = ok ? (unsigned)K - 1u - v : (unsigned)K;
+          atomicAdd(&hist[u >> 1], 1u << ((u & 1u) << 4));
+          pk[k] = ok ? (u | (pm[k] == y[k] ? 0x8000u : 0u)) : (unsigned)K;
         }
-        if (g0 < K) *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
+        *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
         carry = __shfl_sync(FULL, pm[3], 31);
       }
       __syncwarp();
-      // ---- pass C: start[v] = #genes with pm > v + 1, over u = K-1-v ascending
+      // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u)
       uint32_t acc = 0;
       for (int t = 0; t < NT; ++t) {
-        const int vtop = K - 1 - ((t << 7) + 4 * lane);
-        uint32_t cv[4], sum = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          cv[k] = vtop - k >= 0 ? (uint32_t)h16[vtop - k] : 0u;
-          sum += cv[k];
-        }
+        const int u0 = (t << 7) + 4 * lane;
+        const uint2 w = *(const uint2 *)(h16 + u0);   // u0 % 4 == 0: 8-byte aligned
+        const uint32_t c0 = w.x & 0xFFFFu, c1 = w.x >> 16, c2 = w.y & 0xFFFFu, c3 = w.y >> 16;
+        const uint32_t sum = c0 + c1 + c2 + c3;
         uint32_t incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const uint32_t n = __shfl_up_sync(FULL, incl, d);
           if (lane >= d) incl += n;
         }
-        uint32_t run = acc + incl - sum;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (vtop - k >= 0) h16[vtop - k] = (uint16_t)run;
-          run += cv[k];
-        }
+        const uint32_t s0 = acc + incl - sum, s1 = s0 + c0, s2 = s1 + c1, s3 = s2 + c2;
+        if (u0 < K) *(uint2 *)(h16 + u0) = make_uint2(s0 | (s1 << 16), s2 | (s3 << 16));
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
-      // ---- pass D: rank(g) = start[pm - 1] + (g - leader(g)); scatter
+      // ---- pass D: rank(g) = start[u(g)] + (g - leader(g)); scatter (padding
+      // genes write to the dummy rank K)
       int carry_lp = -1;
       for (int t = 0; t < NT; ++t) {
         const int g0 = (t << 7) + 4 * lane;
-        uint32_t pk[4];
-        if (g0 < K) {
-          const uint2 w = *(const uint2 *)(pmv + g0);
-          pk[0] = w.x & 0xFFFFu; pk[1] = w.x >> 16; pk[2] = w.y & 0xFFFFu; pk[3] = w.y >> 16;
-        } else {
-          pk[0] = pk[1] = pk[2] = pk[3] = 0xFFFFu;
-        }
+        const uint2 w = *(const uint2 *)(pmv + g0);
+        const uint32_t pk[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
         int lp = -1;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (pk[k] != 0xFFFFu && (pk[k] & 0x8000u)) lp = g0 + k;
+          if (pk[k] & 0x8000u) lp = g0 + k;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const int n = __shfl_up_sync(FULL, lp, d);
@@ -234,11 +217,12 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
-          if (pk[k] != 0xFFFFu) {
-            if (pk[k] & 0x8000u) run = g;
-            const int r = (int)h16[pk[k] & 0x7FFFu] + (g - run);
-            if ((unsigned)r < (unsigned)K) ord[r] = (uint16_t)(__ldg(a.gbase + g) + (uint32_t)(uint8_t)__ldg(xr + g));
-          }
+          const bool ok = g < K;
+          if (pk[k] & 0x8000u) run = g;
+          const unsigned u = pk[k] & 0x7FFFu;          // K (dummy) for padding genes
+          const unsigned r = ok ? min((unsigned)h16[u] + (unsigned)(g - run), (unsigned)K) : (unsigned)K;
+          const int gg = ok ? g : 0;
+          ord[r] = (uint16_t)(__ldg(a.gbase + gg) + (uint32_t)(uint8_t)__ldg(xr + gg));
         }
         carry_lp = max(carry_lp, __shfl_sync(FULL, lp, 31));
       }
@@ -249,7 +233,17 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
     const int nrows = (int)min((int64_t)32, a.count - tile * 32);
     for (int idx = threadIdx.x; idx < KQ * 32; idx += blockDim.x) {
       const int qd = idx >> 5, cc = idx & 31;
-      if (cc < nrows) dst[idx] = *(const uint2 *)(ordb + (size_t)cc * a.ord_stride + (size_t)qd * 8);
+      if (cc < nrows) {
+        uint2 v = *(const uint2 *)(ordb + (size_t)cc * a.ord_stride + (size_t)qd * 8);
+        const int r0 = 4 * qd;   // ranks >= K are padding: write 0 (a valid table index)
+        if (r0 + 3 >= K) {
+          if (r0 + 0 >= K) v.x &= 0xFFFF0000u;
+          if (r0 + 1 >= K) v.x &= 0x0000FFFFu;
+          if (r0 + 2 >= K) v.y &= 0xFFFF0000u;
+          if (r0 + 3 >= K) v.y &= 0x0000FFFFu;
+        }
+        dst[idx] = v;
+      }
     }
     __syncthreads();
   }
@@ -295,8 +289,54 @@ __device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int dq, u
   }
 }
 
-template <bool UQ, bool SCHED>
+// Per-op constants that do not depend on the decode state (software-pipelined
+// one op ahead): table fields, ready/machine word addresses, and the masks of
+// the branch-free run test for this p (1 <= p <= 8).
+struct OpA {
+  uint32_t e, ra, ma, QQ, M1, M2, M4;
+  int p, q, rsh, msh, sft;
+};
+__device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
+  OpA A;
+  const uint32_t tv = pqt[e];
+  A.e = e;
+  A.p = (int)(tv & 0xFFu);
+  A.q = (int)((tv >> 8) & 0xFFu);
+  const int j = (int)(tv >> 16);
+  const int mi = (int)e - j * GO;
+  A.ra = waddr(L, j >> 1);
+  A.ma = waddr(L, L.RW + (mi >> 1));
+  A.rsh = (j & 1) << 4;
+  A.msh = (mi & 1) << 4;
+  A.QQ = (uint32_t)A.q * 0x01010101u;
+  const int pp = max(A.p, 1);
+  A.M1 = (uint32_t)((pp - 2) >> 31);   // skip the >=2 doubling step when p < 2
+  A.M2 = (uint32_t)((pp - 4) >> 31);
+  A.M4 = (uint32_t)((pp - 8) >> 31);
+  A.sft = pp - (1 << (31 - __clz(pp)));
+  return A;
+}
+
+// exact per-nibble zero test: bit 3 of each nibble set iff that nibble is 0
+__device__ __forceinline__ uint32_t zero_nibbles(uint32_t x) {
+  const uint32_t t = (x & 0x77777777u) + 0x77777777u;
+  return ~(t | x) & 0x88888888u;
+}
+// the 8 nibble flags (bits 3, 7, ..., 31) packed into 8 consecutive bits
+__device__ __forceinline__ uint32_t pack8(uint32_t z) {
+  uint32_t y = z >> 3;
+  y = (y | (y >> 3)) & 0x03030303u;
+  y = (y | (y >> 6)) & 0x000F000Fu;
+  return (y | (y >> 12)) & 0xFFu;
+}
+
+// MODE 0: byte levels, general Q; MODE 1: byte levels, uniform Q;
+// MODE 2: nibble HEADROOM Q_max - Q_t (every Q_jsm == 1, Q_max <= 15):
+//         blocked <=> headroom == 0, commit subtracts 1 per tick.
+template <int MODE, bool SCHED>
 __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
+  constexpr bool UQ = MODE != 0;
+  constexpr bool NIB = MODE == 2;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint4 cmask[32];    // byte masks of [S, S+p) over words S/4 .. S/4+2, by (S%4, p-1)
@@ -309,8 +349,16 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     m.w = 0u;
     cmask[threadIdx.x] = m;
   }
+  __shared__ uint2 nmask[64];    // nibble units of [S, S+p) over words S/8, S/8+1, by (S%8, p-1)
+  if (NIB && threadIdx.x < 64) {
+    const int lo = threadIdx.x >> 3, p = (threadIdx.x & 7) + 1;
+    uint64_t m = 0;
+    for (int i = 0; i < p; ++i) m |= 1ull << (4 * (lo + i));
+    nmask[threadIdx.x] = make_uint2((uint32_t)m, (uint32_t)(m >> 32));
+  }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
+  const uint32_t cm_base = smem_u32(cmask), nm_base = smem_u32(nmask);
   const ImageHdr &h = *(const ImageHdr *)smem;
   const int K = h.K, KQ = (K + 3) >> 2, GO = h.G * h.O;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -319,7 +367,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   L.RW = (h.NJ + 1) >> 1;
   L.MW = (GO + 1) >> 1;
   L.hcap = a.h_cap;
-  L.LW = a.h_cap >> 2;
+  L.LW = NIB ? a.h_cap >> 3 : a.h_cap >> 2;
   L.BW = a.h_cap >> 5;
   const int LB = L.RW + L.MW, BB = LB + L.LW;
   const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
@@ -335,14 +383,23 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     const int64_t c = tile * 32 + lane;
     const bool active = c < a.count;
     const int64_t gc = a.first + c;
+    const int kq_pref = active ? KQ : 0;     // prefetch bound (0 for inactive lanes)
     // --- initial state: ready/machine times, profile of the RUNNING ops
     for (int w = 0; w < L.RW; ++w) sts(waddr(L, w), r16[w]);
     for (int w = 0; w < L.MW; ++w) sts(waddr(L, L.RW + w), m16[w]);
-    for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
-    for (int w = 0; w < BW; ++w) {
-      uint32_t bits = 0;
-      for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
-      sts(waddr(L, BB + w), bits);
+    if (NIB) {
+      const uint32_t *hn0 = (const uint32_t *)(smem + h.off_hn0);
+      const uint32_t *bn0 = (const uint32_t *)(smem + h.off_bn0);
+      const uint32_t full = (uint32_t)h.q_max * 0x11111111u;
+      for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), w < h.hn_words0 ? hn0[w] : full);
+      for (int w = 0; w < BW; ++w) sts(waddr(L, BB + w), w < h.bn_words0 ? bn0[w] : 0u);
+    } else {
+      for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
+      for (int w = 0; w < BW; ++w) {
+        uint32_t bits = 0;
+        for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
+        sts(waddr(L, BB + w), bits);
+      }
     }
     sts(waddr(L, BB + BW), 0u);
     sts(waddr(L, BB + BW + 1), 0u);
@@ -354,57 +411,88 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     bool live = active;            // false when inactive or overflowed
     bool ovf = false;
     const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
+    // software pipeline: the next op's table lookup and every p-dependent
+    // constant (stage A) is computed while the current op runs (B..E)
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
+    OpA nA = stage_a(pqt, L, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
-      uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t e = (k < 2 ? (k == 0 ? cur.x : cur.x >> 16) : (k == 2 ? cur.y : cur.y >> 16)) & 0xFFFFu;
+        const OpA A = nA;
+        {   // stage A of rank 4*qd + k + 1
+          const uint32_t en = k == 0 ? cur.x >> 16 : k == 1 ? cur.y : k == 2 ? cur.y >> 16 : nxt.x;
+          nA = stage_a(pqt, L, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
+        }
         if (live && k < nk) {
-          const uint32_t tv = pqt[e];
-          const int p = (int)(tv & 0xFFu), q = (int)((tv >> 8) & 0xFFu), j = (int)(tv >> 16);
-          const int mi = (int)e - j * GO;
-          const uint32_t ra = waddr(L, j >> 1), ma = waddr(L, L.RW + (mi >> 1));
-          const uint32_t rw = lds(ra), mw = lds(ma);
-          const int rsh = (j & 1) << 4, msh = (mi & 1) << 4;
-          // t0 = max(RS, release / predecessor completion, machine free)
-          const int t0 = max((int)((rw >> rsh) & 0xFFFFu), (int)((mw >> msh) & 0xFFFFu));
-          // first run of p un-blocked ticks in the 32-tick window at t0
-          // (blocked words BW, BW+1 are zero sentinels: no bounds test)
+          // B: t0 = max(RS, release / predecessor completion, machine free)
+          const uint32_t rw = lds(A.ra), mw = lds(A.ma);
+          const int t0 = max((int)((rw >> A.rsh) & 0xFFFFu), (int)((mw >> A.msh) & 0xFFFFu));
+          // C: first run of p un-blocked ticks in the 32-tick window at t0
+          //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
           const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
-          const uint32_t f = runs_p8(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), p);
+          uint32_t f = ~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31);
+          f &= (f >> 1) | A.M1;
+          f &= (f >> 2) | A.M2;
+          f &= (f >> 4) | A.M4;
+          f &= f >> A.sft;
           int S = t0 + __ffs(f) - 1;
-          if (f == 0u || (!UQ && q != qmin)) S = lane_search(L, t0, p, UQ ? 0 : q - qmin, bias4);
-          const int C = S + p;
+          if (f == 0u || (!UQ && A.q != qmin)) S = lane_search(L, t0, A.p, UQ ? 0 : A.q - qmin, bias4);
+          const int C = S + A.p;
           if (C > hcap) {
             ovf = true;
             live = false;
           } else {
-            // commit (p <= 8): bytes [S, C) lie in words w0..w0+2; untouched
-            // words get +0 (the words after them are this lane's own state)
-            const uint32_t QQ = (uint32_t)q * 0x01010101u;
+            // E: job / machine times (the next op's loads follow in program order)
+            sts(A.ra, (rw & ~(0xFFFFu << A.rsh)) | ((uint32_t)C << A.rsh));
+            sts(A.ma, (mw & ~(0xFFFFu << A.msh)) | ((uint32_t)C << A.msh));
+            if (NIB) {
+              // D: headroom -= 1 on [S, C) (<= 2 words, p <= 8); newly
+              // exhausted ticks become blocked
+              const int w0 = S >> 3;
+              uint2 nm;
+              asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
+                           : "=r"(nm.x), "=r"(nm.y)
+                           : "r"(nm_base + ((((S & 7) << 3) + A.p - 1) << 3)));
+              const uint32_t a0 = waddr(L, LB + w0);
+              const uint32_t ba = waddr(L, BB + (w0 >> 2));
+              const uint32_t B0 = lds(ba);
+              const uint32_t v0 = lds(a0) - nm.x;
+              const uint32_t v1 = lds(a0 + 128) - nm.y;
+              sts(a0, v0);
+              sts(a0 + 128, v1);
+              const uint32_t b16 = pack8(zero_nibbles(v0)) | (pack8(zero_nibbles(v1)) << 8);
+              const int sh = (w0 & 3) << 3;
+              sts(ba, B0 | (b16 << sh));
+              const uint32_t spill = sh > 16 ? b16 >> (32 - sh) : 0u;
+              if ((w0 >> 2) + 1 < BW) sts(ba + 128, lds(ba + 128) | spill);
+              if (SCHED) srow[A.e / h.O] = S + h.rs;
+              continue;
+            }
+            // D: level += q on [S, C) (<= 3 words, p <= 8), refresh blocked bits
             const int w0 = S >> 2;
-            const uint4 mk = cmask[((S & 3) << 3) + p - 1];
+            uint4 mk;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(mk.x), "=r"(mk.y), "=r"(mk.z), "=r"(mk.w)
+                         : "r"(cm_base + ((((S & 3) << 3) + A.p - 1) << 4)));
             const uint32_t a0 = waddr(L, LB + w0);
-            const uint32_t v0 = lds(a0) + (QQ & mk.x);
-            const uint32_t v1 = lds(a0 + 128) + (QQ & mk.y);
-            const uint32_t v2 = lds(a0 + 256) + (QQ & mk.z);
+            const uint32_t ba = waddr(L, BB + (w0 >> 3));
+            const uint32_t B0 = lds(ba);
+            const uint32_t v0 = lds(a0) + (A.QQ & mk.x);
+            const uint32_t v1 = lds(a0 + 128) + (A.QQ & mk.y);
+            const uint32_t v2 = lds(a0 + 256) + (A.QQ & mk.z);
             sts(a0, v0);
             sts(a0 + 128, v1);
             sts(a0 + 256, v2);
             // flags of untouched words are already in `blocked`: OR-ing them is harmless
             const uint32_t nib = flag_nibble(v0) | (flag_nibble(v1) << 4) | (flag_nibble(v2) << 8);
             const int sh = (w0 & 7) << 2;
-            const uint32_t ba = waddr(L, BB + (w0 >> 3));
-            const uint32_t spill = sh ? nib >> (32 - sh) : 0u;
-            const uint32_t B0 = lds(ba);
             sts(ba, B0 | (nib << sh));
+            const uint32_t spill = sh ? nib >> (32 - sh) : 0u;
             if ((w0 >> 3) + 1 < BW) sts(ba + 128, lds(ba + 128) | spill);   // stay inside this lane's words
-            sts(ra, (rw & ~(0xFFFFu << rsh)) | ((uint32_t)C << rsh));
-            sts(ma, (mw & ~(0xFFFFu << msh)) | ((uint32_t)C << msh));
-            if (SCHED) srow[e / h.O] = S + h.rs;
+            if (SCHED) srow[A.e / h.O] = S + h.rs;
           }
         }
       }
@@ -463,15 +551,17 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     FFS_CUDA(cudaMalloc(&scr.ordg, (size_t)elems * 2));
     scr.ordg_elems = elems;
   }
-  static size_t a_ord = 0, a_l00 = 0, a_l01 = 0, a_l10 = 0, a_l11 = 0;
+  static size_t a_ord = 0;
   ffs_status e = smem_attr(order_warp_kernel, st.ord_smem, a_ord);
   if (e != FFS_OK) return e;
-  const bool uq = ((const ImageHdr *)st.image_host.data())->uniform_q != 0;
+  const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
-  if (uq && sched) e = smem_attr(lane_decode_kernel<true, true>, st.lane_smem, a_l11);
-  else if (uq) e = smem_attr(lane_decode_kernel<true, false>, st.lane_smem, a_l10);
-  else if (sched) e = smem_attr(lane_decode_kernel<false, true>, st.lane_smem, a_l01);
-  else e = smem_attr(lane_decode_kernel<false, false>, st.lane_smem, a_l00);
+  void (*kern)(EvalArgs, int32_t) =
+      mode == 2 ? (sched ? lane_decode_kernel<2, true> : lane_decode_kernel<2, false>)
+      : mode == 1 ? (sched ? lane_decode_kernel<1, true> : lane_decode_kernel<1, false>)
+                  : (sched ? lane_decode_kernel<0, true> : lane_decode_kernel<0, false>);
+  static size_t attr[6] = {0, 0, 0, 0, 0, 0};
+  e = smem_attr(kern, st.lane_smem, attr[mode * 2 + (sched ? 1 : 0)]);
   if (e != FFS_OK) return e;
   for (int64_t first = 0; first < a0.count; first += chunk) {
     EvalArgs a = a0;
@@ -493,17 +583,14 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ordg = scr.ordg;
     oa.hist_bytes = (uint32_t)st.ord_hist_bytes;
     oa.ord_stride = (uint32_t)st.ord_stride;
-    oa.pm_bytes = (uint32_t)(((size_t)K * 2 + 8 + 15) & ~(size_t)15);
+    oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
     order_warp_kernel<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
     FFS_CUDA(cudaGetLastError());
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);
     const unsigned thr = (unsigned)(wpc * 32);
-    if (uq && sched) lane_decode_kernel<true, true><<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
-    else if (uq) lane_decode_kernel<true, false><<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
-    else if (sched) lane_decode_kernel<false, true><<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
-    else lane_decode_kernel<false, false><<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
+    kern<<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
     FFS_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
   }

@@ -131,7 +131,21 @@ ffs_status State::build_image() {
   H.K = K; H.NJ = NJ; H.G = G; H.O = O; H.rs = rs; H.q_max = in.q_max;
   H.n_pjobs = (int32_t)pjob.size();
   H.wt = in.wt; H.frozen_T = frozen_T; H.frozen_cmax = (int32_t)frozen_cmax; H.cells = cells;
+  int32_t qmin = in.q_max, qmaxv = 0, pmax = 0;
+  for (size_t i = 0; i < in.Q.size(); ++i) {
+    qmin = std::min(qmin, in.Q[i]);
+    qmaxv = std::max(qmaxv, in.Q[i]);
+    pmax = std::max(pmax, in.P[i]);
+  }
+  const bool uq = qmin == qmaxv;
+  // lane decode profile: nibble headroom when every Q_jsm == 1 and Q_max <= 15
+  const int lmode = (uq && qmin == 1 && in.q_max <= 15) ? 2 : (uq ? 1 : 0);
   // lane-decode prefix (staged by the lane kernels), then warp-path tables
+  H.lane_mode = lmode;
+  H.hn_words0 = (int32_t)((Lr + 7) / 8);
+  H.bn_words0 = (int32_t)((Lr + 31) / 32);
+  H.off_hn0 = off; off += r16((uint64_t)H.hn_words0 * 4);
+  H.off_bn0 = off; off += r16((uint64_t)H.bn_words0 * 4);
   H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
   H.off_ready16 = off; off += r16((uint64_t)((NJ + 1) / 2) * 4);
   H.off_mfree16 = off; off += r16((uint64_t)((G * O + 1) / 2) * 4);
@@ -146,14 +160,8 @@ ffs_status State::build_image() {
   H.off_ginfo = off; off += r16((uint64_t)K * 4);
   H.off_ready0 = off; off += r16((uint64_t)NJ * 4);
   H.off_mfree0 = off; off += r16((uint64_t)G * O * 4);
-  int32_t qmin = in.q_max, qmaxv = 0, pmax = 0;
-  for (size_t i = 0; i < in.Q.size(); ++i) {
-    qmin = std::min(qmin, in.Q[i]);
-    qmaxv = std::max(qmaxv, in.Q[i]);
-    pmax = std::max(pmax, in.P[i]);
-  }
   H.thr_min = in.q_max - qmin;
-  H.uniform_q = qmin == qmaxv;
+  H.uniform_q = uq;
   H.image_bytes = off;
   image_host.assign(off, 0);
   uint8_t *img = image_host.data();
@@ -174,6 +182,18 @@ ffs_status State::build_image() {
       if (t < rq.first) L += rq.second;
     if (lvl_bytes == 1) img[H.off_lvl0 + t] = (uint8_t)L;
     else ((uint16_t *)(img + H.off_lvl0))[t] = (uint16_t)L;
+  }
+  {
+    uint32_t *hn = (uint32_t *)(img + H.off_hn0);
+    uint32_t *bn = (uint32_t *)(img + H.off_bn0);
+    for (int64_t t = 0; t < (int64_t)H.hn_words0 * 8; ++t) {
+      int64_t L = 0;
+      for (auto &rq : running)
+        if (t < rq.first) L += rq.second;
+      const int64_t hr = std::max<int64_t>(0, in.q_max - L);
+      hn[t >> 3] |= (uint32_t)(hr & 0xF) << ((t & 7) * 4);
+      if (hr == 0 && (t >> 5) < H.bn_words0) bn[t >> 5] |= 1u << (t & 31);
+    }
   }
   if (!pjob.empty()) {
     std::memcpy(img + H.off_pjob, pjob.data(), pjob.size() * 4);
@@ -225,23 +245,25 @@ ffs_status State::build_image() {
   // --- lane-decode path (one lane per chromosome): eligibility and geometry
   lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 8 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
   if (lane_ok) {
-    const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 256;
+    const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 2048;   // static smem: mask tables + mbarrier
     const int64_t fixed_words = (NJ + 1) / 2 + (G * O + 1) / 2;
-    auto words = [&](int64_t hc) { return fixed_words + hc / 4 + hc / 32 + 2; };   // + 2 sentinel words
+    auto words = [&](int64_t hc) {   // + 2 sentinel words of `blocked`
+      return fixed_words + (lmode == 2 ? hc / 8 : hc / 4) + hc / 32 + 2;
+    };
     // horizon: the proven bound if it fits, else as large as keeps >= 8
     // warps (overflowing chromosomes are re-decoded exactly by the fallback)
     int64_t hc = h_bound;
-    const int target_warps = 8;
+    const int target_warps = lmode == 2 ? 12 : 8;
     if (words(hc) * 128 * target_warps > lbudget)
-      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words) * 32 / 9 / 32 * 32);
+      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - 2) * 32 / (lmode == 2 ? 5 : 9) / 32 * 32);
     if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
     hc = std::min<int64_t>(hc, 65504);
     int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
     // order kernel: 32 warps, per warp hist[K] u16 + ord[K] u16 (stride 8*odd)
-    ord_hist_bytes = ((size_t)((K + 1) / 2) * 4 + 15) & ~(size_t)15;
-    ord_stride = ((size_t)K * 2 + 7) / 8 * 8;
+    ord_hist_bytes = ((size_t)((K + 2 + 127) / 128 * 128) * 2 + 15) & ~(size_t)15;   // u16 [K + 1], tiles of 128
+    ord_stride = ((size_t)(K + 1) * 2 + 7) / 8 * 8;                                    // ord [K] + dummy slot
     if ((ord_stride / 8) % 2 == 0) ord_stride += 8;
-    ord_smem = 32 * (ord_hist_bytes + ord_stride + (((size_t)K * 2 + 8 + 15) & ~(size_t)15));
+    ord_smem = 32 * (ord_hist_bytes + ord_stride + (((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15));
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
     if (warps < 2 || hc < 32 || ord_smem > (size_t)kSmemLimit || K > 65535) {
       lane_ok = false;

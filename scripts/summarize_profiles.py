@@ -1,0 +1,72 @@
+"""Summarise a gpu_round.sh output directory into profiles/<tag>_summary.md
+(ncu launch list shares, per-kernel ncu metrics, bench lines)."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+tag = sys.argv[1]
+src = os.path.join("gpurun_out", tag)
+out = []
+out.append(f"# Profile summary {tag}\n")
+bj = os.path.join(src, "bench.json")
+if os.path.exists(bj):
+    d = json.loads(open(bj).read().strip().splitlines()[-1])
+    out.append("## bench.py (default run)\n")
+    out.append("```json\n" + json.dumps(d, indent=1) + "\n```\n")
+rj = os.path.join(src, "bench_ref.json")
+if os.path.exists(rj):
+    lines = [l for l in open(rj).read().splitlines() if l.startswith("{")]
+    if lines:
+        out.append("## bench.py --impl reference (oracle)\n")
+        out.append("```json\n" + lines[-1] + "\n```\n")
+lc = os.path.join(src, "launches.csv")
+if os.path.exists(lc) and '"ID"' in open(lc).read():
+    txt = open(lc).read()
+    rows = list(csv.reader(io.StringIO(txt[txt.index('"ID"'):])))
+    h = rows[0]
+    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    unit = {}
+    for r in rows[1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("edffs::", "").replace("<unnamed>::", "")
+        v = float(r[vi].replace(",", ""))
+        u = r[h.index("Metric Unit")]
+        v = v / 1000.0 if u == "nsecond" else (v if u == "usecond" else v * 1000.0)
+        tot[name] += v
+        cnt[name] += 1
+    s = sum(tot.values())
+    out.append("## ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised)\n")
+    out.append("| kernel | launches | total us | share |\n|---|---|---|---|")
+    for k in sorted(tot, key=lambda k: -tot[k]):
+        out.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {100 * tot[k] / s:.1f}% |")
+    out.append("")
+want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.per_cycle_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__average_warp_latency_per_inst_issued.ratio"]
+for rep in ("prof_eval", "prof_gen"):
+    p = os.path.join(src, rep + ".ncu-rep")
+    if not os.path.exists(p):
+        continue
+    raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    out.append(f"## ncu --set full: {rep}\n")
+    out.append("| metric | " + " | ".join(r[h.index("Kernel Name")].split("(")[0][-40:] for r in rows[2:]) + " |")
+    out.append("|---|" + "---|" * (len(rows) - 2))
+    for w in want:
+        if w in h:
+            i = h.index(w)
+            out.append(f"| {w} ({units[i]}) | " + " | ".join(r[i] for r in rows[2:]) + " |")
+    out.append("")
+dst = os.path.join("profiles", f"{tag}_summary.md")
+open(dst, "w").write("\n".join(out) + "\n")
+print(dst)
