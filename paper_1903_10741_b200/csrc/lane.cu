@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 struct LaneCtx {
   uint32_t base;         // shared address of this lane's word 0
   int RW, MW, LW, BW;    // words: ready, mfree, level, blocked
+  int pack3;             // ready/mfree packing: 1 -> three 10-bit times per word, 0 -> two u16
   int hcap;
 };
 __device__ __forceinline__ uint32_t waddr(const LaneCtx &L, int w) { return L.base + ((uint32_t)w << 7); }
@@ -305,9 +306,18 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, in
   const int j = (int)(tv >> 16);
   const int mi = (int)e - j * GO;
   A.ra = waddr(L, j >> 1);
-  A.ma = waddr(L, L.RW + (mi >> 1));
-  A.rsh = (j & 1) << 4;
-  A.msh = (mi & 1) << 4;
+  if (L.pack3) {
+    const int wj = (j * 0xAAAB) >> 17, wm = (mi * 0xAAAB) >> 17;   // j / 3, mi / 3 (< 2^16)
+    A.ra = waddr(L, wj);
+    A.ma = waddr(L, L.RW + wm);
+    A.rsh = (j - 3 * wj) * 10;
+    A.msh = (mi - 3 * wm) * 10;
+  } else {
+    A.ra = waddr(L, j >> 1);
+    A.ma = waddr(L, L.RW + (mi >> 1));
+    A.rsh = (j & 1) << 4;
+    A.msh = (mi & 1) << 4;
+  }
   A.QQ = (uint32_t)A.q * 0x01010101u;
   const int pp = max(A.p, 1);
   A.M1 = (uint32_t)((pp - 2) >> 31);   // skip the >=2 doubling step when p < 2
@@ -364,8 +374,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   LaneCtx L;
   L.base = smem_u32(smem + img_bytes + (size_t)warp * lane_wpt * 128) + lane * 4;
-  L.RW = (h.NJ + 1) >> 1;
-  L.MW = (GO + 1) >> 1;
+  L.pack3 = NIB ? 1 : 0;
+  L.RW = NIB ? (h.NJ + 2) / 3 : (h.NJ + 1) >> 1;
+  L.MW = NIB ? (GO + 2) / 3 : (GO + 1) >> 1;
+  constexpr uint32_t TM = NIB ? 0x3FFu : 0xFFFFu;   // time field mask
   L.hcap = a.h_cap;
   L.LW = NIB ? a.h_cap >> 3 : a.h_cap >> 2;
   L.BW = a.h_cap >> 5;
@@ -429,7 +441,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         if (live && k < nk) {
           // B: t0 = max(RS, release / predecessor completion, machine free)
           const uint32_t rw = lds(A.ra), mw = lds(A.ma);
-          const int t0 = max((int)((rw >> A.rsh) & 0xFFFFu), (int)((mw >> A.msh) & 0xFFFFu));
+          const int t0 = max((int)((rw >> A.rsh) & TM), (int)((mw >> A.msh) & TM));
           // C: first run of p un-blocked ticks in the 32-tick window at t0
           //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
           const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
@@ -446,8 +458,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             live = false;
           } else {
             // E: job / machine times (the next op's loads follow in program order)
-            sts(A.ra, (rw & ~(0xFFFFu << A.rsh)) | ((uint32_t)C << A.rsh));
-            sts(A.ma, (mw & ~(0xFFFFu << A.msh)) | ((uint32_t)C << A.msh));
+            sts(A.ra, (rw & ~(TM << A.rsh)) | ((uint32_t)C << A.rsh));
+            sts(A.ma, (mw & ~(TM << A.msh)) | ((uint32_t)C << A.msh));
             if (NIB) {
               // D: headroom -= 1 on [S, C) (<= 2 words, p <= 8); newly
               // exhausted ticks become blocked
@@ -512,7 +524,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     int cm = h.frozen_cmax;
     for (int k = 0; k < h.n_pjobs; ++k) {
       const int j = pj[k];
-      const int Cr = (int)((lds(waddr(L, j >> 1)) >> ((j & 1) << 4)) & 0xFFFFu);
+      const int wj = NIB ? (j * 0xAAAB) >> 17 : j >> 1;
+      const int Cr = (int)((lds(waddr(L, wj)) >> (NIB ? (j - 3 * wj) * 10 : (j & 1) << 4)) & TM);
       const int tj = Cr - pd[k];
       T += tj > 0 ? tj : 0;
       cm = max(cm, Cr + h.rs);

@@ -206,10 +206,17 @@ ffs_status State::build_image() {
         size_t i = (size_t)j * G * O + so;
         pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
       }
-    uint16_t *r16p = (uint16_t *)(img + H.off_ready16);
-    for (int j = 0; j < NJ; ++j) r16p[j] = (uint16_t)std::min<int32_t>(ready0[j], 65535);
-    uint16_t *m16p = (uint16_t *)(img + H.off_mfree16);
-    for (int i = 0; i < G * O; ++i) m16p[i] = (uint16_t)std::min<int32_t>(mfree0[i], 65535);
+    if (lmode == 2) {   // three 10-bit times per word (times >= 1023 overflow to the fallback anyway)
+      uint32_t *r10 = (uint32_t *)(img + H.off_ready16);
+      for (int j = 0; j < NJ; ++j) r10[j / 3] |= (uint32_t)std::min<int32_t>(ready0[j], 1023) << ((j % 3) * 10);
+      uint32_t *m10 = (uint32_t *)(img + H.off_mfree16);
+      for (int i = 0; i < G * O; ++i) m10[i / 3] |= (uint32_t)std::min<int32_t>(mfree0[i], 1023) << ((i % 3) * 10);
+    } else {
+      uint16_t *r16p = (uint16_t *)(img + H.off_ready16);
+      for (int j = 0; j < NJ; ++j) r16p[j] = (uint16_t)std::min<int32_t>(ready0[j], 65535);
+      uint16_t *m16p = (uint16_t *)(img + H.off_mfree16);
+      for (int i = 0; i < G * O; ++i) m16p[i] = (uint16_t)std::min<int32_t>(mfree0[i], 65535);
+    }
   }
 
   // --- geometry: profile capacity and warps per CTA
@@ -246,18 +253,18 @@ ffs_status State::build_image() {
   lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 8 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
   if (lane_ok) {
     const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 2048;   // static smem: mask tables + mbarrier
-    const int64_t fixed_words = (NJ + 1) / 2 + (G * O + 1) / 2;
+    const int64_t fixed_words = lmode == 2 ? (NJ + 2) / 3 + (G * O + 2) / 3 : (NJ + 1) / 2 + (G * O + 1) / 2;
     auto words = [&](int64_t hc) {   // + 2 sentinel words of `blocked`
       return fixed_words + (lmode == 2 ? hc / 8 : hc / 4) + hc / 32 + 2;
     };
     // horizon: the proven bound if it fits, else as large as keeps >= 8
     // warps (overflowing chromosomes are re-decoded exactly by the fallback)
     int64_t hc = h_bound;
-    const int target_warps = lmode == 2 ? 12 : 8;
+    const int target_warps = lmode == 2 ? 14 : 8;
     if (words(hc) * 128 * target_warps > lbudget)
       hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - 2) * 32 / (lmode == 2 ? 5 : 9) / 32 * 32);
     if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
-    hc = std::min<int64_t>(hc, 65504);
+    hc = std::min<int64_t>(hc, lmode == 2 ? 992 : 65504);   // 10-bit times in mode 2
     int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
     // order kernel: 32 warps, per warp hist[K] u16 + ord[K] u16 (stride 8*odd)
     ord_hist_bytes = ((size_t)((K + 2 + 127) / 128 * 128) * 2 + 15) & ~(size_t)15;   // u16 [K + 1], tiles of 128
