@@ -255,7 +255,6 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 struct LaneCtx {
   uint32_t base;         // shared address of this lane's word 0
   int RW, MW, LW, BW;    // words: ready, mfree, level, blocked
-  int pack3;             // ready/mfree packing: 1 -> three 10-bit times per word, 0 -> two u16
   int hcap;
 };
 __device__ __forceinline__ uint32_t waddr(const LaneCtx &L, int w) { return L.base + ((uint32_t)w << 7); }
@@ -297,27 +296,35 @@ struct OpA {
   uint32_t e, ra, ma, QQ, M1, M2, M4;
   int p, q, rsh, msh, sft;
 };
+template <bool NIB>
 __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
   OpA A;
   const uint32_t tv = pqt[e];
   A.e = e;
+  if (NIB) {
+    // host-packed (mode 2): p-1 | ready word | field | machine word | field |
+    // run-test masks (p<2, p<4, p<8) | p - 2^floor(log2 p)
+    A.p = (int)(tv & 7u) + 1;
+    A.q = 1;
+    A.ra = waddr(L, (int)((tv >> 3) & 0x7FFu));
+    A.rsh = (int)((tv >> 14) & 3u) * 10;
+    A.ma = waddr(L, L.RW + (int)((tv >> 16) & 0x1FFu));
+    A.msh = (int)((tv >> 25) & 3u) * 10;
+    A.M1 = (uint32_t)((int32_t)(tv << 4) >> 31);
+    A.M2 = (uint32_t)((int32_t)(tv << 3) >> 31);
+    A.M4 = (uint32_t)((int32_t)(tv << 2) >> 31);
+    A.sft = (int)(tv >> 30);
+    A.QQ = 0x01010101u;
+    return A;
+  }
   A.p = (int)(tv & 0xFFu);
   A.q = (int)((tv >> 8) & 0xFFu);
   const int j = (int)(tv >> 16);
   const int mi = (int)e - j * GO;
   A.ra = waddr(L, j >> 1);
-  if (L.pack3) {
-    const int wj = (j * 0xAAAB) >> 17, wm = (mi * 0xAAAB) >> 17;   // j / 3, mi / 3 (< 2^16)
-    A.ra = waddr(L, wj);
-    A.ma = waddr(L, L.RW + wm);
-    A.rsh = (j - 3 * wj) * 10;
-    A.msh = (mi - 3 * wm) * 10;
-  } else {
-    A.ra = waddr(L, j >> 1);
-    A.ma = waddr(L, L.RW + (mi >> 1));
-    A.rsh = (j & 1) << 4;
-    A.msh = (mi & 1) << 4;
-  }
+  A.ma = waddr(L, L.RW + (mi >> 1));
+  A.rsh = (j & 1) << 4;
+  A.msh = (mi & 1) << 4;
   A.QQ = (uint32_t)A.q * 0x01010101u;
   const int pp = max(A.p, 1);
   A.M1 = (uint32_t)((pp - 2) >> 31);   // skip the >=2 doubling step when p < 2
@@ -374,7 +381,6 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   LaneCtx L;
   L.base = smem_u32(smem + img_bytes + (size_t)warp * lane_wpt * 128) + lane * 4;
-  L.pack3 = NIB ? 1 : 0;
   L.RW = NIB ? (h.NJ + 2) / 3 : (h.NJ + 1) >> 1;
   L.MW = NIB ? (GO + 2) / 3 : (GO + 1) >> 1;
   constexpr uint32_t TM = NIB ? 0x3FFu : 0xFFFFu;   // time field mask
@@ -427,7 +433,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     // constant (stage A) is computed while the current op runs (B..E)
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
-    OpA nA = stage_a(pqt, L, GO, cur.x & 0xFFFFu);
+    OpA nA = stage_a<NIB>(pqt, L, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
       const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         const OpA A = nA;
         {   // stage A of rank 4*qd + k + 1
           const uint32_t en = k == 0 ? cur.x >> 16 : k == 1 ? cur.y : k == 2 ? cur.y >> 16 : nxt.x;
-          nA = stage_a(pqt, L, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
+          nA = stage_a<NIB>(pqt, L, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
         }
         if (live && k < nk) {
           // B: t0 = max(RS, release / predecessor completion, machine free)

@@ -139,7 +139,7 @@ ffs_status State::build_image() {
   }
   const bool uq = qmin == qmaxv;
   // lane decode profile: nibble headroom when every Q_jsm == 1 and Q_max <= 15
-  const int lmode = (uq && qmin == 1 && in.q_max <= 15) ? 2 : (uq ? 1 : 0);
+  const int lmode = (uq && qmin == 1 && in.q_max <= 15 && NJ <= 6144 && G * O <= 1536) ? 2 : (uq ? 1 : 0);
   // lane-decode prefix (staged by the lane kernels), then warp-path tables
   H.lane_mode = lmode;
   H.hn_words0 = (int32_t)((Lr + 7) / 8);
@@ -204,7 +204,18 @@ ffs_status State::build_image() {
     for (int j = 0; j < NJ; ++j)
       for (int so = 0; so < G * O; ++so) {
         size_t i = (size_t)j * G * O + so;
-        pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
+        if (lmode == 2) {
+          // everything the lane decoder needs about the op, precomputed:
+          // p-1 | j/3 | j%3 | mi/3 | mi%3 | p<2 | p<4 | p<8 | p - 2^floor(log2 p)
+          const uint32_t pv = (uint32_t)in.P[i];
+          uint32_t k = 1;
+          while (2 * k <= pv) k *= 2;
+          pqt[i] = (pv - 1) | ((uint32_t)(j / 3) << 3) | ((uint32_t)(j % 3) << 14) | ((uint32_t)(so / 3) << 16) |
+                   ((uint32_t)(so % 3) << 25) | ((pv < 2 ? 1u : 0u) << 27) | ((pv < 4 ? 1u : 0u) << 28) |
+                   ((pv < 8 ? 1u : 0u) << 29) | ((pv - k) << 30);
+        } else {
+          pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
+        }
       }
     if (lmode == 2) {   // three 10-bit times per word (times >= 1023 overflow to the fallback anyway)
       uint32_t *r10 = (uint32_t *)(img + H.off_ready16);
