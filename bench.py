@@ -288,6 +288,54 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = pop_local * world / float(te.item())
 
+    # ---- config E: evaluation throughput sweep (Philox chromosomes, sharded by index)
+    sweep = []
+    for total in (10_000, 100_000, 1_000_000, 10_000_000):
+        share = (total + world - 1) // world
+        first = rank * share
+        n_loc = max(0, min(share, total - first))
+        xs, ys = ffs.random_population(st, n_loc, SEED, first_id=first, stream=stream)
+        ob = torch.empty(max(n_loc, 1), dtype=torch.int64, device=dev)
+        ffs.evaluate(st, xs, ys, ob[:n_loc], stream=stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        reps = 3 if total <= 1_000_000 else 1
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(reps):
+            ffs.evaluate(st, xs, ys, ob[:n_loc], stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ts = torch.tensor([e0.elapsed_time(e1) / 1e3 / reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        sweep.append({"population": total, "evals_per_s": total / float(ts.item()),
+                      "ms": 1e3 * float(ts.item())})
+        del xs, ys, ob
+        torch.cuda.empty_cache()
+
+    # ---- config B: predictive-reactive workflow, 3 arrival events (single GPU)
+    wf = None
+    if world == 1:
+        from paper_1903_10741_b200 import workflow as fwf
+        wlB = wlmod.config_B()
+        fwf.run_events(wlB, shape=(16, 8, 64), generations=5, seed=SEED)      # warm-up
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = fwf.run_events(wlB, shape=(16, 8, 64), generations=100, seed=SEED)
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        evs = [res.plan] + res.events
+        wf = {"workload": "B: gen-v1 30 jobs x 5 stages x 3 machines, Q_max=5; plan + 3 arrival events "
+                          "(RS at 0.25/0.50/0.75 of the plan's C_max, 7 arrivals each); 64 islands x 128 "
+                          "(16x8), 100 generations per event",
+              "seconds_total": dt, "gens_per_s": 100 * len(evs) / dt,
+              "evals_per_s": 100 * len(evs) * 8192 / dt,
+              "events": [{"rs": e.rs, "K": e.K, "objective": e.objective, "makespan": e.makespan,
+                          "seconds": e.seconds} for e in evs]}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -300,6 +348,8 @@ def run_ours(args):
                           "population": pop_local},
             "gpu_launches": launches,
             "best_objective": best["objective"],
+            "sweep_E": sweep,
+            "workflow_B": wf,
             "clocks": clk.summary(),
         }
         alg_ops = None

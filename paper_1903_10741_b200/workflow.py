@@ -1,0 +1,83 @@
+"""Predictive-reactive complete rescheduling (§4.1, Fig. 2).
+
+Host glue over the C-ABI: plan the original jobs (island GA at RS = 0), then for
+every new-job-arrival event e freeze the current plan at RS_e
+(`ffs_reschedule_state`), re-optimise every pending operation of the original
+jobs together with the new jobs (`ffs_evolve`), and merge the frozen part with
+the best schedule found (`ffs_best`): that merged plan is the "original plan"
+of the next event (reading R26).  RS_e = floor(ratio_e * C_max(original plan))
+(P:373-375).  Every step of the method runs in the sm_100a library; this module
+only sequences calls.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from . import ffs
+from .workload import Workload
+
+
+@dataclass
+class EventResult:
+    event: int
+    rs: int
+    K: int
+    objective: int
+    sum_tardiness: int
+    makespan: int
+    assign: np.ndarray
+    start: np.ndarray
+    trace_min: np.ndarray
+    trace_sum: np.ndarray
+    seconds: float
+
+
+@dataclass
+class WorkflowResult:
+    plan: EventResult
+    events: List[EventResult] = field(default_factory=list)
+
+
+def _evolve(st, shape, generations, seed, stream=None) -> EventResult:
+    w, h, islands = shape
+    t0 = time.perf_counter()
+    run = ffs.Run(st, w, h, islands, generations, seed, stream=stream)
+    run.step(generations)
+    b = run.best()
+    dt = time.perf_counter() - t0
+    return EventResult(event=-1, rs=st.rs, K=st.K, objective=b["objective"], sum_tardiness=b["sum_tardiness"],
+                       makespan=b["makespan"], assign=b["assign"], start=b["start"], trace_min=b["trace_min"],
+                       trace_sum=b["trace_sum"], seconds=dt)
+
+
+def run_events(wl: Workload, shape=(16, 8, 64), generations: int = 100, seed: int = 10741,
+               device: int = 0, stream=None) -> WorkflowResult:
+    """Config B workflow: plan at RS = 0, then one rescheduling per event."""
+    base = ffs.Instance.from_arrays(wl.original_instance(), device=device)
+    st0 = ffs.make_state(base, 0)
+    plan = _evolve(st0, shape, generations, seed, stream)
+    plan.event = 0
+    res = WorkflowResult(plan=plan)
+    c_plan = plan.makespan
+    rs_list: List[int] = []
+    cur_assign, cur_start = plan.assign, plan.start
+    keep = [base, st0]
+    for e in range(wl.n_events):
+        rs = wl.rs_from_makespan(wl.ratios[e], c_plan)
+        rs_list.append(rs)
+        arr = wl.instance_at(e, rs_list)
+        inst = ffs.Instance.from_arrays(arr, device=device)
+        st = ffs.make_state(inst, rs, cur_assign, cur_start)
+        ev = _evolve(st, shape, generations, seed + 1 + e, stream) if st.K > 0 else None
+        if ev is None:   # nothing pending: the frozen plan stands
+            assign, start, obj, T, M = ffs.decode_schedule(st, np.zeros(0, np.int8), np.zeros(0, np.int16))
+            ev = EventResult(-1, rs, 0, obj, T, M, assign, start, np.zeros(0, np.int64), np.zeros(0, np.int64), 0.0)
+        ev.event = e + 1
+        res.events.append(ev)
+        cur_assign, cur_start = ev.assign, ev.start
+        keep += [inst, st]
+    return res

@@ -1,0 +1,63 @@
+"""Predictive-reactive workflow (config B: three arrival events) -- the CUDA
+path (paper_1903_10741_b200.workflow) against the same workflow driven by the
+oracle GA: every event's RS, K, best objective, merged schedule and trace must
+be identical."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as orc
+from paper_1903_10741_b200 import workflow
+from paper_1903_10741_b200 import workload as wlmod
+from tests import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_evolve(ctx, shape, G, seed):
+    w, h, islands = shape
+    ga = orc.GA(ctx, w, h, islands, G, seed, nthreads=8)
+    for _ in range(G + 1):
+        ga.step()
+    hx, hy, hobj, hfit = ga.history()
+    b = int(np.argmax(hfit))                    # ties -> lowest island (R28)
+    r = ctx.decode_genes(hx[b], hy[b])
+    tmin, tsum = ga.trace()
+    return r, tmin, tsum
+
+
+def oracle_workflow(wl, shape, G, seed):
+    out = []
+    base = wl.original_instance()
+    c0 = orc.Ctx(fx.workload_instance(base), 0)
+    r, tmin, tsum = oracle_evolve(c0, shape, G, seed)
+    out.append((0, c0.K, r, tmin, tsum))
+    c_plan = r["makespan"]
+    rs_list = []
+    assign, start = r["assign"], r["start"]
+    for e in range(wl.n_events):
+        rs = wl.rs_from_makespan(wl.ratios[e], c_plan)
+        rs_list.append(rs)
+        arr = wl.instance_at(e, rs_list)
+        ctx = orc.Ctx(fx.workload_instance(arr), rs, assign, start)
+        r, tmin, tsum = oracle_evolve(ctx, shape, G, seed + 1 + e)
+        assert ctx.validate(r["assign"], r["start"])[0] == 0      # Eqs. (4)-(10), frozen ops kept
+        out.append((rs, ctx.K, r, tmin, tsum))
+        assign, start = r["assign"], r["start"]
+    return out
+
+
+@pytest.mark.parametrize("shape,G", [((4, 2, 4), 12), ((8, 4, 2), 11)])
+def test_config_b_workflow_parity(shape, G):
+    wl = wlmod.config_B()
+    ref = oracle_workflow(wl, shape, G, 10741)
+    got = workflow.run_events(wl, shape=shape, generations=G, seed=10741)
+    evs = [got.plan] + got.events
+    assert len(evs) == len(ref) == 4
+    for ev, (rs, K, r, tmin, tsum) in zip(evs, ref):
+        assert ev.rs == rs and ev.K == K
+        assert ev.objective == r["objective"] and ev.makespan == r["makespan"]
+        assert ev.sum_tardiness == r["sum_tardiness"]
+        assert (ev.start == r["start"]).all() and (ev.assign == r["assign"]).all()
+        assert (ev.trace_min == tmin).all() and (ev.trace_sum == tsum).all()
