@@ -413,11 +413,13 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
         if ((ma || mb) && o1 >= 1) {
           if (ma) {
             u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)ca, kg, I, k0, k1);
-            xav = (xav + 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1)) % a.O;
+            xav += 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1);   // < 2o: one conditional subtract
+            if (xav >= a.O) xav -= a.O;
           }
           if (mb) {
             u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)cb, kg, I, k0, k1);
-            xbv = (xbv + 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1)) % a.O;
+            xbv += 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1);
+            if (xbv >= a.O) xbv -= a.O;
           }
         }
         xa[g] = (int8_t)xav;

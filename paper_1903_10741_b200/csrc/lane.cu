@@ -130,7 +130,7 @@ __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *hea
                                           uint32_t &h) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? (int)__ldg(yr + g0 + k) : INT_MAX;
-  const uint32_t hw = g0 < K ? __ldg(head + (g0 >> 5)) : 0u;
+  const uint32_t hw = g0 < K ? head[g0 >> 5] : 0u;
   h = (hw >> (g0 & 31)) & 0xFu;
   // genes past the end are their own segments (never merge into valid ones)
   const int valid = K - g0;
@@ -147,6 +147,15 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
                                (size_t)warp * a.pm_bytes);                      // [K] pm-1 | leader<<15
   unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
+  // CTA-shared copies of the per-gene table base and the segment-head bits,
+  // and per-warp staging of the chromosome's machines (read once, in pass A)
+  unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
+  uint32_t *gtab = (uint32_t *)tail;
+  uint32_t *headS = gtab + ((K + 3) & ~3);
+  uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) gtab[i] = __ldg(a.gbase + i);
+  for (int i = threadIdx.x; i < 4 * NT; i += blockDim.x) headS[i] = i < ((K + 31) >> 5) ? __ldg(a.head + i) : 0u;
+  __syncthreads();
   const int64_t ntile = (a.count + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     const int64_t c = tile * 32 + warp;
@@ -163,7 +172,14 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
         uint32_t h;
-        load_quad(yr, a.head, K, g0, y, h);
+        load_quad(yr, headS, K, g0, y, h);
+        {
+          uint32_t xw = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (g0 + k < K) xw |= (uint32_t)(uint8_t)__ldg(xr + g0 + k) << (8 * k);
+          *(uint32_t *)(xs + g0) = xw;
+        }
         pm_quad(y, h, carry, lane, pm);
         uint32_t pk[4];
 #pragma unroll
@@ -222,7 +238,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const unsigned u = pk[k] & 0x7FFFu;          // K (dummy) for padding genes
           const unsigned r = ok ? min((unsigned)h16[u] + (unsigned)(g - run), (unsigned)K) : (unsigned)K;
           const int gg = ok ? g : 0;
-          ord[r] = (uint16_t)(__ldg(a.gbase + gg) + (uint32_t)(uint8_t)__ldg(xr + gg));
+          ord[r] = (uint16_t)(gtab[gg] + (uint32_t)xs[gg]);
         }
         carry_lp = max(carry_lp, __shfl_sync(FULL, lp, 31));
       }

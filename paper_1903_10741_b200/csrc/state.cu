@@ -281,7 +281,12 @@ ffs_status State::build_image() {
     ord_hist_bytes = ((size_t)((K + 2 + 127) / 128 * 128) * 2 + 15) & ~(size_t)15;   // u16 [K + 1], tiles of 128
     ord_stride = ((size_t)(K + 1) * 2 + 7) / 8 * 8;                                    // ord [K] + dummy slot
     if ((ord_stride / 8) % 2 == 0) ord_stride += 8;
-    ord_smem = 32 * (ord_hist_bytes + ord_stride + (((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15));
+    {
+      const size_t ntl = (size_t)(K + 127) / 128;
+      ord_smem = 32 * (ord_hist_bytes + ord_stride + ((ntl * 128 * 2 + 15) & ~(size_t)15)) +   // per warp
+                 (size_t)((K + 3) & ~3) * 4 + ntl * 16 +                                          // gtab, head
+                 32 * ntl * 128;                                                                  // x staging
+    }
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
     if (warps < 2 || hc < 32 || ord_smem > (size_t)kSmemLimit || K > 65535) {
       lane_ok = false;
