@@ -309,9 +309,12 @@ __device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int dq, u
 // one op ahead): table fields, ready/machine word addresses, and the masks of
 // the branch-free run test for this p (1 <= p <= 8).
 struct OpA {
-  uint32_t e, ra, ma, QQ, M1, M2, M4;
+  uint32_t e, ra, ma, QQ, M1, M2, M4, nmo;
   int p, q, rsh, msh, sft;
 };
+// keep a staged value in a register (no rematerialisation on the critical path)
+__device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
+__device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
 template <bool NIB>
 __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
   OpA A;
@@ -331,6 +334,9 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, in
     A.M4 = (uint32_t)((int32_t)(tv << 2) >> 31);
     A.sft = (int)(tv >> 30);
     A.QQ = 0x01010101u;
+    A.nmo = (uint32_t)(tv & 7u) << 3;           // (p - 1) * 8: column of the nibble-mask table
+    pin(A.ra); pin(A.ma); pin(A.rsh); pin(A.msh); pin(A.M1); pin(A.M2); pin(A.M4); pin(A.sft); pin(A.p);
+    pin(A.nmo);
     return A;
   }
   A.p = (int)(tv & 0xFFu);
@@ -347,6 +353,7 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, in
   A.M2 = (uint32_t)((pp - 4) >> 31);
   A.M4 = (uint32_t)((pp - 8) >> 31);
   A.sft = pp - (1 << (31 - __clz(pp)));
+  A.nmo = 0;
   return A;
 }
 
@@ -391,7 +398,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
-  const uint32_t cm_base = smem_u32(cmask), nm_base = smem_u32(nmask);
+  uint32_t cm_base = smem_u32(cmask), nm_base = smem_u32(nmask);
+  pin(cm_base);
+  pin(nm_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
   const int K = h.K, KQ = (K + 3) >> 2, GO = h.G * h.O;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -410,7 +419,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   const uint32_t *lv0 = (const uint32_t *)(smem + h.off_lvl0);
   const int qmin = h.q_max - h.thr_min, lvw0 = h.lvl_words0;
   const uint32_t bias4 = (uint32_t)(0x7F - h.thr_min) * 0x01010101u;
-  const int hcap = L.hcap, BW = L.BW;
+  int hcap = L.hcap, BW = L.BW;
+  pin(hcap);
+  pin(BW);
   const int64_t ntile = (a.count + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
               uint2 nm;
               asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
                            : "=r"(nm.x), "=r"(nm.y)
-                           : "r"(nm_base + ((((S & 7) << 3) + A.p - 1) << 3)));
+                           : "r"(nm_base + ((uint32_t)(S & 7) << 6) + A.nmo));
               const uint32_t a0 = waddr(L, LB + w0);
               const uint32_t ba = waddr(L, BB + (w0 >> 2));
               const uint32_t B0 = lds(ba);
