@@ -102,9 +102,25 @@ FFS_API void ffs_instance_destroy(ffs_instance *inst);
  * ---------------------------------------------------------------------- */
 FFS_API ffs_status ffs_reschedule_state(const ffs_instance *inst, int32_t rs, const int32_t *orig_assign,
                                 const int32_t *orig_start, ffs_state **out, int32_t *K_out);
+/* ------------------------------------------------------------------------
+ * Traditional static approach ("they could only be scheduled after
+ * completing the operations of the original schedule at each stage",
+ * P:313-317 Fig. 7).  Same freeze rule as
+ * ffs_reschedule_state for RUNNING / COMPLETED ops, but every other original
+ * op is KEPT at its plan (cell state 3) instead of becoming pending: only the
+ * arrivals' ops are genes (K = n'*g).  KEPT ops hold their machine and draw
+ * power over their planned interval, so every arrival op starts after the last
+ * original op on its machine (reading R29) and shares Q_max with them (R30).
+ * The same ffs_evaluate / ffs_evolve / ffs_best run on the returned state.
+ *   orig_assign, orig_start: host [n*g] plan, required when n > 0.
+ * Errors: FFS_ERR_INVALID_ARG without a plan, FFS_ERR_INVALID_SCHEDULE if the
+ * plan violates Eqs. (4)-(7).
+ * ---------------------------------------------------------------------- */
+FFS_API ffs_status ffs_static_state(const ffs_instance *inst, int32_t rs, const int32_t *orig_assign,
+                                    const int32_t *orig_start, ffs_state **out, int32_t *K_out);
 /* Host [K] arrays: job and stage of each gene (either may be NULL). */
 FFS_API ffs_status ffs_state_genes(const ffs_state *st, int32_t *gene_job, int32_t *gene_stage);
-/* Host [(n+n')*g]: 0 pending, 1 running, 2 completed. */
+/* Host [(n+n')*g]: 0 pending, 1 running, 2 completed, 3 kept (static policy). */
 FFS_API ffs_status ffs_state_cells(const ffs_state *st, int32_t *cell_state);
 /* Number of cells with row-major position < p, for p in [0, (n+n')*g]:
  * the compact cut of a row-major crossover point (R13).  Host [cells+1]. */

@@ -18,13 +18,15 @@
 
 #define Z_COMPLETED (-2)   /* the paper's "C" in Z(k) */
 #define Z_UNRANKED  (-3)
+#define Z_KEPT      (-4)   /* static baseline: original op held at its plan */
 
 struct or_ctx {
   or_instance in;
   int32_t *Pbuf, *Qbuf, *Rbuf, *Dbuf;
   int32_t rs;
   int32_t NJ, cells, K;
-  int32_t *state;      /* [cells] OR_PENDING / OR_RUNNING / OR_COMPLETED */
+  int32_t *state;      /* [cells] OR_PENDING / OR_RUNNING / OR_COMPLETED / OR_KEPT */
+  int32_t policy;      /* OR_DYNAMIC or OR_STATIC                         */
   int32_t *fassign;    /* [cells] frozen machine (plan), -1 when pending  */
   int32_t *fstart;     /* [cells] frozen start (plan), -1 when pending    */
   int32_t *gene_cell;  /* [K] pending cells in row-major order            */
@@ -112,11 +114,12 @@ static int check_instance(const or_instance *in) {
 /* ------------------------------------------------------------------ */
 /* Freeze at RS (Algorithm 1 frozen branch)                 */
 /* ------------------------------------------------------------------ */
-int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
-                  const int32_t *orig_start, or_ctx **out) {
+static int ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
+                      const int32_t *orig_start, int32_t policy, or_ctx **out) {
   int st = check_instance(inst);
   if (st != OR_OK) return st;
   if (rs < 0 || !out) return OR_ERR_ARG;
+  if (policy == OR_STATIC && inst->n > 0 && !(orig_assign && orig_start)) return OR_ERR_ARG;
   int NJ = inst->n + inst->n_prime, g = inst->g, o = inst->o;
   int cells = NJ * g;
   or_ctx *c = (or_ctx *)calloc(1, sizeof(or_ctx));
@@ -131,7 +134,7 @@ int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assig
   memcpy(c->Rbuf, inst->R, NJ * sizeof(int32_t));
   memcpy(c->Dbuf, inst->D, NJ * sizeof(int32_t));
   c->in.P = c->Pbuf; c->in.Q = c->Qbuf; c->in.R = c->Rbuf; c->in.D = c->Dbuf;
-  c->rs = rs; c->NJ = NJ; c->cells = cells;
+  c->rs = rs; c->NJ = NJ; c->cells = cells; c->policy = policy;
   c->state = (int32_t *)malloc(cells * sizeof(int32_t));
   c->fassign = (int32_t *)malloc(cells * sizeof(int32_t));
   c->fstart = (int32_t *)malloc(cells * sizeof(int32_t));
@@ -192,6 +195,10 @@ int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assig
           running_power += Qjsm(in, j, s, m);
         } else if (C <= rs) {
           c->state[cell] = OR_COMPLETED;
+        } else if (policy == OR_STATIC) {
+          /* traditional static approach (Fig. 7): the original
+           * jobs keep their schedule in full */
+          c->state[cell] = OR_KEPT;
         }
         if (c->state[cell] != OR_PENDING) { c->fassign[cell] = m; c->fstart[cell] = (int32_t)S; }
       }
@@ -206,6 +213,16 @@ int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assig
   c->K = K;
   *out = c;
   return OR_OK;
+}
+
+int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
+                  const int32_t *orig_start, or_ctx **out) {
+  return ctx_create(inst, rs, orig_assign, orig_start, OR_DYNAMIC, out);
+}
+
+int or_ctx_create_static(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
+                         const int32_t *orig_start, or_ctx **out) {
+  return ctx_create(inst, rs, orig_assign, orig_start, OR_STATIC, out);
 }
 
 void or_ctx_destroy(or_ctx *c) {
@@ -231,6 +248,7 @@ int or_order(const or_ctx *c, const int32_t *Y, int32_t *Z) {
   for (int cell = 0; cell < c->cells; ++cell) {
     if (c->state[cell] == OR_RUNNING) Z[cell] = 0;
     else if (c->state[cell] == OR_COMPLETED) Z[cell] = Z_COMPLETED;
+    else if (c->state[cell] == OR_KEPT) Z[cell] = Z_KEPT;
     else Z[cell] = Z_UNRANKED;
   }
   for (int rank = 1; rank <= c->K; ++rank) {
@@ -277,7 +295,11 @@ int or_decode(const or_ctx *c, const int32_t *X, const int32_t *Y, const int32_t
     }
 
   /* frozen operations keep their plan; RUNNING ones occupy their machine and
-   * draw power until completion (R3); COMPLETED ones are over by RS. */
+   * draw power until completion (R3); COMPLETED ones are over by RS.  In the
+   * static baseline the KEPT original ops do the same over their planned
+   * interval, so an arrival op waits for the last original op on its machine
+   * ("only be scheduled after completing the operations of the original
+   * schedule", reading R29) and shares Q_max with them (R30). */
   for (int s = 0; s < g; ++s)
     for (int m = 0; m < o; ++m) mfree[s * o + m] = rs;
   for (int cell = 0; cell < cells; ++cell) {
@@ -287,7 +309,7 @@ int or_decode(const or_ctx *c, const int32_t *X, const int32_t *Y, const int32_t
     asg[cell] = m;
     S[cell] = c->fstart[cell];
     C[cell] = S[cell] + Pjsm(in, j, s, m);
-    if (c->state[cell] == OR_RUNNING) {
+    if (c->state[cell] == OR_RUNNING || c->state[cell] == OR_KEPT) {
       iv[niv].start = S[cell]; iv[niv].end = C[cell]; iv[niv].q = Qjsm(in, j, s, m); ++niv;
       mfree[s * o + m] = max64(mfree[s * o + m], C[cell]);
     }
@@ -414,6 +436,14 @@ int or_validate(const or_ctx *c, const int32_t *assign, const int32_t *start, in
       ++nviol; kinds |= 32;
     }
   }
+  if (c->policy == OR_STATIC)     /* arrivals after the originals on each machine (R29) */
+    for (int a = 0; a < cells; ++a) {
+      if (c->state[a] != OR_PENDING) continue;
+      for (int b = 0; b < cells; ++b) {
+        if (c->state[b] == OR_PENDING || b % g != a % g || c->fassign[b] != assign[a]) continue;
+        if (start[a] < (int64_t)c->fstart[b] + Pjsm(in, b / g, b % g, c->fassign[b])) { ++nviol; kinds |= 128; }
+      }
+    }
   if (kinds_out) *kinds_out = kinds;
   return nviol;
 }
@@ -506,7 +536,8 @@ int or_brute_force(const or_ctx *c, int64_t limit, int64_t *best_objective,
   b.next_stage = (int32_t *)malloc(c->NJ * sizeof(int32_t));
   for (int cell = 0; cell < c->cells; ++cell) {
     b.X[cell] = -1;
-    b.Z[cell] = c->state[cell] == OR_RUNNING ? 0 : c->state[cell] == OR_COMPLETED ? Z_COMPLETED : Z_UNRANKED;
+    b.Z[cell] = c->state[cell] == OR_RUNNING ? 0 : c->state[cell] == OR_COMPLETED ? Z_COMPLETED
+              : c->state[cell] == OR_KEPT ? Z_KEPT : Z_UNRANKED;
   }
   for (int j = 0; j < c->NJ; ++j) {
     int s = 0;

@@ -33,6 +33,11 @@ extern "C" {
 #define OR_PENDING   0
 #define OR_RUNNING   1   /* z_js = 0  */
 #define OR_COMPLETED 2   /* z_js = C  */
+#define OR_KEPT      3   /* static baseline only: original op held at its plan */
+
+/* rescheduling policies */
+#define OR_DYNAMIC 0     /* predictive-reactive complete rescheduling (Fig. 8) */
+#define OR_STATIC  1     /* traditional static approach (Fig. 7)                */
 
 #define OR_OK 0
 #define OR_ERR_ARG 1
@@ -67,16 +72,25 @@ typedef struct {
  * (Eqs. (4)-(7)) and the power precondition. */
 int or_ctx_create(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
                   const int32_t *orig_start, or_ctx **out);
+/* Traditional static approach (Fig. 7): the
+ * original jobs keep their whole plan (OR_KEPT for the ops still pending at
+ * RS), only the new jobs' ops are genes (K = n'*g).  KEPT ops hold their
+ * machine and draw power over their planned interval, so every arrival op
+ * starts after the last original op on its machine (R29) within Q_max (R30).
+ * The plan is required when n > 0. */
+int or_ctx_create_static(const or_instance *inst, int32_t rs, const int32_t *orig_assign,
+                         const int32_t *orig_start, or_ctx **out);
 void or_ctx_destroy(or_ctx *c);
 int32_t or_ctx_K(const or_ctx *c);
 int32_t or_ctx_cells(const or_ctx *c);
-/* state per cell [(n+n')*g]: OR_PENDING/OR_RUNNING/OR_COMPLETED */
+/* state per cell [(n+n')*g]: OR_PENDING/OR_RUNNING/OR_COMPLETED/OR_KEPT */
 void or_ctx_states(const or_ctx *c, int32_t *state);
 /* canonical gene order: the pending cells in row-major order [K] */
 void or_ctx_pending_cells(const or_ctx *c, int32_t *cell_of_gene);
 
 /* Algorithm 1, greedy reading (DESIGN R1): Z[(n+n')*g] gets
- * 0 for RUNNING, -2 for COMPLETED (the paper's "C"), rank 1..K otherwise. */
+ * 0 for RUNNING, -2 for COMPLETED (the paper's "C"), -4 for KEPT, rank
+ * 1..K otherwise. */
 int or_order(const or_ctx *c, const int32_t *Y, int32_t *Z);
 
 /* Algorithm 2 decode of one chromosome.
@@ -95,7 +109,8 @@ void or_objective(const or_instance *inst, const int32_t *assign, const int32_t 
 
 /* Constraint check, Eqs. (4)-(10) + frozen ops unchanged.  Returns the
  * number of violations; kinds (bitmask, may be NULL): 1 Eq4, 2 Eq5, 4 Eq6,
- * 8 Eq7, 16 Eq10, 32 frozen op moved, 64 machine index out of range. */
+ * 8 Eq7, 16 Eq10, 32 frozen op moved, 64 machine index out of range,
+ * 128 (static policy) a new op starts before an original op on its machine ends. */
 int or_validate(const or_ctx *c, const int32_t *assign, const int32_t *start, int32_t *kinds);
 
 /* Power profile level Q_t at instant t (Eqs. (8)-(9)) of a full schedule. */

@@ -21,8 +21,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "ffs_oracle.c")
 LIB = os.path.join(HERE, "libffs_oracle.so")
 
-PENDING, RUNNING, COMPLETED = 0, 1, 2
+PENDING, RUNNING, COMPLETED, KEPT = 0, 1, 2, 3
 Z_COMPLETED = -2
+Z_KEPT = -4
 OK, ERR_ARG, ERR_INFEASIBLE, ERR_SCHEDULE, ERR_LIMIT = 0, 1, 2, 3, 4
 
 
@@ -70,6 +71,7 @@ def lib():
         _lib = C.CDLL(build())
         P = C.c_void_p
         _lib.or_ctx_create.argtypes = [C.POINTER(_Inst), C.c_int32, P, P, C.POINTER(P)]
+        _lib.or_ctx_create_static.argtypes = [C.POINTER(_Inst), C.c_int32, P, P, C.POINTER(P)]
         _lib.or_ctx_destroy.argtypes = [P]
         _lib.or_ctx_K.argtypes = [P]
         _lib.or_ctx_cells.argtypes = [P]
@@ -177,14 +179,17 @@ def power_at(inst: Instance, assign, start, t) -> int:
 class Ctx:
     """Frozen rescheduling context at RS (Algorithm 1 frozen branch)."""
 
-    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None):
+    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None, static: bool = False):
+        """static=True: the traditional static approach (Fig. 7) --
+        the originals keep their whole plan, only the new jobs are genes."""
         self.inst = inst
+        self.static = bool(static)
         self._ci = inst._c()
         self._oa = None if orig_assign is None else _i32(orig_assign).ravel()
         self._os = None if orig_start is None else _i32(orig_start).ravel()
         h = C.c_void_p()
-        _chk(lib().or_ctx_create(C.byref(self._ci), int(rs), _p(self._oa), _p(self._os),
-                                 C.byref(h)), "ctx_create")
+        create = lib().or_ctx_create_static if static else lib().or_ctx_create
+        _chk(create(C.byref(self._ci), int(rs), _p(self._oa), _p(self._os), C.byref(h)), "ctx_create")
         self.h = h
         self.rs = int(rs)
         self.K = lib().or_ctx_K(h)

@@ -96,18 +96,21 @@ ffs_status State::build_image() {
       frozen_cmax = std::max(frozen_cmax, Cj);
     }
   }
-  // machine free times and the initial profile from RUNNING ops
+  // machine free times and the initial profile from the frozen ops that end
+  // after RS: RUNNING ones (R3) and, in the static policy, KEPT ones (R29, R30)
   int64_t Lr = 0;
-  std::vector<std::pair<int64_t, int32_t>> running;  // (C - RS, q)
+  struct FrozenIv { int64_t a, c; int32_t q; };      // [a, c) relative to RS
+  std::vector<FrozenIv> running;
   for (int j = 0; j < NJ; ++j)
     for (int s = 0; s < G; ++s) {
       int cell = j * G + s;
-      if (cell_state[cell] != 1) continue;
+      if (cell_state[cell] != 1 && cell_state[cell] != 3) continue;
       int m = fassign[cell];
       int64_t Crel = comp(j, s) - rs;
+      int64_t Srel = std::max<int64_t>((int64_t)fstart[cell] - rs, 0);
       mfree0[(size_t)s * O + m] = (int32_t)std::max<int64_t>(mfree0[(size_t)s * O + m], Crel);
       base = std::max(base, Crel);
-      running.push_back({Crel, Qof(j, s, m)});
+      running.push_back({Srel, Crel, Qof(j, s, m)});
       Lr = std::max(Lr, Crel);
     }
   int64_t sum_p = 0;
@@ -179,7 +182,7 @@ ffs_status State::build_image() {
   for (int64_t t = 0; t < Lr; ++t) {
     int64_t L = 0;
     for (auto &rq : running)
-      if (t < rq.first) L += rq.second;
+      if (rq.a <= t && t < rq.c) L += rq.q;
     if (lvl_bytes == 1) img[H.off_lvl0 + t] = (uint8_t)L;
     else ((uint16_t *)(img + H.off_lvl0))[t] = (uint16_t)L;
   }
@@ -189,7 +192,7 @@ ffs_status State::build_image() {
     for (int64_t t = 0; t < (int64_t)H.hn_words0 * 8; ++t) {
       int64_t L = 0;
       for (auto &rq : running)
-        if (t < rq.first) L += rq.second;
+        if (rq.a <= t && t < rq.c) L += rq.q;
       const int64_t hr = std::max<int64_t>(0, in.q_max - L);
       hn[t >> 3] |= (uint32_t)(hr & 0xF) << ((t & 7) * 4);
       if (hr == 0 && (t >> 5) < H.bn_words0) bn[t >> 5] |= 1u << (t & 31);
@@ -362,12 +365,18 @@ ffs_status ffs_instance_create(const ffs_instance_desc *d, int cuda_device, ffs_
 
 void ffs_instance_destroy(ffs_instance *inst) { delete inst; }
 
-ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_t *orig_assign,
-                                const int32_t *orig_start, ffs_state **out, int32_t *K_out) {
+// policy 0: predictive-reactive complete rescheduling (freeze at RS, every
+// other op pending); policy 1: traditional static approach (P:313-315,
+// Fig. 7): every original op keeps its plan (cell state 3 = KEPT for those
+// not over or running at RS), only the arrivals' ops are genes.
+static ffs_status make_state(const ffs_instance *ih, int32_t rs, const int32_t *orig_assign,
+                             const int32_t *orig_start, int policy, ffs_state **out, int32_t *K_out) {
   if (!ih || !out) return fail(FFS_ERR_INVALID_ARG, "null argument");
   if (rs < 0) return fail(FFS_ERR_INVALID_ARG, "RS must be >= 0");
   if ((orig_assign == nullptr) != (orig_start == nullptr))
     return fail(FFS_ERR_INVALID_ARG, "orig_assign and orig_start must both be given or both NULL");
+  if (policy == 1 && ih->v.n > 0 && !orig_assign)
+    return fail(FFS_ERR_INVALID_ARG, "the static policy needs the original plan");
   const Instance &in = ih->v;
   const int G = in.g, O = in.o, n = in.n, NJ = in.NJ;
   auto Pof = [&](int j, int s, int m) { return (int64_t)in.P[((size_t)j * G + s) * O + m]; };
@@ -424,7 +433,7 @@ ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_
     for (int s = 0; s < G; ++s) {
       int c = j * G + s, m = orig_assign[c];
       int64_t S = orig_start[c], C = S + Pof(j, s, m);
-      int stt = (S < rs && rs < C) ? 1 : (C <= rs ? 2 : 0);
+      int stt = (S < rs && rs < C) ? 1 : (C <= rs ? 2 : (policy == 1 ? 3 : 0));
       st.cell_state[c] = stt;
       if (stt) {
         st.fassign[c] = m;
@@ -474,6 +483,16 @@ ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_
   *out = h;
   if (K_out) *K_out = st.K;
   return FFS_OK;
+}
+
+ffs_status ffs_reschedule_state(const ffs_instance *ih, int32_t rs, const int32_t *orig_assign,
+                                const int32_t *orig_start, ffs_state **out, int32_t *K_out) {
+  return make_state(ih, rs, orig_assign, orig_start, 0, out, K_out);
+}
+
+ffs_status ffs_static_state(const ffs_instance *ih, int32_t rs, const int32_t *orig_assign,
+                            const int32_t *orig_start, ffs_state **out, int32_t *K_out) {
+  return make_state(ih, rs, orig_assign, orig_start, 1, out, K_out);
 }
 
 ffs_status ffs_state_genes(const ffs_state *h, int32_t *gene_job, int32_t *gene_stage) {

@@ -24,7 +24,7 @@ MUT_010 = 429496729   # floor(0.1 * 2^32), mutation rate of P:395
 # every entry point declared in include/ffs.h
 EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
-    "ffs_reschedule_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
+    "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
     "ffs_state_set_horizon_cap", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
     "ffs_evaluate_host", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
@@ -75,6 +75,7 @@ def lib():
             "ffs_instance_create": ([C.POINTER(_Desc), C.c_int, P], C.c_int),
             "ffs_instance_destroy": ([P], None),
             "ffs_reschedule_state": ([P, C.c_int32, P, P, P, P], C.c_int),
+            "ffs_static_state": ([P, C.c_int32, P, P, P, P], C.c_int),
             "ffs_state_genes": ([P, P, P], C.c_int), "ffs_state_cells": ([P, P], C.c_int),
             "ffs_state_cut_table": ([P, P], C.c_int),
             "ffs_state_set_horizon_cap": ([P, C.c_int32], C.c_int),
@@ -150,16 +151,18 @@ class Instance:
 
 
 class State:
-    """Frozen rescheduling context at RS (ffs_reschedule_state)."""
+    """Frozen rescheduling context at RS (ffs_reschedule_state), or with
+    static=True the traditional static approach (ffs_static_state)."""
 
-    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None):
+    def __init__(self, inst: Instance, rs: int, orig_assign=None, orig_start=None, static: bool = False):
         self.inst = inst
+        self.static = bool(static)
         oa = None if orig_assign is None else np.ascontiguousarray(np.asarray(orig_assign, np.int32)).ravel()
         os_ = None if orig_start is None else np.ascontiguousarray(np.asarray(orig_start, np.int32)).ravel()
         h = C.c_void_p()
         K = C.c_int32()
-        _check(lib().ffs_reschedule_state(inst.h, int(rs), _np_ptr(oa), _np_ptr(os_), C.byref(h), C.byref(K)),
-               "ffs_reschedule_state")
+        fn = "ffs_static_state" if static else "ffs_reschedule_state"
+        _check(getattr(lib(), fn)(inst.h, int(rs), _np_ptr(oa), _np_ptr(os_), C.byref(h), C.byref(K)), fn)
         self.h = h
         self.K = K.value
         self.rs = int(rs)
@@ -277,9 +280,9 @@ def decode_schedule(state: State, x_genes, y_genes):
     return assign, start, int(obj.item()), int(T.item()), int(M.item())
 
 
-def make_state(inst: Instance, rs: int, orig_assign=None, orig_start=None) -> State:
+def make_state(inst: Instance, rs: int, orig_assign=None, orig_start=None, static: bool = False) -> State:
     """State plus the frozen assignment kept for merged-schedule assembly."""
-    st = State(inst, rs, orig_assign, orig_start)
+    st = State(inst, rs, orig_assign, orig_start, static=static)
     fa = -np.ones(st.cells, np.int32)
     if orig_assign is not None:
         oa = np.asarray(orig_assign, np.int32).ravel()

@@ -81,3 +81,64 @@ def run_events(wl: Workload, shape=(16, 8, 64), generations: int = 100, seed: in
         cur_assign, cur_start = ev.assign, ev.start
         keep += [inst, st]
     return res
+
+
+# ---------------------------------------------------------------------------
+# Dynamic vs static comparison (Table 10 design)
+# ---------------------------------------------------------------------------
+@dataclass
+class PolicyRow:
+    ratio: float
+    n_prime: int
+    static_mean: float
+    dynamic_mean: float
+    improvement_ratio: float
+    runs: List[dict]
+
+
+def test3_workload(ratio: float, seed: int, n: int = 10, g: int = 3, o: int = 2, q_max: int = 4) -> Workload:
+    """Test 3's instance (10 original jobs, 3 stages, 2 machines, Q_max 4)
+    with n' = round(ratio * n) arrivals (reading R31)."""
+    from .workload import gen_v1
+    return gen_v1("T10", n, g, o, q_max, arrivals_per_event=[int(round(ratio * n))], ratios=[ratio], seed=seed)
+
+
+def compare_policies(ratios=(0.2, 0.4, 0.6, 0.8), seeds=(1903,), shape=(8, 8, 64), generations: int = 100,
+                     device: int = 0, make_workload=test3_workload, stream=None) -> List[PolicyRow]:
+    """For every seed: plan the original jobs (island GA at RS = 0, the
+    "original schedule of an optimized solution", Fig. 6); for every ratio take
+    RS = floor(ratio * C_max(plan)), then optimise the same arrivals with the
+    predictive-reactive policy (ffs_reschedule_state) and with the traditional
+    static policy (ffs_static_state), same GA seed.  improvement ratio =
+    mean static objective / mean dynamic objective (Table 10's last column)."""
+    rows = []
+    plans = {}
+    for ratio in ratios:
+        runs = []
+        for seed in seeds:
+            wl = make_workload(ratio, seed)
+            base_arr = wl.original_instance()
+            key = (seed, base_arr["P"].tobytes(), base_arr["R"].tobytes(), base_arr["D"].tobytes())
+            if key not in plans:
+                base = ffs.Instance.from_arrays(base_arr, device=device)
+                st0 = ffs.make_state(base, 0)
+                plans[key] = (_evolve(st0, shape, generations, seed, stream), base, st0)
+            plan = plans[key][0]
+            rs = wl.rs_from_makespan(ratio, plan.makespan)
+            arr = wl.instance_at(0, [rs])
+            inst = ffs.Instance.from_arrays(arr, device=device)
+            n_g = wl.n * wl.g
+            res = {}
+            for name, static in (("dynamic", False), ("static", True)):
+                st = ffs.make_state(inst, rs, plan.assign[:n_g], plan.start[:n_g], static=static)
+                ev = _evolve(st, shape, generations, seed + 1, stream)
+                res[name] = ev
+            runs.append(dict(seed=seed, rs=rs, plan_makespan=plan.makespan, K_dynamic=res["dynamic"].K,
+                             K_static=res["static"].K, dynamic=res["dynamic"].objective,
+                             static=res["static"].objective, dynamic_result=res["dynamic"],
+                             static_result=res["static"]))
+        sm = float(np.mean([r["static"] for r in runs]))
+        dm = float(np.mean([r["dynamic"] for r in runs]))
+        rows.append(PolicyRow(ratio=ratio, n_prime=int(wl.arr_event.size), static_mean=sm, dynamic_mean=dm,
+                              improvement_ratio=sm / dm if dm > 0 else float("inf"), runs=runs))
+    return rows

@@ -28,25 +28,53 @@ if os.path.exists(lc) and '"ID"' in open(lc).read():
     txt = open(lc).read()
     rows = list(csv.reader(io.StringIO(txt[txt.index('"ID"'):])))
     h = rows[0]
-    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
-    tot = defaultdict(float)
-    cnt = defaultdict(int)
-    unit = {}
+    ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    seq = []
     for r in rows[1:]:
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].split("(")[0].replace("void ", "").replace("edffs::", "").replace("<unnamed>::", "")
+        name = name.replace("unnamed>::", "")
         v = float(r[vi].replace(",", ""))
-        u = r[h.index("Metric Unit")]
-        v = v / 1000.0 if u == "nsecond" else (v if u == "usecond" else v * 1000.0)
-        tot[name] += v
-        cnt[name] += 1
-    s = sum(tot.values())
-    out.append("## ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised)\n")
-    out.append("| kernel | launches | total us | share |\n|---|---|---|---|")
-    for k in sorted(tot, key=lambda k: -tot[k]):
-        out.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {100 * tot[k] / s:.1f}% |")
-    out.append("")
+        u = r[ui]
+        v = v / 1000.0 if u in ("ns", "nsecond") else (v * 1000.0 if u in ("ms", "msecond") else v)
+        seq.append((name, v))
+
+    def table(items, title):
+        tot, cnt = defaultdict(float), defaultdict(int)
+        for name, v in items:
+            tot[name] += v
+            cnt[name] += 1
+        s_ = sum(tot.values()) or 1.0
+        out.append(title + "\n")
+        out.append("| kernel | launches | total us | avg us | share |\n|---|---|---|---|---|")
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            out.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.1f} | {100 * tot[k] / s_:.1f}% |")
+        out.append("")
+        return tot, cnt
+
+    table(seq, "## ncu launch list, every captured launch (`--metrics gpu__time_duration.sum --clock-control none`, "
+               "cold-cache, serialised)")
+    gen = [i for i, (n, _) in enumerate(seq) if n == "generation_kernel"]
+    if gen:
+        a = gen[0]
+        b = next((i for i in range(a, len(seq)) if seq[i][0] == "random_population_kernel"), len(seq))
+        # run.best() after the timed steps decodes one chromosome with its schedule
+        # (lane_decode_kernel<., 1>, preceded by its order kernel): not a step
+        def is_sched(nm):
+            if nm.startswith("lane_decode_kernel"):
+                return nm.endswith(", 1>")
+            if nm.startswith("evaluate_kernel"):
+                return nm.split(",")[1].strip() == "1"
+            return False
+        sched = [i for i in range(a, b) if is_sched(seq[i][0])]
+        if sched:
+            b = sched[0] - 1
+        ng = sum(1 for i in gen if a <= i < b)
+        tot, cnt = table(seq[a:b], f"## GA step region of the same list ({ng} generations of the bench's GA: from "
+                                   "the first generation_kernel up to run.best())")
+        per_step = sum(tot.values()) / ng
+        out.append(f"Per generation (sum of the region / generations): {per_step:.1f} us\n")
 want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.per_cycle_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",

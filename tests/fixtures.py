@@ -65,10 +65,11 @@ def workload_instance(arrs):
                         arrs["R"], arrs["D"], arrs["q_max"], arrs["wt"])
 
 
-def oracle_event_ctx(wl, e=0):
+def oracle_event_ctx(wl, e=0, static=False):
     """Oracle-side construction of a workload's rescheduling context at event 0:
     decode the recorded plan chromosome at RS = 0 with the ORACLE, take
-    RS = floor(ratio * C_max), freeze."""
+    RS = floor(ratio * C_max), freeze (static=True: the traditional static
+    approach's context instead)."""
     base = wl.original_instance()
     c0 = orc.Ctx(workload_instance(base), 0)
     X, Y = c0.to_matrix(wl.plan_x, wl.plan_y)
@@ -76,5 +77,5 @@ def oracle_event_ctx(wl, e=0):
     rs = wl.rs_from_makespan(wl.ratios[0], plan["makespan"])
     arr = wl.instance_at(0, [rs])
     ctx = orc.Ctx(workload_instance(arr), rs, plan["assign"][: wl.n * wl.g],
-                  plan["start"][: wl.n * wl.g])
+                  plan["start"][: wl.n * wl.g], static=static)
     return ctx, arr, plan, rs

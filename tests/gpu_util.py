@@ -6,17 +6,17 @@ from paper_1903_10741_b200 import ffs
 from tests import fixtures as fx
 
 
-def gpu_state(arrs, rs, oa=None, os_=None, device=0):
+def gpu_state(arrs, rs, oa=None, os_=None, device=0, static=False):
     inst = ffs.Instance.from_arrays(arrs, device=device)
-    st = ffs.make_state(inst, rs, oa, os_)
+    st = ffs.make_state(inst, rs, oa, os_, static=static)
     st._inst_ref = inst
     return st
 
 
-def both_event_ctx(wl):
+def both_event_ctx(wl, static=False):
     """Each side builds the event-0 context independently (plan decode on its
     own decoder); the plans must agree exactly."""
-    octx, arr, oplan, ors = fx.oracle_event_ctx(wl)
+    octx, arr, oplan, ors = fx.oracle_event_ctx(wl, static=static)
     base = wl.original_instance()
     st0 = gpu_state(base, 0)
     assign, start, obj, T, M = ffs.decode_schedule(st0, wl.plan_x, wl.plan_y)
@@ -24,7 +24,7 @@ def both_event_ctx(wl):
     assert rs == ors and M == oplan["makespan"]
     assert (start == oplan["start"]).all() and (assign == oplan["assign"]).all()
     arr_g = wl.instance_at(0, [rs])
-    st = gpu_state(arr_g, rs, assign[: wl.n * wl.g], start[: wl.n * wl.g])
+    st = gpu_state(arr_g, rs, assign[: wl.n * wl.g], start[: wl.n * wl.g], static=static)
     return octx, st, arr
 
 

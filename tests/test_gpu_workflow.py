@@ -61,3 +61,44 @@ def test_config_b_workflow_parity(shape, G):
         assert ev.sum_tardiness == r["sum_tardiness"]
         assert (ev.start == r["start"]).all() and (ev.assign == r["assign"]).all()
         assert (ev.trace_min == tmin).all() and (ev.trace_sum == tsum).all()
+
+
+def oracle_compare(ratios, seeds, shape, G):
+    """The Table 10 comparison driven by the oracle GA."""
+    from paper_1903_10741_b200.workflow import test3_workload
+    out = {}
+    for ratio in ratios:
+        for seed in seeds:
+            wl = test3_workload(ratio, seed)
+            c0 = orc.Ctx(fx.workload_instance(wl.original_instance()), 0)
+            plan, _, _ = oracle_evolve(c0, shape, G, seed)
+            rs = wl.rs_from_makespan(ratio, plan["makespan"])
+            arr = wl.instance_at(0, [rs])
+            n_g = wl.n * wl.g
+            for name, static in (("dynamic", False), ("static", True)):
+                ctx = orc.Ctx(fx.workload_instance(arr), rs, plan["assign"][:n_g], plan["start"][:n_g],
+                              static=static)
+                r, tmin, _ = oracle_evolve(ctx, shape, G, seed + 1)
+                assert ctx.validate(r["assign"], r["start"])[0] == 0
+                out[(ratio, seed, name)] = (rs, ctx.K, r, tmin)
+    return out
+
+
+def test_policy_comparison_parity():
+    """Dynamic vs static (Table 10 design): every run's RS, K, best objective,
+    schedule and trace equal the oracle-driven comparison."""
+    ratios, seeds, shape, G = (0.2, 0.6), (1903, 7), (4, 4, 4), 11
+    ref = oracle_compare(ratios, seeds, shape, G)
+    rows = workflow.compare_policies(ratios=ratios, seeds=seeds, shape=shape, generations=G)
+    assert [r.ratio for r in rows] == list(ratios)
+    for row in rows:
+        assert row.n_prime == round(row.ratio * 10)
+        for run in row.runs:
+            for name in ("dynamic", "static"):
+                rs, K, r, tmin = ref[(row.ratio, run["seed"], name)]
+                ev = run[name + "_result"]
+                assert run["rs"] == rs and ev.K == K
+                assert ev.objective == r["objective"] and ev.makespan == r["makespan"]
+                assert (ev.start == r["start"]).all() and (ev.assign == r["assign"]).all()
+                assert (ev.trace_min == tmin).all()
+            assert run["K_static"] == row.n_prime * 3
