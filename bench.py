@@ -336,6 +336,44 @@ def run_ours(args):
               "events": [{"rs": e.rs, "K": e.K, "objective": e.objective, "makespan": e.makespan,
                           "seconds": e.seconds} for e in evs]}
 
+    # ---- f1: traditional static approach (ffs_static_state) on config C, and the
+    # Table 10 dynamic-vs-static comparison (test 3 instance, 4 ratios x 3 seeds)
+    static_c = policy = None
+    if world == 1:
+        from paper_1903_10741_b200 import workflow as fwf
+        sst = ffs.make_state(inst, rs, passign, pstart[: wl.n * wl.g], static=True)
+        xs_, ys_ = ffs.random_population(sst, pop_local, SEED, stream=stream)
+        ob_ = torch.empty(pop_local, dtype=torch.int64, device=dev)
+        for _ in range(3):
+            ffs.evaluate(sst, xs_, ys_, ob_, stream=stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ffs.evaluate(sst, xs_, ys_, ob_, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ts_ = e0.elapsed_time(e1) / 1e3 / args.steps
+        static_c = {"workload": "C, traditional static approach: originals keep their plan, the 20 arrivals' "
+                                "200 ops are the genes", "K": sst.K, "population": pop_local,
+                    "evals_per_s": pop_local / ts_, "ms_per_launch": 1e3 * ts_}
+        del xs_, ys_, ob_
+        fwf.compare_policies(ratios=(0.2,), seeds=(1,), shape=(8, 8, 64), generations=3)   # warm-up
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rows = fwf.compare_policies(ratios=(0.2, 0.4, 0.6, 0.8), seeds=(1903, 1904, 1905), shape=(8, 8, 64),
+                                    generations=100)
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        policy = {"workload": "test 3 instance (P:373): gen-v1 10 jobs x 3 stages x 2 machines, Q_max=4; "
+                              "n' = ratio x 10 arrivals; 64 islands x 64 (8x8), 100 generations per run; "
+                              "plan by the same GA at RS=0; seeds 1903-1905",
+                  "seconds_total": dt, "ga_runs": 3 + 4 * 3 * 2,
+                  "rows": [{"ratio": r.ratio, "n_prime": r.n_prime, "static_mean": r.static_mean,
+                            "dynamic_mean": r.dynamic_mean, "improvement_ratio": r.improvement_ratio}
+                           for r in rows]}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -350,6 +388,8 @@ def run_ours(args):
             "best_objective": best["objective"],
             "sweep_E": sweep,
             "workflow_B": wf,
+            "static_C": static_c,
+            "policy_T10": policy,
             "clocks": clk.summary(),
         }
         alg_ops = None

@@ -27,6 +27,8 @@ struct or_ctx {
   int32_t NJ, cells, K;
   int32_t *state;      /* [cells] OR_PENDING / OR_RUNNING / OR_COMPLETED / OR_KEPT */
   int32_t policy;      /* OR_DYNAMIC or OR_STATIC                         */
+  int32_t real_wt;     /* 1: Eq. (1) with the real weight wt_real (Table 11) */
+  double wt_real;
   int32_t *fassign;    /* [cells] frozen machine (plan), -1 when pending  */
   int32_t *fstart;     /* [cells] frozen start (plan), -1 when pending    */
   int32_t *gene_cell;  /* [K] pending cells in row-major order            */
@@ -468,6 +470,40 @@ int64_t or_fitness(int64_t objective, int64_t emax) {
   return f > 0 ? f : 0;
 }
 
+/* The same two rules over binary64 values (fractional WT, Table 11; exact for
+ * integer values below 2^53).  Powers of ten are exact in binary64 up to 1e22. */
+double or_emax_real(const double *objectives, int64_t count) {
+  double E = 10.0;
+  for (;;) {
+    int all_smaller = 1;
+    for (int64_t i = 0; i < count; ++i)
+      if (!(objectives[i] < E)) { all_smaller = 0; break; }
+    if (all_smaller) return E;
+    E *= 10.0;
+  }
+}
+double or_fitness_real(double objective, double emax) {
+  double f = emax - objective;
+  return f > 0.0 ? f : 0.0;
+}
+
+/* Eq. (1) as a binary64 value in the context's weight mode:
+ * integer WT (R25): the exact integer WT*sum T + C_max; real WT (Table 11,
+ * P:473-489): fl(fl(WT * sum T) + C_max), two roundings, no fused
+ * multiply-add (the library is built with -ffp-contract=off). */
+double or_objective_value(const or_ctx *c, int64_t sum_tardiness, int64_t makespan) {
+  if (!c->real_wt) return (double)(c->in.wt * sum_tardiness + makespan);
+  double weighted = (double)sum_tardiness * c->wt_real;
+  return weighted + (double)makespan;
+}
+
+int or_ctx_set_real_weight(or_ctx *c, double wt) {
+  if (!c || !(wt >= 0.0) || wt > 1e300) return OR_ERR_ARG;
+  c->real_wt = 1;
+  c->wt_real = wt;
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* Brute force over the decoder-reachable set                          */
 /* ------------------------------------------------------------------ */
@@ -617,6 +653,7 @@ typedef struct {
   const int32_t *Xs, *Ys;        /* matrix form [count*cells] or NULL */
   const int8_t *xc; const int16_t *yc;   /* compact form [count*K]  */
   int64_t *obj, *sumT, *cmax;
+  double *value;                 /* Eq. (1) in the context's weight mode */
   or_counters cnt;
   int status;
 } eval_job;
@@ -646,6 +683,7 @@ static void *eval_worker(void *arg) {
     if (w->obj) w->obj[i] = O;
     if (w->sumT) w->sumT[i] = T;
     if (w->cmax) w->cmax[i] = M;
+    if (w->value) w->value[i] = or_objective_value(c, T, M);
   }
   free(X); free(Y);
   return NULL;
@@ -653,7 +691,7 @@ static void *eval_worker(void *arg) {
 
 static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int32_t *Ys,
                     const int8_t *xc, const int16_t *yc, int64_t *obj, int64_t *sumT,
-                    int64_t *cmax, int nthreads, or_counters *cnt) {
+                    int64_t *cmax, double *value, int nthreads, or_counters *cnt) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > count) nthreads = count > 0 ? (int)count : 1;
   eval_job *jobs = (eval_job *)calloc(nthreads, sizeof(eval_job));
@@ -663,7 +701,7 @@ static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int
     jobs[t].begin = count * t / nthreads;
     jobs[t].end = count * (t + 1) / nthreads;
     jobs[t].Xs = Xs; jobs[t].Ys = Ys; jobs[t].xc = xc; jobs[t].yc = yc;
-    jobs[t].obj = obj; jobs[t].sumT = sumT; jobs[t].cmax = cmax;
+    jobs[t].obj = obj; jobs[t].sumT = sumT; jobs[t].cmax = cmax; jobs[t].value = value;
   }
   if (nthreads == 1) eval_worker(&jobs[0]);
   else {
@@ -684,8 +722,8 @@ static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int
 
 int or_evaluate_batch(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
                       int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
-                      int32_t nthreads, or_counters *cnt) {
-  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, nthreads, cnt);
+                      double *value, int32_t nthreads, or_counters *cnt) {
+  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, value, nthreads, cnt);
 }
 
 /* ------------------------------------------------------------------ */
@@ -696,12 +734,14 @@ struct or_run {
   or_ga_cfg cfg;
   int32_t tile, nisl, nloc;          /* cells per island, local islands, local cells */
   int32_t gen;                       /* last completed generation (-1 = fresh) */
-  int64_t emax;
+  /* objective / fitness values are binary64: exact for the integer
+   * objective (< 2^53), and the real-WT objective of Table 11 */
+  double emax;
   int32_t *X, *Y;                    /* [nloc*cells] */
-  int64_t *obj, *fit;                /* [nloc] */
+  double *obj, *fit;                 /* [nloc] */
   int32_t *HX, *HY;                  /* history elites [nisl*cells] */
-  int64_t *hobj, *hfit;
-  int64_t *tmin, *tsum;              /* [G+1] local trace */
+  double *hobj, *hfit;
+  double *tmin, *tsum;               /* [G+1] local trace */
 };
 
 int or_ga_create(const or_ctx *c, const or_ga_cfg *cfg, or_run **out) {
@@ -718,14 +758,14 @@ int or_ga_create(const or_ctx *c, const or_ga_cfg *cfg, or_run **out) {
   size_t cells = c->cells;
   r->X = (int32_t *)malloc((size_t)r->nloc * cells * sizeof(int32_t));
   r->Y = (int32_t *)malloc((size_t)r->nloc * cells * sizeof(int32_t));
-  r->obj = (int64_t *)malloc(r->nloc * sizeof(int64_t));
-  r->fit = (int64_t *)malloc(r->nloc * sizeof(int64_t));
+  r->obj = (double *)malloc(r->nloc * sizeof(double));
+  r->fit = (double *)malloc(r->nloc * sizeof(double));
   r->HX = (int32_t *)malloc((size_t)r->nisl * cells * sizeof(int32_t));
   r->HY = (int32_t *)malloc((size_t)r->nisl * cells * sizeof(int32_t));
-  r->hobj = (int64_t *)malloc(r->nisl * sizeof(int64_t));
-  r->hfit = (int64_t *)malloc(r->nisl * sizeof(int64_t));
-  r->tmin = (int64_t *)calloc(cfg->generations + 1, sizeof(int64_t));
-  r->tsum = (int64_t *)calloc(cfg->generations + 1, sizeof(int64_t));
+  r->hobj = (double *)malloc(r->nisl * sizeof(double));
+  r->hfit = (double *)malloc(r->nisl * sizeof(double));
+  r->tmin = (double *)calloc(cfg->generations + 1, sizeof(double));
+  r->tsum = (double *)calloc(cfg->generations + 1, sizeof(double));
   *out = r;
   return OR_OK;
 }
@@ -740,12 +780,12 @@ static int32_t *cellX(or_run *r, int idx) { return r->X + (size_t)idx * r->c->ce
 static int32_t *cellY(or_run *r, int idx) { return r->Y + (size_t)idx * r->c->cells; }
 
 static void evaluate_population(or_run *r) {
-  run_eval(r->c, r->nloc, r->X, r->Y, NULL, NULL, r->obj, NULL, NULL, r->cfg.nthreads, NULL);
-  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness(r->obj[i], r->emax);
+  run_eval(r->c, r->nloc, r->X, r->Y, NULL, NULL, NULL, NULL, NULL, r->obj, r->cfg.nthreads, NULL);
+  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness_real(r->obj[i], r->emax);
 }
 
 static void record_trace(or_run *r, int k) {
-  int64_t mn = r->obj[0], sum = 0;
+  double mn = r->obj[0], sum = 0.0;      /* sum in index order */
   for (int i = 0; i < r->nloc; ++i) { if (r->obj[i] < mn) mn = r->obj[i]; sum += r->obj[i]; }
   r->tmin[k] = mn; r->tsum[k] = sum;
 }
@@ -798,13 +838,13 @@ static int ga_init(or_run *r) {
   }
   free(keys);
   /* E_max from every individual's initial objective (R23: global) */
-  r->emax = 10;   /* placeholder so evaluate_population computes fitness */
+  r->emax = 10.0;   /* placeholder so evaluate_population computes fitness */
   evaluate_population(r);
-  int64_t mx = r->obj[0];
+  double mx = r->obj[0];
   for (int i = 1; i < r->nloc; ++i) if (r->obj[i] > mx) mx = r->obj[i];
   if (r->cfg.allreduce_max && r->cfg.allreduce_max(r->cfg.user, &mx) != 0) return OR_ERR_ARG;
-  r->emax = or_emax(&mx, 1);
-  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness(r->obj[i], r->emax);
+  r->emax = or_emax_real(&mx, 1);
+  for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness_real(r->obj[i], r->emax);
   for (int li = 0; li < r->nisl; ++li) set_history(r, li, island_best(r, li));
   record_trace(r, 0);
   r->gen = 0;
@@ -819,9 +859,9 @@ static int ga_generation(or_run *r, int k) {
   size_t bytes = (size_t)r->nloc * cells * sizeof(int32_t);
   /* snapshot of generation k-1 (synchronous update, R18) */
   int32_t *PX = (int32_t *)malloc(bytes), *PY = (int32_t *)malloc(bytes);
-  int64_t *Pfit = (int64_t *)malloc(r->nloc * sizeof(int64_t));
+  double *Pfit = (double *)malloc(r->nloc * sizeof(double));
   memcpy(PX, r->X, bytes); memcpy(PY, r->Y, bytes);
-  memcpy(Pfit, r->fit, r->nloc * sizeof(int64_t));
+  memcpy(Pfit, r->fit, r->nloc * sizeof(double));
   int32_t *winner = (int32_t *)malloc(tile * sizeof(int32_t));
   uint32_t *rx = (uint32_t *)malloc((K + 1) * sizeof(uint32_t));
 
@@ -891,7 +931,7 @@ static int ga_generation(or_run *r, int k) {
 
   /* single-ring migration every migration_interval generations (R22) */
   if (k % r->cfg.migration_interval == 0 && r->cfg.islands_total >= 2) {
-    size_t rec = (size_t)cells * 2 * sizeof(int32_t) + 2 * sizeof(int64_t);
+    size_t rec = (size_t)cells * 2 * sizeof(int32_t) + 2 * sizeof(double);
     char *donors = (char *)malloc(rec * r->nisl);
     int *worst = (int *)malloc(r->nisl * sizeof(int));
     for (int li = 0; li < r->nisl; ++li) {    /* snapshot first: synchronous */
@@ -899,8 +939,8 @@ static int ga_generation(or_run *r, int k) {
       char *d = donors + rec * li;
       memcpy(d, cellX(r, b), cells * sizeof(int32_t));
       memcpy(d + cells * sizeof(int32_t), cellY(r, b), cells * sizeof(int32_t));
-      memcpy(d + cells * 2 * sizeof(int32_t), &r->obj[b], sizeof(int64_t));
-      memcpy(d + cells * 2 * sizeof(int32_t) + sizeof(int64_t), &r->fit[b], sizeof(int64_t));
+      memcpy(d + cells * 2 * sizeof(int32_t), &r->obj[b], sizeof(double));
+      memcpy(d + cells * 2 * sizeof(int32_t) + sizeof(double), &r->fit[b], sizeof(double));
       worst[li] = island_worst(r, li);
     }
     /* island begin receives from global island begin-1: the last island of
@@ -919,8 +959,8 @@ static int ga_generation(or_run *r, int k) {
       int wst = worst[li];
       memcpy(cellX(r, wst), src, cells * sizeof(int32_t));
       memcpy(cellY(r, wst), src + cells * sizeof(int32_t), cells * sizeof(int32_t));
-      memcpy(&r->obj[wst], src + cells * 2 * sizeof(int32_t), sizeof(int64_t));
-      memcpy(&r->fit[wst], src + cells * 2 * sizeof(int32_t) + sizeof(int64_t), sizeof(int64_t));
+      memcpy(&r->obj[wst], src + cells * 2 * sizeof(int32_t), sizeof(double));
+      memcpy(&r->fit[wst], src + cells * 2 * sizeof(int32_t) + sizeof(double), sizeof(double));
     }
     free(donors); free(worst); free(incoming);
   }
@@ -936,9 +976,9 @@ int or_ga_step(or_run *r) {
   return ga_generation(r, r->gen + 1);
 }
 int32_t or_ga_generation(const or_run *r) { return r->gen; }
-int64_t or_ga_emax(const or_run *r) { return r->emax; }
+double or_ga_emax(const or_run *r) { return r->emax; }
 
-void or_ga_population(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+void or_ga_population(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit) {
   const or_ctx *c = r->c;
   for (int i = 0; i < r->nloc; ++i)
     for (int gi = 0; gi < c->K; ++gi) {
@@ -946,11 +986,11 @@ void or_ga_population(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int6
       if (x) x[(size_t)i * c->K + gi] = (int8_t)r->X[(size_t)i * c->cells + cell];
       if (y) y[(size_t)i * c->K + gi] = (int16_t)r->Y[(size_t)i * c->cells + cell];
     }
-  if (obj) memcpy(obj, r->obj, r->nloc * sizeof(int64_t));
-  if (fit) memcpy(fit, r->fit, r->nloc * sizeof(int64_t));
+  if (obj) memcpy(obj, r->obj, r->nloc * sizeof(double));
+  if (fit) memcpy(fit, r->fit, r->nloc * sizeof(double));
 }
 
-void or_ga_history(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+void or_ga_history(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit) {
   const or_ctx *c = r->c;
   for (int li = 0; li < r->nisl; ++li)
     for (int gi = 0; gi < c->K; ++gi) {
@@ -958,12 +998,12 @@ void or_ga_history(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t
       if (x) x[(size_t)li * c->K + gi] = (int8_t)r->HX[(size_t)li * c->cells + cell];
       if (y) y[(size_t)li * c->K + gi] = (int16_t)r->HY[(size_t)li * c->cells + cell];
     }
-  if (obj) memcpy(obj, r->hobj, r->nisl * sizeof(int64_t));
-  if (fit) memcpy(fit, r->hfit, r->nisl * sizeof(int64_t));
+  if (obj) memcpy(obj, r->hobj, r->nisl * sizeof(double));
+  if (fit) memcpy(fit, r->hfit, r->nisl * sizeof(double));
 }
 
-void or_ga_trace(const or_run *r, int64_t *tmin, int64_t *tsum) {
+void or_ga_trace(const or_run *r, double *tmin, double *tsum) {
   int n = r->cfg.generations + 1;
-  if (tmin) memcpy(tmin, r->tmin, n * sizeof(int64_t));
-  if (tsum) memcpy(tsum, r->tsum, n * sizeof(int64_t));
+  if (tmin) memcpy(tmin, r->tmin, n * sizeof(double));
+  if (tsum) memcpy(tsum, r->tsum, n * sizeof(double));
 }

@@ -121,6 +121,17 @@ int64_t or_power_at(const or_instance *inst, const int32_t *assign, const int32_
 int64_t or_emax(const int64_t *objectives, int64_t count);
 /* Eq. (13): max(E_max - objective, 0). */
 int64_t or_fitness(int64_t objective, int64_t emax);
+/* the same two rules over binary64 values (used by the GA; exact for the
+ * integer objective below 2^53, and the fractional-WT objective of Table 11) */
+double or_emax_real(const double *objectives, int64_t count);
+double or_fitness_real(double objective, double emax);
+
+/* Fractional WT (Table 11): switch the context to
+ * Eq. (1) with a real weight wt >= 0.  or_objective_value then returns
+ * fl(fl(WT * sum T) + C_max) (two binary64 roundings, no FMA); without the
+ * switch it returns the exact integer objective of the instance's WT. */
+int or_ctx_set_real_weight(or_ctx *c, double wt);
+double or_objective_value(const or_ctx *c, int64_t sum_tardiness, int64_t makespan);
 
 /* Brute force over every X in [0,o-1]^K and every linear extension of the
  * job chains (the decoder-reachable set), decoding each order directly.
@@ -156,9 +167,10 @@ typedef struct {
   int32_t generations;                /* G                                    */
   uint64_t seed;
   int32_t nthreads;                   /* evaluation threads (timing only)     */
-  /* shard exchange (NULL when single shard): global max of int64; allgather
-   * of bytes_per_rank from every shard into recv (rank-major) */
-  int (*allreduce_max)(void *user, int64_t *val);
+  /* shard exchange (NULL when single shard): global max of a binary64
+   * objective; allgather of bytes_per_rank from every shard into recv
+   * (rank-major) */
+  int (*allreduce_max)(void *user, double *val);
   int (*allgather)(void *user, const void *send, void *recv, size_t bytes_per_rank);
   int32_t rank, world;
   void *user;
@@ -171,19 +183,22 @@ int or_ga_create(const or_ctx *c, const or_ga_cfg *cfg, or_run **out);
  * migrate, trace). */
 int or_ga_step(or_run *r);
 int32_t or_ga_generation(const or_run *r);
-int64_t or_ga_emax(const or_run *r);
+/* The GA keeps objectives (or_objective_value) and fitness in binary64. */
+double or_ga_emax(const or_run *r);
 /* local shard population as compact genes (canonical order) [cells_local*K] */
-void or_ga_population(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit);
-/* local trace: per generation min objective and sum of objectives [G+1] */
-void or_ga_trace(const or_run *r, int64_t *tmin, int64_t *tsum);
+void or_ga_population(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit);
+/* local trace: per generation min objective and sum of objectives (summed in
+ * cell-index order) [G+1] */
+void or_ga_trace(const or_run *r, double *tmin, double *tsum);
 /* per-island history elites of the shard: [islands_local*K] + obj/fit */
-void or_ga_history(const or_run *r, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit);
+void or_ga_history(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit);
 void or_ga_destroy(or_run *r);
 
-/* batch evaluation of compact chromosomes, nthreads workers (timing leg) */
+/* batch evaluation of compact chromosomes, nthreads workers; objective is
+ * the integer-WT Eq. (1), value (may be NULL) or_objective_value */
 int or_evaluate_batch(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
                       int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
-                      int32_t nthreads, or_counters *cnt);
+                      double *value, int32_t nthreads, or_counters *cnt);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc (no GPU, no shared code)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
             os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "ffs_oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-Wextra", "-Wno-unused-parameter",
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-Wall", "-Wextra", "-Wno-unused-parameter",
                                "-shared", "-fPIC", "-o", LIB, SRC, "-lpthread"])
     return LIB
 
@@ -48,7 +48,7 @@ class _Cnt(C.Structure):
                 ("jumps", C.c_int64), ("updates", C.c_int64)]
 
 
-_ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64))
+_ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double))
 _ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 
 
@@ -87,6 +87,13 @@ def lib():
         _lib.or_emax.restype = C.c_int64
         _lib.or_fitness.argtypes = [C.c_int64, C.c_int64]
         _lib.or_fitness.restype = C.c_int64
+        _lib.or_emax_real.argtypes = [P, C.c_int64]
+        _lib.or_emax_real.restype = C.c_double
+        _lib.or_fitness_real.argtypes = [C.c_double, C.c_double]
+        _lib.or_fitness_real.restype = C.c_double
+        _lib.or_ctx_set_real_weight.argtypes = [P, C.c_double]
+        _lib.or_objective_value.argtypes = [P, C.c_int64, C.c_int64]
+        _lib.or_objective_value.restype = C.c_double
         _lib.or_brute_force.argtypes = [P, C.c_int64, P, P, P, P]
         _lib.or_philox4x32_10.argtypes = [P, P, P]
         _lib.or_repair.argtypes = [P, P]
@@ -96,12 +103,12 @@ def lib():
         _lib.or_ga_step.argtypes = [P]
         _lib.or_ga_generation.argtypes = [P]
         _lib.or_ga_emax.argtypes = [P]
-        _lib.or_ga_emax.restype = C.c_int64
+        _lib.or_ga_emax.restype = C.c_double
         _lib.or_ga_population.argtypes = [P, P, P, P, P]
         _lib.or_ga_trace.argtypes = [P, P, P]
         _lib.or_ga_history.argtypes = [P, P, P, P, P]
         _lib.or_ga_destroy.argtypes = [P]
-        _lib.or_evaluate_batch.argtypes = [P, C.c_int64, P, P, P, P, P, C.c_int32, C.POINTER(_Cnt)]
+        _lib.or_evaluate_batch.argtypes = [P, C.c_int64, P, P, P, P, P, P, C.c_int32, C.POINTER(_Cnt)]
     return _lib
 
 
@@ -162,6 +169,23 @@ def fitness(objective: int, e_max: int) -> int:
     return int(lib().or_fitness(int(objective), int(e_max)))
 
 
+def emax_real(objectives) -> float:
+    a = np.ascontiguousarray(np.asarray(objectives, dtype=np.float64))
+    return float(lib().or_emax_real(_p(a), len(a)))
+
+
+def fitness_real(objective: float, e_max: float) -> float:
+    return float(lib().or_fitness_real(float(objective), float(e_max)))
+
+
+def _values(a, real):
+    """GA values are binary64 in the oracle: int64 view for the integer objective."""
+    if real:
+        return a
+    assert np.all(np.abs(a) < 2.0 ** 53) and np.all(a == np.floor(a))
+    return a.astype(np.int64)
+
+
 def objective(inst: Instance, assign, start):
     ci = inst._c()
     a, s = _i32(assign).ravel(), _i32(start).ravel()
@@ -184,6 +208,7 @@ class Ctx:
         the originals keep their whole plan, only the new jobs are genes."""
         self.inst = inst
         self.static = bool(static)
+        self.real_wt = None
         self._ci = inst._c()
         self._oa = None if orig_assign is None else _i32(orig_assign).ravel()
         self._os = None if orig_start is None else _i32(orig_start).ravel()
@@ -205,6 +230,15 @@ class Ctx:
         if getattr(self, "h", None) and _lib is not None:
             _lib.or_ctx_destroy(self.h)
             self.h = None
+
+    def set_real_weight(self, wt: float):
+        """Fractional WT (Table 11): Eq. (1) in binary64 from now on."""
+        _chk(lib().or_ctx_set_real_weight(self.h, float(wt)), "set_real_weight")
+        self.real_wt = float(wt)
+
+    def objective_value(self, sum_tardiness: int, makespan: int):
+        v = float(lib().or_objective_value(self.h, int(sum_tardiness), int(makespan)))
+        return v if self.real_wt is not None else int(v)
 
     # compact canonical genes <-> paper matrices
     def to_matrix(self, x_genes, y_genes):
@@ -236,7 +270,7 @@ class Ctx:
         _chk(lib().or_decode(self.h, _p(Xc), _p(Yc), _p(Zc), _p(asg), _p(st), C.byref(T),
                              C.byref(M), C.byref(O), C.byref(cnt)), "decode")
         return dict(assign=asg, start=st, sum_tardiness=T.value, makespan=M.value,
-                    objective=O.value,
+                    objective=O.value, value=self.objective_value(T.value, M.value),
                     counters=dict(dispatches=cnt.dispatches, checks=cnt.checks,
                                   jumps=cnt.jumps, updates=cnt.updates))
 
@@ -284,9 +318,12 @@ class Ctx:
         obj = np.zeros(count, dtype=np.int64)
         T = np.zeros(count, dtype=np.int64)
         M = np.zeros(count, dtype=np.int64)
+        val = np.zeros(count, dtype=np.float64)
         cnt = _Cnt()
-        _chk(lib().or_evaluate_batch(self.h, count, _p(x), _p(y), _p(obj), _p(T), _p(M),
+        _chk(lib().or_evaluate_batch(self.h, count, _p(x), _p(y), _p(obj), _p(T), _p(M), _p(val),
                                      int(nthreads), C.byref(cnt)), "evaluate_batch")
+        if self.real_wt is not None:       # Eq. (1) with the real weight, binary64
+            obj = val
         return obj, T, M, dict(dispatches=cnt.dispatches, checks=cnt.checks, jumps=cnt.jumps,
                                updates=cnt.updates)
 
@@ -309,7 +346,7 @@ class GA:
         ag = _ALLGATHER()
         if allreduce_max is not None:
             def _ar(user, ptr):
-                ptr[0] = int(allreduce_max(int(ptr[0])))
+                ptr[0] = float(allreduce_max(float(ptr[0])))
                 return 0
             ar = _ALLRED(_ar)
         if allgather is not None:
@@ -344,29 +381,34 @@ class GA:
         return lib().or_ga_generation(self.h)
 
     @property
+    def real(self):
+        return self.ctx.real_wt is not None
+
+    @property
     def emax(self):
-        return int(lib().or_ga_emax(self.h))
+        e = float(lib().or_ga_emax(self.h))
+        return e if self.real else int(e)
 
     def population(self):
         K = self.ctx.K
         x = np.zeros((self.nloc, K), dtype=np.int8)
         y = np.zeros((self.nloc, K), dtype=np.int16)
-        obj = np.zeros(self.nloc, dtype=np.int64)
-        fit = np.zeros(self.nloc, dtype=np.int64)
+        obj = np.zeros(self.nloc, dtype=np.float64)
+        fit = np.zeros(self.nloc, dtype=np.float64)
         lib().or_ga_population(self.h, _p(x), _p(y), _p(obj), _p(fit))
-        return x, y, obj, fit
+        return x, y, _values(obj, self.real), _values(fit, self.real)
 
     def history(self):
         K = self.ctx.K
         x = np.zeros((self.nisl, K), dtype=np.int8)
         y = np.zeros((self.nisl, K), dtype=np.int16)
-        obj = np.zeros(self.nisl, dtype=np.int64)
-        fit = np.zeros(self.nisl, dtype=np.int64)
+        obj = np.zeros(self.nisl, dtype=np.float64)
+        fit = np.zeros(self.nisl, dtype=np.float64)
         lib().or_ga_history(self.h, _p(x), _p(y), _p(obj), _p(fit))
-        return x, y, obj, fit
+        return x, y, _values(obj, self.real), _values(fit, self.real)
 
     def trace(self):
-        tmin = np.zeros(self.generations + 1, dtype=np.int64)
-        tsum = np.zeros(self.generations + 1, dtype=np.int64)
+        tmin = np.zeros(self.generations + 1, dtype=np.float64)
+        tsum = np.zeros(self.generations + 1, dtype=np.float64)
         lib().or_ga_trace(self.h, _p(tmin), _p(tsum))
-        return tmin, tsum
+        return _values(tmin, self.real), _values(tsum, self.real)

@@ -68,8 +68,8 @@ def _worker(rank, world, port, out_dir):
         b, e = fdist.shard(islands, rank, world)
 
         def ar(x):
-            t = torch.tensor([x], dtype=torch.int64)
-            return int(fdist.allreduce_max_tensor(t)[0])
+            t = torch.tensor([x], dtype=torch.float64)
+            return float(fdist.allreduce_max_tensor(t)[0])
 
         def ag(buf):
             t = torch.frombuffer(bytearray(buf), dtype=torch.uint8)
