@@ -374,6 +374,39 @@ def run_ours(args):
                             "dynamic_mean": r.dynamic_mean, "improvement_ratio": r.improvement_ratio}
                            for r in rows]}
 
+    # ---- f3: fractional WT (Table 11): evaluate throughput with binary64 objective
+    # words on config C, and the Table 11 WT sweep on the test 3 instance
+    realwt = None
+    if world == 1:
+        from paper_1903_10741_b200 import workflow as fwf
+        rst = ffs.make_state(inst, rs, passign, pstart[: wl.n * wl.g])
+        rst.set_objective_weight(0.37)
+        ob_ = torch.empty(pop_local, dtype=torch.int64, device=dev)
+        for _ in range(3):
+            ffs.evaluate(rst, x, y, ob_, stream=stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ffs.evaluate(rst, x, y, ob_, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tr_ = e0.elapsed_time(e1) / 1e3 / args.steps
+        fwf.wt_sweep(wts=(0.5,), seeds=(1,), shape=(8, 8, 64), generations=3)     # warm-up
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        wrows = fwf.wt_sweep(seeds=(1903, 1904, 1905), ratio=0.5, shape=(8, 8, 64), generations=100)
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        realwt = {"evaluate_C": {"wt": 0.37, "evals_per_s": pop_local / tr_, "ms_per_launch": 1e3 * tr_},
+                  "table11": {"workload": "test 3 instance (P:373), RS = 0.5 x plan C_max (5 arrivals); "
+                                          "64 islands x 64 (8x8), 100 generations per WT; seeds 1903-1905",
+                              "seconds_total": dt,
+                              "rows": [{"wt": r.wt, "sum_tardiness": r.tardiness_mean,
+                                        "makespan": r.makespan_mean, "objective": r.objective_mean}
+                                       for r in wrows]}}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -390,6 +423,7 @@ def run_ours(args):
             "workflow_B": wf,
             "static_C": static_c,
             "policy_T10": policy,
+            "real_wt": realwt,
             "clocks": clk.summary(),
         }
         alg_ops = None

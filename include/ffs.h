@@ -135,12 +135,28 @@ FFS_API ffs_status ffs_state_info(const ffs_state *st, int32_t *K, int32_t *cell
 FFS_API void ffs_state_destroy(ffs_state *st);
 
 /* ------------------------------------------------------------------------
+ * Fractional WT (Table 11).  Switches the state to
+ * Eq. (1) with a real weight: objective = fl(fl(WT * sum T_j) + C_max) in
+ * IEEE-754 binary64 (two roundings, no fused multiply-add), fitness (Eq. (13))
+ * = max(E_max - objective, +0) and E_max = the smallest 10^a above
+ * every initial objective, all in binary64.  From then on every `objective`,
+ * `fitness`, E_max and trace word of ffs_evaluate / ffs_evaluate_host /
+ * ffs_run_* / ffs_best is the 64-bit pattern of that double (reinterpret it);
+ * the trace sum is a fixed-order binary64 sum.  Decoding does not depend on
+ * WT.  wt: finite, >= 0.  Call before ffs_evolve_begin; a run keeps the mode
+ * it started with only if the state is not switched again while it runs.
+ * Errors: FFS_ERR_INVALID_ARG for a negative or non-finite wt.
+ * ---------------------------------------------------------------------- */
+FFS_API ffs_status ffs_state_set_objective_weight(ffs_state *st, double wt);
+
+/* ------------------------------------------------------------------------
  * Decode + evaluate (Algorithm 1; Algorithm 2, P:273-289;
  * Eqs. (1)-(3)).  One warp per chromosome.
  *   x: device int8  [count*K], machine of each gene, in [0, o-1] (X(k))
  *   y: device int16 [count*K], priorities: a permutation of 1..K per
  *      chromosome, larger = earlier (Y(k)).  Not validated.
- *   objective:       device int64 [count], WT*sum T_j + C_max     (may be NULL)
+ *   objective:       device int64 [count], WT*sum T_j + C_max     (may be NULL;
+ *                    binary64 bit patterns after ffs_state_set_objective_weight)
  *   total_tardiness: device int64 [count], sum_j T_j over J u J'   (may be NULL)
  *   makespan:        device int32 [count], C_max                   (may be NULL)
  *   start_out:       device int32 [count*(n+n')*g], S_js of the merged schedule

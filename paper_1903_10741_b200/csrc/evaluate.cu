@@ -175,14 +175,11 @@ __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
     }
     T += h.frozen_T;
     if (lane == 0) {
-      int64_t obj = h.wt * T + (int64_t)cm;
+      const int64_t obj = objective_word(h.real_wt, h.wt, h.wt_f, T, cm);
       if (a.obj) a.obj[c] = obj;
       if (a.tard) a.tard[c] = T;
       if (a.cmax) a.cmax[c] = cm;
-      if (a.fit) {                                 // Eq. (13)
-        int64_t f = *a.emax - obj;
-        a.fit[c] = f > 0 ? f : 0;
-      }
+      if (a.fit) a.fit[c] = fitness_word(h.real_wt, *a.emax, obj);   // Eq. (13)
     }
     __syncwarp();
   }

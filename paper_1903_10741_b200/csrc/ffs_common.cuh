@@ -61,7 +61,9 @@ struct ImageHdr {
   int32_t hn_words0;
   uint32_t off_bn0;              // u32 [bn_words0] initial blocked bits (mode 2)
   int32_t bn_words0;
-  uint32_t pad_[2];
+  int32_t real_wt;               // 1: fractional WT (f3), objective/fitness are binary64 bit patterns
+  int32_t pad_;
+  double wt_f;                   // the real weight when real_wt
 };
 
 struct Instance {
@@ -103,7 +105,9 @@ struct HostStage {
 struct State {
   const Instance *inst = nullptr;
   int32_t rs = 0, K = 0, cells = 0;
-  std::vector<int32_t> cell_state;   // 0 pending, 1 running, 2 completed
+  std::vector<int32_t> cell_state;   // 0 pending, 1 running, 2 completed, 3 kept (static policy)
+  int32_t real_wt = 0;               // fractional WT (f3): binary64 objective words
+  double wt_f = 0.0;
   std::vector<int32_t> fassign, fstart;
   std::vector<int32_t> gene_job, gene_stage, gene_cell;
   std::vector<int32_t> pend_before;  // [cells+1]
@@ -136,6 +140,25 @@ struct State {
 };
 
 // Arguments of one evaluate launch (device pointers).
+// Eq. (1) and Eq. (13) on the 64-bit objective/fitness words:
+// integer WT (R25) -> exact int64; real WT (Table 11, f3) -> binary64 bit
+// patterns of fl(fl(WT * sum T) + C_max) and max(E_max - obj, +0).  Every
+// objective and fitness is >= 0, so the bit patterns order like the values
+// and every GA comparison (selection, replacement, migration, E_max's
+// max-reduction, trace min) works on the int64 words unchanged.
+__device__ __forceinline__ int64_t objective_word(int real, int64_t wt, double wt_f, int64_t T, int32_t cm) {
+  if (real) return __double_as_longlong(__dadd_rn(__dmul_rn(__ll2double_rn(T), wt_f), __int2double_rn(cm)));
+  return wt * T + (int64_t)cm;
+}
+__device__ __forceinline__ int64_t fitness_word(int real, int64_t emax, int64_t obj) {
+  if (real) {
+    const double f = __dsub_rn(__longlong_as_double(emax), __longlong_as_double(obj));
+    return f > 0.0 ? __double_as_longlong(f) : 0;
+  }
+  const int64_t f = emax - obj;
+  return f > 0 ? f : 0;
+}
+
 struct EvalArgs {
   const void *image;
   int64_t count;

@@ -122,15 +122,21 @@ __global__ void max_kernel(const int64_t *obj, int64_t n, int64_t *out) {
   }
 }
 
-__global__ void emax_fitness_kernel(int64_t *scal, const int64_t *obj, int64_t *fit, int64_t n) {
-  int64_t mx = scal[1];
-  int64_t E = 10;
-  while (E <= mx) E *= 10;
-  if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = E;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t f = E - obj[i];
-    fit[i] = f > 0 ? f : 0;                       // Eq. (13)
+__global__ void emax_fitness_kernel(int64_t *scal, const int64_t *obj, int64_t *fit, int64_t n, int real) {
+  int64_t E;
+  if (real) {   // binary64 words (f3); powers of ten are exact up to 1e22
+    const double mx = __longlong_as_double(scal[1]);
+    double e = 10.0;
+    while (e <= mx) e *= 10.0;
+    E = __double_as_longlong(e);
+  } else {
+    const int64_t mx = scal[1];
+    E = 10;
+    while (E <= mx) E *= 10;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = E;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    fit[i] = fitness_word(real, E, obj[i]);       // Eq. (13)
 }
 
 // ---- block helpers: argmax / argmin of fitness inside one island (ties -> lowest index)
@@ -253,10 +259,39 @@ __global__ void import_kernel(int K, size_t rec, const unsigned char *donor, con
   }
 }
 
-__global__ void trace_kernel(const int64_t *obj, int64_t n, int64_t *tmin, int64_t *tsum, int k) {
+// trace[k] = (min objective, sum of objectives).  Real-WT words (f3): the min
+// works on the words (non-negative doubles), the sum is a binary64 sum in a
+// fixed order (per-thread strided partials, then a fixed shuffle tree), so it
+// is deterministic but rounds differently from a sequential sum.
+__global__ void trace_kernel(const int64_t *obj, int64_t n, int64_t *tmin, int64_t *tsum, int k, int real) {
   __shared__ long long smin[32];
   __shared__ long long ssum[32];
+  __shared__ double dsum[32];
   long long mn = LLONG_MAX, sm = 0;
+  if (real) {
+    double ds = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      mn = min(mn, (long long)obj[i]);
+      ds += __longlong_as_double(obj[i]);
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+      ds += __shfl_xor_sync(FULL, ds, d);
+    }
+    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = mn; dsum[threadIdx.x >> 5] = ds; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = blockDim.x >> 5;
+      mn = threadIdx.x < nw ? smin[threadIdx.x] : LLONG_MAX;
+      ds = threadIdx.x < nw ? dsum[threadIdx.x] : 0.0;
+      for (int d = 16; d > 0; d >>= 1) {
+        mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+        ds += __shfl_xor_sync(FULL, ds, d);
+      }
+      if (threadIdx.x == 0) { tmin[k] = mn; tsum[k] = __double_as_longlong(ds); }
+    }
+    return;
+  }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     mn = min(mn, (long long)obj[i]);
     sm += obj[i];
@@ -495,12 +530,12 @@ static ffs_status ga_init(Run &r) {
       return fail(FFS_ERR_COMM, "allreduce_max_i64 hook failed");
   }
   emax_fitness_kernel<<<(unsigned)std::min<int64_t>((r.nloc + 255) / 256, 1024), 256, 0, r.s>>>(
-      r.scal, r.obj[0], r.fit[0], r.nloc);
+      r.scal, r.obj[0], r.fit[0], r.nloc, st.real_wt);
   FFS_CUDA(cudaGetLastError());
   history_init_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.x[0], r.y[0], r.obj[0], r.fit[0], r.hx, r.hy, r.hobj,
                                                r.hfit);
   FFS_CUDA(cudaGetLastError());
-  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.tmin, r.tsum, 0);
+  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.tmin, r.tsum, 0, st.real_wt);
   FFS_CUDA(cudaGetLastError());
   r.launches += 3;
   r.cur = 0;
@@ -554,7 +589,7 @@ static ffs_status ga_generation(Run &r) {
     FFS_CUDA(cudaGetLastError());
     r.launches++;
   }
-  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[nb], r.nloc, r.tmin, r.tsum, k);
+  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[nb], r.nloc, r.tmin, r.tsum, k, st.real_wt);
   FFS_CUDA(cudaGetLastError());
   r.launches++;
   r.cur = nb;

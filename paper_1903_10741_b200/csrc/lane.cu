@@ -564,14 +564,11 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
       cm = max(cm, Cr + h.rs);
     }
     T += h.frozen_T;
-    const int64_t obj = h.wt * T + (int64_t)cm;
+    const int64_t obj = objective_word(h.real_wt, h.wt, h.wt_f, T, cm);
     if (a.obj) a.obj[gc] = obj;
     if (a.tard) a.tard[gc] = T;
     if (a.cmax) a.cmax[gc] = cm;
-    if (a.fit) {  // Eq. (13)
-      int64_t fv = *a.emax - obj;
-      a.fit[gc] = fv > 0 ? fv : 0;
-    }
+    if (a.fit) a.fit[gc] = fitness_word(h.real_wt, *a.emax, obj);   // Eq. (13)
   }
 }
 

@@ -133,7 +133,7 @@ ffs_status State::build_image() {
   std::memset(&H, 0, sizeof(H));
   H.K = K; H.NJ = NJ; H.G = G; H.O = O; H.rs = rs; H.q_max = in.q_max;
   H.n_pjobs = (int32_t)pjob.size();
-  H.wt = in.wt; H.frozen_T = frozen_T; H.frozen_cmax = (int32_t)frozen_cmax; H.cells = cells;
+  H.wt = in.wt; H.real_wt = real_wt; H.wt_f = wt_f; H.frozen_T = frozen_T; H.frozen_cmax = (int32_t)frozen_cmax; H.cells = cells;
   int32_t qmin = in.q_max, qmaxv = 0, pmax = 0;
   for (size_t i = 0; i < in.Q.size(); ++i) {
     qmin = std::min(qmin, in.Q[i]);
@@ -517,6 +517,15 @@ ffs_status ffs_state_cut_table(const ffs_state *h, int32_t *pb) {
 ffs_status ffs_state_set_horizon_cap(ffs_state *h, int32_t cap) {
   if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
   h->v.h_cap_user = cap > 0 ? cap : 0;
+  cudaSetDevice(h->v.inst->dev);
+  return h->v.build_image();
+}
+
+ffs_status ffs_state_set_objective_weight(ffs_state *h, double wt) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
+  if (!(wt >= 0.0) || wt > 1e300) return fail(FFS_ERR_INVALID_ARG, "WT must be finite and >= 0");
+  h->v.real_wt = 1;
+  h->v.wt_f = wt;
   cudaSetDevice(h->v.inst->dev);
   return h->v.build_image();
 }

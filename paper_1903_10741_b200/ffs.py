@@ -25,7 +25,7 @@ MUT_010 = 429496729   # floor(0.1 * 2^32), mutation rate of P:395
 EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
-    "ffs_state_set_horizon_cap", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
+    "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
     "ffs_evaluate_host", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
     "ffs_run_destroy",
@@ -79,6 +79,7 @@ def lib():
             "ffs_state_genes": ([P, P, P], C.c_int), "ffs_state_cells": ([P, P], C.c_int),
             "ffs_state_cut_table": ([P, P], C.c_int),
             "ffs_state_set_horizon_cap": ([P, C.c_int32], C.c_int),
+            "ffs_state_set_objective_weight": ([P, C.c_double], C.c_int),
             "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
             "ffs_evaluate": ([P, C.c_int64, P, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
@@ -166,6 +167,7 @@ class State:
         self.h = h
         self.K = K.value
         self.rs = int(rs)
+        self.real_wt = None
         self.cells = inst.NJ * inst.g
 
     def __del__(self):
@@ -188,6 +190,12 @@ class State:
         c = np.zeros(self.cells + 1, np.int32)
         _check(lib().ffs_state_cut_table(self.h, _np_ptr(c)), "ffs_state_cut_table")
         return c
+
+    def set_objective_weight(self, wt: float):
+        """Fractional WT (Table 11): objectives/fitness become binary64."""
+        _check(lib().ffs_state_set_objective_weight(self.h, C.c_double(float(wt))),
+               "ffs_state_set_objective_weight")
+        self.real_wt = float(wt)
 
     def set_horizon_cap(self, cap: int):
         _check(lib().ffs_state_set_horizon_cap(self.h, int(cap)), "ffs_state_set_horizon_cap")
@@ -220,6 +228,8 @@ def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=
                               _dev_ptr(makespan, torch.int32, count, "makespan"),
                               _dev_ptr(start_out, torch.int32, count * state.cells, "start_out"),
                               _stream(stream)), "ffs_evaluate")
+    if state.real_wt is not None:
+        objective = objective.view(torch.float64)
     return objective, total_tardiness, makespan, start_out
 
 
@@ -233,7 +243,12 @@ def evaluate_host(state: State, x: np.ndarray, y: np.ndarray, stream=None):
     M = np.zeros(count, np.int32)
     _check(lib().ffs_evaluate_host(state.h, count, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(T), _np_ptr(M),
                                    _stream(stream)), "ffs_evaluate_host")
-    return obj, T, M
+    return _words(state, obj), T, M
+
+
+def _words(state: State, a: np.ndarray) -> np.ndarray:
+    """64-bit objective words as values: int64, or binary64 in real-WT mode."""
+    return a.view(np.float64) if state.real_wt is not None else a
 
 
 def evaluate_host_into(state: State, x: np.ndarray, y: np.ndarray, obj: np.ndarray, T: np.ndarray,
@@ -331,7 +346,10 @@ class Run:
         ev = C.c_int64()
         nl = C.c_int32()
         _check(lib().ffs_run_info(self.h, C.byref(g), C.byref(e), C.byref(ev), C.byref(nl)), "ffs_run_info")
-        return dict(generation=g.value, emax=e.value, evaluations=ev.value, launches=nl.value)
+        emax = e.value
+        if self.state.real_wt is not None:
+            emax = float(np.array([emax], np.int64).view(np.float64)[0])
+        return dict(generation=g.value, emax=emax, evaluations=ev.value, launches=nl.value)
 
     def population(self):
         K = self.state.K
@@ -341,7 +359,7 @@ class Run:
         fit = np.zeros(self.nloc, np.int64)
         _check(lib().ffs_run_population(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)),
                "ffs_run_population")
-        return x, y, obj, fit
+        return x, y, _words(self.state, obj), _words(self.state, fit)
 
     def history(self):
         K = self.state.K
@@ -350,7 +368,7 @@ class Run:
         obj = np.zeros(self.nisl, np.int64)
         fit = np.zeros(self.nisl, np.int64)
         _check(lib().ffs_run_history(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)), "ffs_run_history")
-        return x, y, obj, fit
+        return x, y, _words(self.state, obj), _words(self.state, fit)
 
     def best(self):
         K, cells = self.state.K, self.state.cells
@@ -364,5 +382,9 @@ class Run:
         tsum = np.zeros(max(g + 1, 1), np.int64)
         _check(lib().ffs_best(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(assign), _np_ptr(start), C.byref(obj),
                               C.byref(T), C.byref(M), _np_ptr(tmin), _np_ptr(tsum)), "ffs_best")
-        return dict(x=x[:K], y=y[:K], assign=assign, start=start, objective=obj.value, sum_tardiness=T.value,
-                    makespan=M.value, trace_min=tmin[:g + 1], trace_sum=tsum[:g + 1])
+        objective = obj.value
+        if self.state.real_wt is not None:
+            objective = float(np.array([objective], np.int64).view(np.float64)[0])
+        return dict(x=x[:K], y=y[:K], assign=assign, start=start, objective=objective, sum_tardiness=T.value,
+                    makespan=M.value, trace_min=_words(self.state, tmin[:g + 1]),
+                    trace_sum=_words(self.state, tsum[:g + 1]))

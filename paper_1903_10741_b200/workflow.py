@@ -142,3 +142,50 @@ def compare_policies(ratios=(0.2, 0.4, 0.6, 0.8), seeds=(1903,), shape=(8, 8, 64
         rows.append(PolicyRow(ratio=ratio, n_prime=int(wl.arr_event.size), static_mean=sm, dynamic_mean=dm,
                               improvement_ratio=sm / dm if dm > 0 else float("inf"), runs=runs))
     return rows
+
+
+# ---------------------------------------------------------------------------
+# WT sensitivity (Table 11)
+# ---------------------------------------------------------------------------
+TABLE11_WT = (0.01, 0.1, 0.4, 0.7, 1.0, 4.0, 7.0, 10.0, 100.0)
+
+
+@dataclass
+class WeightRow:
+    wt: float
+    tardiness_mean: float
+    makespan_mean: float
+    objective_mean: float
+    runs: List[dict]
+
+
+def wt_sweep(wts=TABLE11_WT, seeds=(1903,), ratio: float = 0.5, shape=(8, 8, 64), generations: int = 100,
+             device: int = 0, make_workload=test3_workload, stream=None) -> List[WeightRow]:
+    """For every seed: plan the originals with the instance's integer WT (GA at
+    RS = 0), freeze at RS = floor(ratio * C_max) (reading R32), then for every
+    WT of the grid re-optimise with the fractional objective
+    fl(fl(WT * sum T) + C_max) (ffs_state_set_objective_weight) and record the
+    best schedule's sum T, C_max and objective (Table 11's columns)."""
+    rows = []
+    ctxs = []
+    for seed in seeds:
+        wl = make_workload(ratio, seed)
+        base = ffs.Instance.from_arrays(wl.original_instance(), device=device)
+        st0 = ffs.make_state(base, 0)
+        plan = _evolve(st0, shape, generations, seed, stream)
+        rs = wl.rs_from_makespan(ratio, plan.makespan)
+        inst = ffs.Instance.from_arrays(wl.instance_at(0, [rs]), device=device)
+        n_g = wl.n * wl.g
+        ctxs.append((seed, rs, inst, plan.assign[:n_g], plan.start[:n_g], base, st0))
+    for wt in wts:
+        runs = []
+        for seed, rs, inst, oa, os_, _, _ in ctxs:
+            st = ffs.make_state(inst, rs, oa, os_)
+            st.set_objective_weight(wt)
+            ev = _evolve(st, shape, generations, seed + 1, stream)
+            runs.append(dict(seed=seed, rs=rs, K=ev.K, objective=ev.objective, sum_tardiness=ev.sum_tardiness,
+                             makespan=ev.makespan, result=ev))
+        rows.append(WeightRow(wt=float(wt), tardiness_mean=float(np.mean([r["sum_tardiness"] for r in runs])),
+                              makespan_mean=float(np.mean([r["makespan"] for r in runs])),
+                              objective_mean=float(np.mean([r["objective"] for r in runs])), runs=runs))
+    return rows

@@ -18,7 +18,7 @@ from oracle import oracle as orc
 from paper_1903_10741_b200 import workload as wlmod
 from tests import fixtures as fx
 
-TABLE11_WT = [0.01, 0.1, 1.0, 10.0, 100.0]
+TABLE11_WT = [0.01, 0.1, 0.4, 0.7, 1.0, 4.0, 7.0, 10.0, 100.0]       # Table 11
 
 
 def test_emax_and_fitness_real_closed_forms():
