@@ -407,6 +407,19 @@ def run_ours(args):
                                         "makespan": r.makespan_mean, "objective": r.objective_mean}
                                        for r in wrows]}}
 
+    # ---- f4: GPU brute force (ground truth) on a K = 12 instance at RS = 0
+    brute = None
+    if world == 1:
+        wlb = wlmod.gen_v1("bf", 4, 3, 2, 3, seed=12)
+        bst = ffs.make_state(ffs.Instance.from_arrays(wlb.original_instance(), device=local), 0)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        bbest, bev, _, _ = ffs.brute_force(bst, stream=stream)
+        dt = time.perf_counter() - t0
+        brute = {"workload": "gen-v1 4 jobs x 3 stages x 2 machines, Q_max=3, RS=0: K=12, 2^12 x 12!/(3!)^4 "
+                             "decodes", "K": bst.K, "decodes": bev, "seconds": dt, "decodes_per_s": bev / dt,
+                 "best_objective": bbest}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -424,6 +437,7 @@ def run_ours(args):
             "static_C": static_c,
             "policy_T10": policy,
             "real_wt": realwt,
+            "brute_force": brute,
             "clocks": clk.summary(),
         }
         alg_ops = None

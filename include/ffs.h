@@ -170,6 +170,23 @@ FFS_API ffs_status ffs_evaluate(const ffs_state *st, int64_t count, const int8_t
 FFS_API ffs_status ffs_evaluate_host(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
                              int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                              void *cuda_stream);
+/* ------------------------------------------------------------------------
+ * Brute force over the decoder-reachable set:
+ * every X in [0, o-1]^K times every linear extension of the job chains (the
+ * orders Algorithm 1 can produce; o^K * K!/prod_j L_j! of them,
+ * L_j = pending ops of job j), each decoded by the ffs_evaluate kernels.
+ * Enumeration index i = order_rank * o^K + x_rank (x_rank = K base-o digits,
+ * gene g = digit g; order_rank = multinomial rank, jobs ascending); the
+ * chromosome of an order has y = K - position.  Ties -> lowest index.
+ *   limit: maximum number of decodes; FFS_ERR_INVALID_ARG beyond it, for
+ *          K = 0, K > 64 or more than 64 jobs with pending ops.
+ *   best_objective: host, the minimum objective word (binary64 pattern in
+ *          real-WT mode); evaluated: host, the number of decodes;
+ *   best_x [K], best_y [K]: host, a chromosome reaching it (may be NULL).
+ * Synchronises `cuda_stream`.
+ * ---------------------------------------------------------------------- */
+FFS_API ffs_status ffs_brute_force(const ffs_state *st, int64_t limit, int64_t *best_objective, int64_t *evaluated,
+                                   int8_t *best_x, int16_t *best_y, void *cuda_stream);
 /* Counter-based random chromosomes (the GA's initialisation operator,
  * P:227): chromosome id -> island id>>20, individual id&(2^20-1); device
  * x [count*K], y [count*K]. */

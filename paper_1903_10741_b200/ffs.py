@@ -26,7 +26,7 @@ EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
     "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
-    "ffs_evaluate_host", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
+    "ffs_evaluate_host", "ffs_brute_force", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
     "ffs_run_destroy",
 ]
@@ -80,6 +80,7 @@ def lib():
             "ffs_state_cut_table": ([P, P], C.c_int),
             "ffs_state_set_horizon_cap": ([P, C.c_int32], C.c_int),
             "ffs_state_set_objective_weight": ([P, C.c_double], C.c_int),
+            "ffs_brute_force": ([P, C.c_int64, P, P, P, P, P], C.c_int),
             "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
             "ffs_evaluate": ([P, C.c_int64, P, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
@@ -256,6 +257,21 @@ def evaluate_host_into(state: State, x: np.ndarray, y: np.ndarray, obj: np.ndarr
     """evaluate_host() into caller-provided (e.g. pinned) host buffers."""
     _check(lib().ffs_evaluate_host(state.h, x.shape[0], _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(T),
                                    _np_ptr(M), _stream(stream)), "ffs_evaluate_host")
+
+
+def brute_force(state: State, limit: int = 1 << 34, stream=None):
+    """Exhaustive ground truth over o^K x linear extensions (ffs_brute_force):
+    returns (best objective, evaluated, best x [K], best y [K])."""
+    K = state.K
+    best, ev = C.c_int64(), C.c_int64()
+    bx = np.zeros(max(K, 1), np.int8)
+    by = np.zeros(max(K, 1), np.int16)
+    _check(lib().ffs_brute_force(state.h, int(limit), C.byref(best), C.byref(ev), _np_ptr(bx), _np_ptr(by),
+                                 _stream(stream)), "ffs_brute_force")
+    b = best.value
+    if state.real_wt is not None:
+        b = float(np.array([b], np.int64).view(np.float64)[0])
+    return b, ev.value, bx[:K], by[:K]
 
 
 def random_population(state: State, count: int, seed: int, first_id: int = 0, device=None, stream=None):
