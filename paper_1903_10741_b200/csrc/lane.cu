@@ -92,33 +92,27 @@ struct OrdArgs {
   uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
 };
 
-// (v, f) segmented-min combine of an inclusive scan (f = segment head seen)
-__device__ __forceinline__ void segmin_scan(int &v, uint32_t &f, int lane) {
+// prefix minima of the lane's four genes given the running min before the tile
+__device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, int lane, int pm[4]) {
+  // v = min over the lane's genes from its last segment head (or all four)
+  int v = y[0];
+#pragma unroll
+  for (int k = 1; k < 4; ++k) v = ((h >> k) & 1u) ? y[k] : min(v, y[k]);
+  // lanes whose quad holds a segment head; the scan of lane l only combines
+  // lanes >= the last head lane <= l (one shuffle per step)
+  const uint32_t hb = __ballot_sync(FULL, h != 0u);
+  const uint32_t below = hb & (0xFFFFFFFFu >> (31 - lane));      // head lanes <= lane
+  const int s0 = below ? 31 - __clz(below) : -1;                    // -1: no head in this tile yet
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int vn = __shfl_up_sync(FULL, v, d);
-    const uint32_t fn = __shfl_up_sync(FULL, f, d);
-    if (lane >= d) {
-      if (!f) v = min(v, vn);
-      f |= fn;
-    }
+    if (lane - d >= s0 && lane >= d) v = min(v, vn);
   }
-}
-
-// prefix minima of the lane's four genes given the running min before the tile
-__device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, int lane, int pm[4]) {
-  int v = y[0];
-  uint32_t f = h & 1u;
-#pragma unroll
-  for (int k = 1; k < 4; ++k) {
-    const bool hk = (h >> k) & 1u;
-    v = hk ? y[k] : min(v, y[k]);
-    f |= hk;
-  }
-  segmin_scan(v, f, lane);
+  // exclusive value for the lane: min over lanes [s_prev, lane-1] (+ carry if
+  // no head since the tile start)
   const int vex = __shfl_up_sync(FULL, v, 1);
-  const uint32_t fex = __shfl_up_sync(FULL, f, 1);
-  int run = lane == 0 ? carry : (fex ? vex : min(vex, carry));
+  const uint32_t bex = hb & ((1u << lane) - 1u);                    // head lanes < lane
+  int run = lane == 0 ? carry : (bex ? vex : min(vex, carry));
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     run = ((h >> k) & 1u) ? y[k] : min(run, y[k]);
@@ -135,6 +129,13 @@ __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *hea
   // genes past the end are their own segments (never merge into valid ones)
   const int valid = K - g0;
   if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
+}
+
+__device__ __forceinline__ void load_xquad(const int8_t *xr, int K, int g0, uint32_t &xw) {
+  xw = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (g0 + k < K) xw |= (uint32_t)(uint8_t)__ldg(xr + g0 + k) << (8 * k);
 }
 
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
@@ -168,17 +169,21 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       __syncwarp();
       // ---- pass A: prefix minima (kept with a leader flag in bit 15), histogram
       int carry = INT_MAX;
+      // software pipeline: tile t+1's genes are loaded while tile t is scanned
+      int yq[4];
+      uint32_t hq, xq;
+      load_quad(yr, headS, K, 4 * lane, yq, hq);
+      load_xquad(xr, K, 4 * lane, xq);
       for (int t = 0; t < NT; ++t) {
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
-        uint32_t h;
-        load_quad(yr, headS, K, g0, y, h);
-        {
-          uint32_t xw = 0;
+        uint32_t h = hq;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (g0 + k < K) xw |= (uint32_t)(uint8_t)__ldg(xr + g0 + k) << (8 * k);
-          *(uint32_t *)(xs + g0) = xw;
+        for (int k = 0; k < 4; ++k) y[k] = yq[k];
+        *(uint32_t *)(xs + g0) = xq;
+        if (t + 1 < NT) {
+          load_quad(yr, headS, K, g0 + 128, yq, hq);
+          load_xquad(xr, K, g0 + 128, xq);
         }
         pm_quad(y, h, carry, lane, pm);
         uint32_t pk[4];
@@ -223,13 +228,11 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (pk[k] & 0x8000u) lp = g0 + k;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int n = __shfl_up_sync(FULL, lp, d);
-          if (lane >= d) lp = max(lp, n);
-        }
-        int run = __shfl_up_sync(FULL, lp, 1);
-        run = lane == 0 ? carry_lp : max(run, carry_lp);
+        // last leader before this lane's quad: the highest lower lane holding one
+        const uint32_t lb = __ballot_sync(FULL, lp >= 0) & ((1u << lane) - 1u);
+        const int src = lb ? 31 - __clz(lb) : 0;
+        const int lpx = __shfl_sync(FULL, lp, src);
+        int run = lb ? lpx : carry_lp;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
@@ -240,7 +243,11 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const int gg = ok ? g : 0;
           ord[r] = (uint16_t)(gtab[gg] + (uint32_t)xs[gg]);
         }
-        carry_lp = max(carry_lp, __shfl_sync(FULL, lp, 31));
+        {
+          const uint32_t all = __ballot_sync(FULL, lp >= 0);
+          const int last = __shfl_sync(FULL, lp, all ? 31 - __clz(all) : 0);
+          if (all) carry_lp = last;
+        }
       }
     }
     __syncthreads();
