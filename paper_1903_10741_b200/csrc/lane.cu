@@ -490,8 +490,26 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
           f &= (f >> 2) | A.M2;
           f &= (f >> 4) | A.M4;
           f &= f >> A.sft;
-          int S = t0 + __ffs(f) - 1;
-          if (f == 0u || (!UQ && A.q != qmin)) S = lane_search(L, t0, A.p, UQ ? 0 : A.q - qmin, bias4);
+          int S;
+          if (UQ) {
+            // window miss: slide by 33 - p ticks (a run starting in the last
+            // p - 1 ticks of the window was not testable) with the same masks;
+            // the zero sentinel words past the horizon end the loop
+            int t = t0;
+            while (f == 0u) {
+              t += 33 - A.p;
+              const uint32_t bwb = waddr(L, BB + min(t >> 5, BW));
+              f = ~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31);
+              f &= (f >> 1) | A.M1;
+              f &= (f >> 2) | A.M2;
+              f &= (f >> 4) | A.M4;
+              f &= f >> A.sft;
+            }
+            S = t + __ffs(f) - 1;
+          } else {
+            S = t0 + __ffs(f) - 1;
+            if (f == 0u || A.q != qmin) S = lane_search(L, t0, A.p, A.q - qmin, bias4);
+          }
           const int C = S + A.p;
           if (C > hcap) {
             ovf = true;
