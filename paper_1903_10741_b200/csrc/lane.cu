@@ -323,26 +323,34 @@ struct OpA {
 __device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
 __device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
 template <bool NIB>
-__device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
+__device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, uint32_t mbase, uint32_t pt_base,
+                                       int GO, uint32_t e) {
   OpA A;
   const uint32_t tv = pqt[e];
   A.e = e;
   if (NIB) {
-    // host-packed (mode 2): p-1 | ready word | field | machine word | field |
-    // run-test masks (p<2, p<4, p<8) | p - 2^floor(log2 p)
-    A.p = (int)(tv & 7u) + 1;
+    // host-packed (mode 2): rsh[0:5] | msh[5:10] | ready word[10:21] |
+    // machine word[21:29] | p-1[29:32].  The field shifts are used by wrap
+    // (mod 32) funnel shifts, so they need no extraction; the p-dependent
+    // run-test shifts and the nibble-mask column come from ptab[p-1].
+    const uint32_t pm1 = tv >> 29;
+    A.p = (int)pm1 + 1;
     A.q = 1;
-    A.ra = waddr(L, (int)((tv >> 3) & 0x7FFu));
-    A.rsh = (int)((tv >> 14) & 3u) * 10;
-    A.ma = waddr(L, L.RW + (int)((tv >> 16) & 0x1FFu));
-    A.msh = (int)((tv >> 25) & 3u) * 10;
-    A.M1 = (uint32_t)((int32_t)(tv << 4) >> 31);
-    A.M2 = (uint32_t)((int32_t)(tv << 3) >> 31);
-    A.M4 = (uint32_t)((int32_t)(tv << 2) >> 31);
-    A.sft = (int)(tv >> 30);
+    A.rsh = (int)tv;
+    A.msh = (int)(tv >> 5);
+    A.ra = L.base + ((tv >> 3) & 0x3FF80u);
+    A.ma = mbase + ((tv >> 14) & 0x7F80u);
+    uint4 pt;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(pt.x), "=r"(pt.y), "=r"(pt.z), "=r"(pt.w)
+                 : "r"(pt_base + (pm1 << 4)));
+    A.M1 = pt.x;
+    A.M2 = pt.y;
+    A.M4 = pt.z;
+    A.nmo = pt.w;                               // address of the nibble-mask column of p
+    A.sft = 0;
     A.QQ = 0x01010101u;
-    A.nmo = (uint32_t)(tv & 7u) << 3;           // (p - 1) * 8: column of the nibble-mask table
-    pin(A.ra); pin(A.ma); pin(A.rsh); pin(A.msh); pin(A.M1); pin(A.M2); pin(A.M4); pin(A.sft); pin(A.p);
+    pin(A.ra); pin(A.ma); pin(A.rsh); pin(A.msh); pin(A.M1); pin(A.M2); pin(A.M4); pin(A.p);
     pin(A.nmo);
     return A;
   }
@@ -362,6 +370,32 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, in
   A.sft = pp - (1 << (31 - __clz(pp)));
   A.nmo = 0;
   return A;
+}
+
+// first run of p free ticks: mode 2 shifts by ptab's (a, b, c) with
+// runs(p) = ((f & f>>a) & ..>>b) & ..>>c; modes 0/1 use the doubling masks
+template <bool NIB>
+__device__ __forceinline__ uint32_t run_test(uint32_t f, const OpA &A) {
+  if (NIB) {
+    f &= __funnelshift_r(f, 0u, A.M1);
+    f &= __funnelshift_r(f, 0u, A.M2);
+    f &= __funnelshift_r(f, 0u, A.M4);
+    return f;
+  }
+  f &= (f >> 1) | A.M1;
+  f &= (f >> 2) | A.M2;
+  f &= (f >> 4) | A.M4;
+  return f & (f >> A.sft);
+}
+// field extraction / placement at a per-op shift (mode 2: wrap shifts of the
+// raw table word)
+template <bool NIB>
+__device__ __forceinline__ uint32_t field_at(uint32_t w, int sh) {
+  return NIB ? __funnelshift_r(w, 0u, (uint32_t)sh) : w >> sh;
+}
+template <bool NIB>
+__device__ __forceinline__ uint32_t place_at(uint32_t v, int sh) {
+  return NIB ? __funnelshift_l(0u, v, (uint32_t)sh) : v << sh;
 }
 
 // exact per-nibble zero test: bit 3 of each nibble set iff that nibble is 0
@@ -403,11 +437,19 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     for (int i = 0; i < p; ++i) m |= 1ull << (4 * (lo + i));
     nmask[threadIdx.x] = make_uint2((uint32_t)m, (uint32_t)(m >> 32));
   }
+  __shared__ uint4 ptab[8];      // mode 2, by p-1: run-test shifts (a, b, c), nibble-mask column address
+  if (NIB && threadIdx.x < 8) {
+    const int p = threadIdx.x + 1;
+    const uint32_t sa = p >= 2 ? 1u : 0u;
+    const uint32_t sb = p >= 4 ? 2u : (p == 3 ? 1u : 0u);
+    const uint32_t sc = p >= 5 ? (uint32_t)(p - 4) : 0u;
+    ptab[threadIdx.x] = make_uint4(sa, sb, sc, smem_u32(nmask) + (uint32_t)(8 * (p - 1)));
+  }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
-  uint32_t cm_base = smem_u32(cmask), nm_base = smem_u32(nmask);
+  uint32_t cm_base = smem_u32(cmask), pt_base = smem_u32(ptab);
   pin(cm_base);
-  pin(nm_base);
+  pin(pt_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
   const int K = h.K, KQ = (K + 3) >> 2, GO = h.G * h.O;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -427,8 +469,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   const int qmin = h.q_max - h.thr_min, lvw0 = h.lvl_words0;
   const uint32_t bias4 = (uint32_t)(0x7F - h.thr_min) * 0x01010101u;
   int hcap = L.hcap, BW = L.BW;
+  uint32_t mbase = waddr(L, L.RW);
   pin(hcap);
   pin(BW);
+  pin(mbase);
   const int64_t ntile = (a.count + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
@@ -467,7 +511,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     // constant (stage A) is computed while the current op runs (B..E)
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
-    OpA nA = stage_a<NIB>(pqt, L, GO, cur.x & 0xFFFFu);
+    OpA nA = stage_a<NIB>(pqt, L, mbase, pt_base, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
       const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
@@ -476,20 +520,16 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         const OpA A = nA;
         {   // stage A of rank 4*qd + k + 1
           const uint32_t en = k == 0 ? cur.x >> 16 : k == 1 ? cur.y : k == 2 ? cur.y >> 16 : nxt.x;
-          nA = stage_a<NIB>(pqt, L, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
+          nA = stage_a<NIB>(pqt, L, mbase, pt_base, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
         }
         if (live && k < nk) {
           // B: t0 = max(RS, release / predecessor completion, machine free)
           const uint32_t rw = lds(A.ra), mw = lds(A.ma);
-          const int t0 = max((int)((rw >> A.rsh) & TM), (int)((mw >> A.msh) & TM));
+          const int t0 = max((int)(field_at<NIB>(rw, A.rsh) & TM), (int)(field_at<NIB>(mw, A.msh) & TM));
           // C: first run of p un-blocked ticks in the 32-tick window at t0
           //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
           const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
-          uint32_t f = ~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31);
-          f &= (f >> 1) | A.M1;
-          f &= (f >> 2) | A.M2;
-          f &= (f >> 4) | A.M4;
-          f &= f >> A.sft;
+          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), A);
           int S;
           if (UQ) {
             // window miss: slide by 33 - p ticks (a run starting in the last
@@ -499,11 +539,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             while (f == 0u) {
               t += 33 - A.p;
               const uint32_t bwb = waddr(L, BB + min(t >> 5, BW));
-              f = ~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31);
-              f &= (f >> 1) | A.M1;
-              f &= (f >> 2) | A.M2;
-              f &= (f >> 4) | A.M4;
-              f &= f >> A.sft;
+              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31), A);
             }
             S = t + __ffs(f) - 1;
           } else {
@@ -516,8 +552,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             live = false;
           } else {
             // E: job / machine times (the next op's loads follow in program order)
-            sts(A.ra, (rw & ~(TM << A.rsh)) | ((uint32_t)C << A.rsh));
-            sts(A.ma, (mw & ~(TM << A.msh)) | ((uint32_t)C << A.msh));
+            sts(A.ra, (rw & ~place_at<NIB>(TM, A.rsh)) | place_at<NIB>((uint32_t)C, A.rsh));
+            sts(A.ma, (mw & ~place_at<NIB>(TM, A.msh)) | place_at<NIB>((uint32_t)C, A.msh));
             if (NIB) {
               // D: headroom -= 1 on [S, C) (<= 2 words, p <= 8); newly
               // exhausted ticks become blocked
@@ -525,7 +561,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
               uint2 nm;
               asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
                            : "=r"(nm.x), "=r"(nm.y)
-                           : "r"(nm_base + ((uint32_t)(S & 7) << 6) + A.nmo));
+                           : "r"(A.nmo + ((uint32_t)(S & 7) << 6)));
               const uint32_t a0 = waddr(L, LB + w0);
               const uint32_t ba = waddr(L, BB + (w0 >> 2));
               const uint32_t B0 = lds(ba);

@@ -142,7 +142,7 @@ ffs_status State::build_image() {
   }
   const bool uq = qmin == qmaxv;
   // lane decode profile: nibble headroom when every Q_jsm == 1 and Q_max <= 15
-  const int lmode = (uq && qmin == 1 && in.q_max <= 15 && NJ <= 6144 && G * O <= 1536) ? 2 : (uq ? 1 : 0);
+  const int lmode = (uq && qmin == 1 && in.q_max <= 15 && NJ <= 6144 && G * O <= 768) ? 2 : (uq ? 1 : 0);
   // lane-decode prefix (staged by the lane kernels), then warp-path tables
   H.lane_mode = lmode;
   H.hn_words0 = (int32_t)((Lr + 7) / 8);
@@ -209,13 +209,11 @@ ffs_status State::build_image() {
         size_t i = (size_t)j * G * O + so;
         if (lmode == 2) {
           // everything the lane decoder needs about the op, precomputed:
-          // p-1 | j/3 | j%3 | mi/3 | mi%3 | p<2 | p<4 | p<8 | p - 2^floor(log2 p)
+          // shift of the job's 10-bit ready field [0:5] | of the machine's
+          // field [5:10] | ready word j/3 [10:21] | machine word mi/3 [21:29] | p-1 [29:32]
           const uint32_t pv = (uint32_t)in.P[i];
-          uint32_t k = 1;
-          while (2 * k <= pv) k *= 2;
-          pqt[i] = (pv - 1) | ((uint32_t)(j / 3) << 3) | ((uint32_t)(j % 3) << 14) | ((uint32_t)(so / 3) << 16) |
-                   ((uint32_t)(so % 3) << 25) | ((pv < 2 ? 1u : 0u) << 27) | ((pv < 4 ? 1u : 0u) << 28) |
-                   ((pv < 8 ? 1u : 0u) << 29) | ((pv - k) << 30);
+          pqt[i] = (uint32_t)((j % 3) * 10) | ((uint32_t)((so % 3) * 10) << 5) | ((uint32_t)(j / 3) << 10) |
+                   ((uint32_t)(so / 3) << 21) | ((pv - 1) << 29);
         } else {
           pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
         }
@@ -266,7 +264,7 @@ ffs_status State::build_image() {
   // --- lane-decode path (one lane per chromosome): eligibility and geometry
   lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 8 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
   if (lane_ok) {
-    const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 2048;   // static smem: mask tables + mbarrier
+    const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 3072;   // static smem: mask tables + mbarrier
     const int64_t fixed_words = lmode == 2 ? (NJ + 2) / 3 + (G * O + 2) / 3 : (NJ + 1) / 2 + (G * O + 1) / 2;
     auto words = [&](int64_t hc) {   // + 2 sentinel words of `blocked`
       return fixed_words + (lmode == 2 ? hc / 8 : hc / 4) + hc / 32 + 2;
