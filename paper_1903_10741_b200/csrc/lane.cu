@@ -347,7 +347,7 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, ui
     A.M1 = pt.x;
     A.M2 = pt.y;
     A.M4 = pt.z;
-    A.nmo = pt.w;                               // address of the nibble-mask column of p
+    A.nmo = pt.w;                               // (1 << p) - 1
     A.sft = 0;
     A.QQ = 0x01010101u;
     pin(A.ra); pin(A.ma); pin(A.rsh); pin(A.msh); pin(A.M1); pin(A.M2); pin(A.M4); pin(A.p);
@@ -398,22 +398,10 @@ __device__ __forceinline__ uint32_t place_at(uint32_t v, int sh) {
   return NIB ? __funnelshift_l(0u, v, (uint32_t)sh) : v << sh;
 }
 
-// exact per-nibble zero test: bit 3 of each nibble set iff that nibble is 0
-__device__ __forceinline__ uint32_t zero_nibbles(uint32_t x) {
-  const uint32_t t = (x & 0x77777777u) + 0x77777777u;
-  return ~(t | x) & 0x88888888u;
-}
-// the 8 nibble flags (bits 3, 7, ..., 31) packed into 8 consecutive bits
-__device__ __forceinline__ uint32_t pack8(uint32_t z) {
-  uint32_t y = z >> 3;
-  y = (y | (y >> 3)) & 0x03030303u;
-  y = (y | (y >> 6)) & 0x000F000Fu;
-  return (y | (y >> 12)) & 0xFFu;
-}
-
 // MODE 0: byte levels, general Q; MODE 1: byte levels, uniform Q;
-// MODE 2: nibble HEADROOM Q_max - Q_t (every Q_jsm == 1, Q_max <= 15):
-//         blocked <=> headroom == 0, commit subtracts 1 per tick.
+// MODE 2: HEADROOM Q_max - Q_t in four bit planes per 32 ticks (every Q_jsm
+//         == 1, Q_max <= 15): blocked <=> headroom == 0, commit subtracts 1
+//         per tick with a borrow chain across the planes.
 template <int MODE, bool SCHED>
 __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
   constexpr bool UQ = MODE != 0;
@@ -430,20 +418,13 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     m.w = 0u;
     cmask[threadIdx.x] = m;
   }
-  __shared__ uint2 nmask[64];    // nibble units of [S, S+p) over words S/8, S/8+1, by (S%8, p-1)
-  if (NIB && threadIdx.x < 64) {
-    const int lo = threadIdx.x >> 3, p = (threadIdx.x & 7) + 1;
-    uint64_t m = 0;
-    for (int i = 0; i < p; ++i) m |= 1ull << (4 * (lo + i));
-    nmask[threadIdx.x] = make_uint2((uint32_t)m, (uint32_t)(m >> 32));
-  }
-  __shared__ uint4 ptab[8];      // mode 2, by p-1: run-test shifts (a, b, c), nibble-mask column address
+  __shared__ uint4 ptab[8];      // mode 2, by p-1: run-test shifts (a, b, c), p-bit mask
   if (NIB && threadIdx.x < 8) {
     const int p = threadIdx.x + 1;
     const uint32_t sa = p >= 2 ? 1u : 0u;
     const uint32_t sb = p >= 4 ? 2u : (p == 3 ? 1u : 0u);
     const uint32_t sc = p >= 5 ? (uint32_t)(p - 4) : 0u;
-    ptab[threadIdx.x] = make_uint4(sa, sb, sc, smem_u32(nmask) + (uint32_t)(8 * (p - 1)));
+    ptab[threadIdx.x] = make_uint4(sa, sb, sc, (1u << p) - 1u);
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
@@ -459,7 +440,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   L.MW = NIB ? (GO + 2) / 3 : (GO + 1) >> 1;
   constexpr uint32_t TM = NIB ? 0x3FFu : 0xFFFFu;   // time field mask
   L.hcap = a.h_cap;
-  L.LW = NIB ? a.h_cap >> 3 : a.h_cap >> 2;
+  // mode 2: per 32-tick word w, five words at LB + 5w: the four bit planes of
+  // the headroom Q_max - Q_t and the blocked bits (headroom == 0); two
+  // sentinel tick-words past the horizon are free
+  L.LW = NIB ? 5 * ((a.h_cap >> 5) + 2) : a.h_cap >> 2;
   L.BW = a.h_cap >> 5;
   const int LB = L.RW + L.MW, BB = LB + L.LW;
   const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
@@ -484,11 +468,14 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     for (int w = 0; w < L.RW; ++w) sts(waddr(L, w), r16[w]);
     for (int w = 0; w < L.MW; ++w) sts(waddr(L, L.RW + w), m16[w]);
     if (NIB) {
-      const uint32_t *hn0 = (const uint32_t *)(smem + h.off_hn0);
-      const uint32_t *bn0 = (const uint32_t *)(smem + h.off_bn0);
-      const uint32_t full = (uint32_t)h.q_max * 0x11111111u;
-      for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), w < h.hn_words0 ? hn0[w] : full);
-      for (int w = 0; w < BW; ++w) sts(waddr(L, BB + w), w < h.bn_words0 ? bn0[w] : 0u);
+      const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
+      const uint32_t qm = (uint32_t)h.q_max;
+      for (int w = 0; w < L.LW; w += 5)
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+          const uint32_t v = w < h.hn_words0 ? pl0[w + b] : (b < 4 && ((qm >> b) & 1u) ? 0xFFFFFFFFu : 0u);
+          sts(waddr(L, LB + w + b), v);
+        }
     } else {
       for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
       for (int w = 0; w < BW; ++w) {
@@ -497,8 +484,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         sts(waddr(L, BB + w), bits);
       }
     }
-    sts(waddr(L, BB + BW), 0u);
-    sts(waddr(L, BB + BW + 1), 0u);
+    if (!NIB) {
+      sts(waddr(L, BB + BW), 0u);
+      sts(waddr(L, BB + BW + 1), 0u);
+    }
     int32_t *srow = nullptr;
     if (SCHED && active) {
       srow = a.start_out + gc * h.cells;
@@ -528,8 +517,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
           const int t0 = max((int)(field_at<NIB>(rw, A.rsh) & TM), (int)(field_at<NIB>(mw, A.msh) & TM));
           // C: first run of p un-blocked ticks in the 32-tick window at t0
           //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
-          const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
-          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), A);
+          constexpr uint32_t BST = NIB ? 5 * 128 : 128;     // bytes between consecutive blocked words
+          const uint32_t bwa = NIB ? waddr(L, LB + 5 * min(t0 >> 5, BW) + 4) : waddr(L, BB + min(t0 >> 5, BW));
+          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + BST), t0 & 31), A);
           int S;
           if (UQ) {
             // window miss: slide by 33 - p ticks (a run starting in the last
@@ -538,8 +528,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             int t = t0;
             while (f == 0u) {
               t += 33 - A.p;
-              const uint32_t bwb = waddr(L, BB + min(t >> 5, BW));
-              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31), A);
+              const uint32_t bwb = NIB ? waddr(L, LB + 5 * min(t >> 5, BW) + 4) : waddr(L, BB + min(t >> 5, BW));
+              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + BST), t & 31), A);
             }
             S = t + __ffs(f) - 1;
           } else {
@@ -555,25 +545,45 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             sts(A.ra, (rw & ~place_at<NIB>(TM, A.rsh)) | place_at<NIB>((uint32_t)C, A.rsh));
             sts(A.ma, (mw & ~place_at<NIB>(TM, A.msh)) | place_at<NIB>((uint32_t)C, A.msh));
             if (NIB) {
-              // D: headroom -= 1 on [S, C) (<= 2 words, p <= 8); newly
-              // exhausted ticks become blocked
-              const int w0 = S >> 3;
-              uint2 nm;
-              asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
-                           : "=r"(nm.x), "=r"(nm.y)
-                           : "r"(A.nmo + ((uint32_t)(S & 7) << 6)));
-              const uint32_t a0 = waddr(L, LB + w0);
-              const uint32_t ba = waddr(L, BB + (w0 >> 2));
-              const uint32_t B0 = lds(ba);
-              const uint32_t v0 = lds(a0) - nm.x;
-              const uint32_t v1 = lds(a0 + 128) - nm.y;
-              sts(a0, v0);
-              sts(a0 + 128, v1);
-              const uint32_t b16 = pack8(zero_nibbles(v0)) | (pack8(zero_nibbles(v1)) << 8);
-              const int sh = (w0 & 3) << 3;
-              sts(ba, B0 | (b16 << sh));
-              const uint32_t spill = sh > 16 ? b16 >> (32 - sh) : 0u;
-              if ((w0 >> 2) + 1 < BW) sts(ba + 128, lds(ba + 128) | spill);
+              // D: headroom -= 1 on [S, C): borrow chain through the four
+              // bit planes under the p-bit mask (a second tick-word only when
+              // the interval crosses a 32-tick boundary); blocked = headroom 0
+              const int sh = S & 31;
+              const uint32_t a0 = waddr(L, LB + 5 * (S >> 5));
+              uint32_t bm = A.nmo << sh;
+              const uint32_t bhi = __funnelshift_l(A.nmo, 0u, (uint32_t)sh);
+              {
+                const uint32_t h0 = lds(a0), h1 = lds(a0 + 128), h2 = lds(a0 + 256), h3 = lds(a0 + 384);
+                const uint32_t n0 = h0 ^ bm;
+                bm &= ~h0;
+                const uint32_t n1 = h1 ^ bm;
+                bm &= ~h1;
+                const uint32_t n2 = h2 ^ bm;
+                bm &= ~h2;
+                const uint32_t n3 = h3 ^ bm;
+                sts(a0, n0);
+                sts(a0 + 128, n1);
+                sts(a0 + 256, n2);
+                sts(a0 + 384, n3);
+                sts(a0 + 512, ~(n0 | n1 | n2 | n3));
+              }
+              if (bhi) {
+                uint32_t b2 = bhi;
+                const uint32_t a1 = a0 + 640;
+                const uint32_t h0 = lds(a1), h1 = lds(a1 + 128), h2 = lds(a1 + 256), h3 = lds(a1 + 384);
+                const uint32_t n0 = h0 ^ b2;
+                b2 &= ~h0;
+                const uint32_t n1 = h1 ^ b2;
+                b2 &= ~h1;
+                const uint32_t n2 = h2 ^ b2;
+                b2 &= ~h2;
+                const uint32_t n3 = h3 ^ b2;
+                sts(a1, n0);
+                sts(a1 + 128, n1);
+                sts(a1 + 256, n2);
+                sts(a1 + 384, n3);
+                sts(a1 + 512, ~(n0 | n1 | n2 | n3));
+              }
               if (SCHED) srow[A.e / h.O] = S + h.rs;
               continue;
             }

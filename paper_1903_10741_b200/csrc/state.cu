@@ -145,8 +145,10 @@ ffs_status State::build_image() {
   const int lmode = (uq && qmin == 1 && in.q_max <= 15 && NJ <= 6144 && G * O <= 768) ? 2 : (uq ? 1 : 0);
   // lane-decode prefix (staged by the lane kernels), then warp-path tables
   H.lane_mode = lmode;
-  H.hn_words0 = (int32_t)((Lr + 7) / 8);
-  H.bn_words0 = (int32_t)((Lr + 31) / 32);
+  // mode 2: 5 words (4 headroom bit planes + blocked bits) per 32 ticks;
+  // modes 0/1 take the byte profile lvl0 instead
+  H.hn_words0 = lmode == 2 ? (int32_t)(5 * ((Lr + 31) / 32)) : 0;
+  H.bn_words0 = 0;
   H.off_hn0 = off; off += r16((uint64_t)H.hn_words0 * 4);
   H.off_bn0 = off; off += r16((uint64_t)H.bn_words0 * 4);
   H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
@@ -187,15 +189,16 @@ ffs_status State::build_image() {
     else ((uint16_t *)(img + H.off_lvl0))[t] = (uint16_t)L;
   }
   {
-    uint32_t *hn = (uint32_t *)(img + H.off_hn0);
-    uint32_t *bn = (uint32_t *)(img + H.off_bn0);
-    for (int64_t t = 0; t < (int64_t)H.hn_words0 * 8; ++t) {
+    uint32_t *pl = (uint32_t *)(img + H.off_hn0);
+    for (int64_t t = 0; t < (int64_t)(H.hn_words0 / 5) * 32; ++t) {
       int64_t L = 0;
       for (auto &rq : running)
         if (rq.a <= t && t < rq.c) L += rq.q;
       const int64_t hr = std::max<int64_t>(0, in.q_max - L);
-      hn[t >> 3] |= (uint32_t)(hr & 0xF) << ((t & 7) * 4);
-      if (hr == 0 && (t >> 5) < H.bn_words0) bn[t >> 5] |= 1u << (t & 31);
+      uint32_t *w = pl + 5 * (t >> 5);
+      for (int b = 0; b < 4; ++b)
+        if ((hr >> b) & 1) w[b] |= 1u << (t & 31);
+      if (hr == 0) w[4] |= 1u << (t & 31);
     }
   }
   if (!pjob.empty()) {
@@ -266,15 +269,16 @@ ffs_status State::build_image() {
   if (lane_ok) {
     const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 3072;   // static smem: mask tables + mbarrier
     const int64_t fixed_words = lmode == 2 ? (NJ + 2) / 3 + (G * O + 2) / 3 : (NJ + 1) / 2 + (G * O + 1) / 2;
-    auto words = [&](int64_t hc) {   // + 2 sentinel words of `blocked`
-      return fixed_words + (lmode == 2 ? hc / 8 : hc / 4) + hc / 32 + 2;
+    auto words = [&](int64_t hc) {   // + 2 sentinel words / tick-words of `blocked`
+      return lmode == 2 ? fixed_words + 5 * (hc / 32 + 2) : fixed_words + hc / 4 + hc / 32 + 2;
     };
     // horizon: the proven bound if it fits, else as large as keeps >= 8
     // warps (overflowing chromosomes are re-decoded exactly by the fallback)
     int64_t hc = h_bound;
     const int target_warps = lmode == 2 ? 14 : 8;
     if (words(hc) * 128 * target_warps > lbudget)
-      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - 2) * 32 / (lmode == 2 ? 5 : 9) / 32 * 32);
+      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - (lmode == 2 ? 10 : 2)) * 32 /
+                                      (lmode == 2 ? 5 : 9) / 32 * 32);
     if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
     hc = std::min<int64_t>(hc, lmode == 2 ? 992 : 65504);   // 10-bit times in mode 2
     int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
