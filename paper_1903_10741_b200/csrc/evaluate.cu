@@ -142,8 +142,9 @@ __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
   const int K = h.K;
   for (int64_t i = gw; i < count; i += nw) {
     const int64_t c = FALLBACK ? (int64_t)a.ovf[1 + i] : i;
-    const int8_t *xr = a.x + c * K;
-    const int16_t *yr = a.y + c * K;
+    const int64_t row = a.row > 0 ? a.row : K;
+    const int8_t *xr = a.x + c * row;
+    const int16_t *yr = a.y + c * row;
     int32_t *srow = SCHED ? a.start_out + c * h.cells : nullptr;
     if (SCHED)
       for (int k = lane; k < h.cells; k += 32) srow[k] = a.fstart[k];

@@ -177,6 +177,7 @@ struct EvalArgs {
   int32_t per_warp_bytes;
   const uint16_t *ordg;          // lane path
   int64_t first;                 // lane path: first chromosome of this chunk
+  int64_t row;                   // genes between consecutive chromosomes of x / y (0: K)
 };
 
 ffs_status launch_lane(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s, int *launches);

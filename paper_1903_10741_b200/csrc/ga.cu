@@ -1,9 +1,11 @@
 // ga.cu -- island GA of one rescheduling point on sm_100a.
 //
 // Population: global island I owns cells I*tile + i (i row-major in the
-// island tile, tile = island_w * island_h); SoA device buffers x int8[cell][K],
-// y int16[cell][K], obj/fit int64[cell], double-buffered across generations
-// (synchronous update from the previous generation's snapshot, R18).
+// island tile, tile = island_w * island_h); SoA device buffers x int8[cell][KP],
+// y int16[cell][KP] (rows padded to KP = K rounded up to 16 genes, so every
+// row is 16-B aligned and moves with 16-B vector accesses), obj/fit
+// int64[cell], double-buffered across generations (synchronous update from
+// the previous generation's snapshot, R18).
 // Per generation (operator order R20):
 //   generation_kernel  warp per horizontal pair: asteroid selection,
 //                      neighbouring paired crossover + correction,
@@ -29,6 +31,7 @@ struct Run {
   ffs_ga_config cfg{};
   cudaStream_t s = nullptr;
   int tile = 0, nisl = 0, K = 0, cells = 0;
+  int64_t row = 0;                  // KP: padded genes per population / history row
   int64_t nloc = 0;
   int gen = -1;
   int cur = 0;
@@ -67,7 +70,7 @@ namespace {
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
 // ---- initialisation: x ~ U{0..o-1}, y = 1 + rank of a random key
-__global__ void __launch_bounds__(256) init_kernel(int32_t K, int32_t O, int64_t count, int32_t tile,
+__global__ void __launch_bounds__(256) init_kernel(int32_t K, int64_t row, int32_t O, int64_t count, int32_t tile,
                                                    int32_t island0, uint64_t seed, int8_t *x, int16_t *y) {
   extern __shared__ __align__(16) uint32_t keys_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(256) init_kernel(int32_t K, int32_t O, int64_t
     for (int g = lane; g < K; g += 32) {
       u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
-      x[c * K + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
+      x[c * row + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
       keys[g] = word_of(ry, g & 3);
     }
     __syncwarp();
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(256) init_kernel(int32_t K, int32_t O, int64_t
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         int gg = g0 + lane + 32 * u;
-        if (gg < K) y[c * K + gg] = (int16_t)(rk[u] + 1);
+        if (gg < K) y[c * row + gg] = (int16_t)(rk[u] + 1);
       }
     }
     __syncwarp();
@@ -183,56 +186,61 @@ __device__ void island_best_worst(const int64_t *fit, int tile, int &best, int &
 __device__ __forceinline__ void copy_bytes(unsigned char *dst, const unsigned char *src, size_t n) {
   for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
+// a padded population / history row (x: row bytes, y: 2*row bytes; 16-B aligned)
+__device__ __forceinline__ void copy_row(int8_t *dx, int16_t *dy, const int8_t *sx, const int16_t *sy, int64_t row) {
+  const int nx = (int)(row >> 4), ny = (int)(row >> 3);
+  for (int i = threadIdx.x; i < nx + ny; i += blockDim.x) {
+    if (i < nx) ((uint4 *)dx)[i] = ((const uint4 *)sx)[i];
+    else ((uint4 *)dy)[i - nx] = ((const uint4 *)sy)[i - nx];
+  }
+}
 
 // history elite record per island; generation 0 sets it unconditionally
-__global__ void history_init_kernel(int K, int tile, const int8_t *x, const int16_t *y, const int64_t *obj,
+__global__ void history_init_kernel(int64_t row, int tile, const int8_t *x, const int16_t *y, const int64_t *obj,
                                     const int64_t *fit, int8_t *hx, int16_t *hy, int64_t *hobj, int64_t *hfit) {
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
   island_best_worst(fit + base, tile, b, w);
   const int64_t c = base + b;
-  copy_bytes((unsigned char *)(hx + (int64_t)li * K), (const unsigned char *)(x + c * K), (size_t)K);
-  copy_bytes((unsigned char *)(hy + (int64_t)li * K), (const unsigned char *)(y + c * K), (size_t)K * 2);
+  copy_row(hx + (int64_t)li * row, hy + (int64_t)li * row, x + c * row, y + c * row, row);
   if (threadIdx.x == 0) { hobj[li] = obj[c]; hfit[li] = fit[c]; }
 }
 
 // elitist replacement (R21): strict improvement updates the history;
 // the island's worst cell is overwritten by the history elite.
-__global__ void replace_kernel(int K, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
+__global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
                                int16_t *hy, int64_t *hobj, int64_t *hfit) {
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
   island_best_worst(fit + base, tile, b, w);
   const int64_t cb = base + b, cw = base + w;
-  int8_t *hxr = hx + (int64_t)li * K;
-  int16_t *hyr = hy + (int64_t)li * K;
+  int8_t *hxr = hx + (int64_t)li * row;
+  int16_t *hyr = hy + (int64_t)li * row;
   const bool upd = fit[cb] > hfit[li];
   __syncthreads();
   if (upd) {
-    copy_bytes((unsigned char *)hxr, (const unsigned char *)(x + cb * K), (size_t)K);
-    copy_bytes((unsigned char *)hyr, (const unsigned char *)(y + cb * K), (size_t)K * 2);
+    copy_row(hxr, hyr, x + cb * row, y + cb * row, row);
     if (threadIdx.x == 0) { hobj[li] = obj[cb]; hfit[li] = fit[cb]; }
   }
   __syncthreads();
-  copy_bytes((unsigned char *)(x + cw * K), (const unsigned char *)hxr, (size_t)K);
-  copy_bytes((unsigned char *)(y + cw * K), (const unsigned char *)hyr, (size_t)K * 2);
+  copy_row(x + cw * row, y + cw * row, hxr, hyr, row);
   if (threadIdx.x == 0) { obj[cw] = hobj[li]; fit[cw] = hfit[li]; }
 }
 
 // ring migration, part 1: snapshot every island's best (after replacement)
 // and remember its worst cell (R22)
-__global__ void donor_kernel(int K, int tile, size_t rec, const int8_t *x, const int16_t *y, const int64_t *obj,
-                             const int64_t *fit, unsigned char *donor, int32_t *worst_idx) {
+__global__ void donor_kernel(int K, int64_t row, int tile, size_t rec, const int8_t *x, const int16_t *y,
+                             const int64_t *obj, const int64_t *fit, unsigned char *donor, int32_t *worst_idx) {
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
   island_best_worst(fit + base, tile, b, w);
   const int64_t cb = base + b;
-  unsigned char *d = donor + (size_t)li * rec;
-  copy_bytes(d, (const unsigned char *)(x + cb * K), (size_t)K);
-  copy_bytes(d + K, (const unsigned char *)(y + cb * K), (size_t)K * 2);
+  unsigned char *d = donor + (size_t)li * rec;   // compact record: x[K] y[K] obj fit
+  copy_bytes(d, (const unsigned char *)(x + cb * row), (size_t)K);
+  copy_bytes(d + K, (const unsigned char *)(y + cb * row), (size_t)K * 2);
   if (threadIdx.x == 0) {
     int64_t o = obj[cb], f = fit[cb];
     memcpy(d + 3 * (size_t)K, &o, 8);
@@ -243,13 +251,14 @@ __global__ void donor_kernel(int K, int tile, size_t rec, const int8_t *x, const
 
 // part 2: island li's worst cell <- best of island li-1; island 0 of the shard
 // <- `incoming` (the last island of the previous shard, or of this shard)
-__global__ void import_kernel(int K, size_t rec, const unsigned char *donor, const unsigned char *incoming,
-                              const int32_t *worst_idx, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit) {
+__global__ void import_kernel(int K, int64_t row, size_t rec, const unsigned char *donor,
+                              const unsigned char *incoming, const int32_t *worst_idx, int8_t *x, int16_t *y,
+                              int64_t *obj, int64_t *fit) {
   const int li = blockIdx.x;
   const unsigned char *src = li == 0 ? incoming : donor + (size_t)(li - 1) * rec;
   const int64_t cw = worst_idx[li];
-  copy_bytes((unsigned char *)(x + cw * K), src, (size_t)K);
-  copy_bytes((unsigned char *)(y + cw * K), src + K, (size_t)K * 2);
+  copy_bytes((unsigned char *)(x + cw * row), src, (size_t)K);
+  copy_bytes((unsigned char *)(y + cw * row), src + K, (size_t)K * 2);
   if (threadIdx.x == 0) {
     int64_t o, f;
     memcpy(&o, src + 3 * (size_t)K, 8);
@@ -320,6 +329,7 @@ struct GenArgs {
   uint32_t xo_thr, mut_thr;
   uint64_t seed;
   int64_t npairs;
+  int64_t row;                                 // padded genes per row (multiple of 16)
   const int32_t *cut;                          // pending cells before row-major position p
   const int8_t *xp; const int16_t *yp; const int64_t *fp;   // previous generation
   int8_t *xn; int16_t *yn;                     // next generation
@@ -347,6 +357,40 @@ __device__ __forceinline__ void argmax5(int lane, int sub, const int64_t *fitI, 
   winner = __shfl_sync(FULL, nb, sub * 16);
 }
 
+// byte / half-word masks of the genes before the cut inside one 16-B word
+// (n = cut - first gene of the word)
+__device__ __forceinline__ uint32_t mask_x(int n, int k) {   // word k of 16 int8 genes
+  const int nb = min(max(n - 4 * k, 0), 4);
+  return nb == 4 ? 0xFFFFFFFFu : (1u << (8 * nb)) - 1u;
+}
+__device__ __forceinline__ uint32_t mask_y(int n, int k) {   // word k of 8 int16 genes
+  const int nb = min(max(n - 2 * k, 0), 2);
+  return nb == 2 ? 0xFFFFFFFFu : (nb == 1 ? 0xFFFFu : 0u);
+}
+__device__ __forceinline__ uint32_t wsel(uint4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ void wset(uint4 &v, int k, uint32_t w) {
+  if (k == 0) v.x = w; else if (k == 1) v.y = w; else if (k == 2) v.z = w; else v.w = w;
+}
+
+// a8 on 16 machines: x <- (x + 1 + floor(r (o-1) / 2^32)) mod o, one Philox
+// block per 4 genes (R15)
+__device__ __forceinline__ uint4 mutate16(uint4 v, int g0, uint32_t cell, uint32_t kg, uint32_t I, uint32_t k0,
+                                          uint32_t k1, int O, int o1) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)((g0 >> 2) + b), cell, kg, I, k0, k1);
+    uint32_t w = wsel(v, b), out = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int xv = (int)((w >> (8 * j)) & 0xFFu) + 1 + (int)bounded(word_of(r, j), (uint32_t)o1);
+      if (xv >= O) xv -= O;
+      out |= (uint32_t)xv << (8 * j);
+    }
+    wset(v, b, out);
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -359,6 +403,8 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int half = a.tile >> 1, wh = a.w >> 1;
+  const int64_t row = a.row;
+  const int nxv = (int)(row >> 4), nyv = (int)(row >> 3);   // 16-B words of a row
   for (int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; pi < a.npairs; pi += nw) {
     const int64_t li = pi / half;
     const int pr = (int)(pi % half);
@@ -369,10 +415,10 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
     int wa, wb;
     argmax5(lane, 0, a.fp + base, ca, a.w, a.h, wa);
     argmax5(lane, 1, a.fp + base, cb, a.w, a.h, wb);
-    const int8_t *XA = a.xp + (base + wa) * K, *XB = a.xp + (base + wb) * K;
-    const int16_t *YA = a.yp + (base + wa) * K, *YB = a.yp + (base + wb) * K;
-    int8_t *xa = a.xn + (base + ca) * K, *xb = a.xn + (base + cb) * K;
-    int16_t *ya = a.yn + (base + ca) * K, *yb = a.yn + (base + cb) * K;
+    const uint4 *XA = (const uint4 *)(a.xp + (base + wa) * row), *XB = (const uint4 *)(a.xp + (base + wb) * row);
+    const uint4 *YA = (const uint4 *)(a.yp + (base + wa) * row), *YB = (const uint4 *)(a.yp + (base + wb) * row);
+    uint4 *xa = (uint4 *)(a.xn + (base + ca) * row), *xb = (uint4 *)(a.xn + (base + cb) * row);
+    uint4 *ya = (uint4 *)(a.yn + (base + ca) * row), *yb = (uint4 *)(a.yn + (base + cb) * row);
     // a7: crossover fires with p_c; one row-major cut shared by X and Y (R13)
     u32x4 rxo = philox((RNG_XO << 24), (uint32_t)ca, kg, I, k0, k1);
     int kc = K;
@@ -391,10 +437,18 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
       // in A's prefix; assigned in ascending order to duplicates in gene order.
       for (int i = lane; i < nwd; i += 32) { PA[i] = 0u; PB[i] = 0u; }
       __syncwarp();
-      for (int g = lane; g < kc; g += 32) {
-        int va = YA[g] - 1, vb = YB[g] - 1;
-        if ((unsigned)va < (unsigned)K) atomicOr(&PA[va >> 5], 1u << (va & 31));
-        if ((unsigned)vb < (unsigned)K) atomicOr(&PB[vb >> 5], 1u << (vb & 31));
+      for (int i = lane; i < ((kc + 7) >> 3); i += 32) {
+        const uint4 va = YA[i], vb = YB[i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (8 * i + j < kc) {
+            const int sh = 16 * (j & 1);
+            const int ta = (int)((wsel(va, j >> 1) >> sh) & 0xFFFFu) - 1;
+            const int tb = (int)((wsel(vb, j >> 1) >> sh) & 0xFFFFu) - 1;
+            if ((unsigned)ta < (unsigned)K) atomicOr(&PA[ta >> 5], 1u << (ta & 31));
+            if ((unsigned)tb < (unsigned)K) atomicOr(&PB[tb >> 5], 1u << (tb & 31));
+          }
+        }
       }
       __syncwarp();
       int offa = 0, offb = 0;
@@ -403,64 +457,94 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
         uint32_t wa_ = i < nwd ? (PB[i] & ~PA[i]) : 0u;
         uint32_t wb_ = i < nwd ? (PA[i] & ~PB[i]) : 0u;
         int na = __popc(wa_), nb = __popc(wb_);
-        int ia = na, ib = nb;
+        int ia = na | (nb << 16);
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          int t1 = __shfl_up_sync(FULL, ia, d), t2 = __shfl_up_sync(FULL, ib, d);
-          if (lane >= d) { ia += t1; ib += t2; }
+          int t1 = __shfl_up_sync(FULL, ia, d);
+          if (lane >= d) ia += t1;
         }
-        int pa = offa + ia - na, pb = offb + ib - nb;
+        int pa = offa + (ia & 0xFFFF) - na, pb = offb + (ia >> 16) - nb;
         while (wa_) { int bit = __ffs(wa_) - 1; wa_ &= wa_ - 1; LA[pa++] = (uint16_t)(i * 32 + bit + 1); }
         while (wb_) { int bit = __ffs(wb_) - 1; wb_ &= wb_ - 1; LB[pb++] = (uint16_t)(i * 32 + bit + 1); }
-        offa += __shfl_sync(FULL, ia, 31);
-        offb += __shfl_sync(FULL, ib, 31);
+        const int tot = __shfl_sync(FULL, ia, 31);
+        offa += tot & 0xFFFF;
+        offb += tot >> 16;
       }
       __syncwarp();
     }
-    // write children: prefix from own parent, suffix from the other (corrected)
-    int da = 0, db = 0;  // duplicates seen so far (gene order)
+    // children X, 16 genes per lane-word: prefix from own parent, suffix from
+    // the other; a8 resamples every machine of a mutated child
     const int o1 = a.O - 1;
-    for (int g0 = 0; g0 < K; g0 += 32) {
-      int g = g0 + lane;
-      bool v = g < K;
-      bool pre = g < kc;
-      int xav = 0, xbv = 0, yav = 0, ybv = 0;
-      bool dupa = false, dupb = false;
-      if (v) {
-        xav = pre ? XA[g] : XB[g];
-        xbv = pre ? XB[g] : XA[g];
-        yav = pre ? YA[g] : YB[g];
-        ybv = pre ? YB[g] : YA[g];
-        if (repair && !pre) {
-          int ta = yav - 1, tb = ybv - 1;
-          dupa = (unsigned)ta < (unsigned)K && ((PA[ta >> 5] >> (ta & 31)) & 1u);
-          dupb = (unsigned)tb < (unsigned)K && ((PB[tb >> 5] >> (tb & 31)) & 1u);
+    for (int i = lane; i < nxv; i += 32) {
+      const uint4 va = XA[i], vb = XB[i];
+      uint4 za, zb;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t m = mask_x(kc - 16 * i, k), wa_ = wsel(va, k), wb_ = wsel(vb, k);
+        wset(za, k, (wa_ & m) | (wb_ & ~m));
+        wset(zb, k, (wb_ & m) | (wa_ & ~m));
+      }
+      if (ma && o1 >= 1) za = mutate16(za, 16 * i, (uint32_t)ca, kg, I, k0, k1, a.O, o1);
+      if (mb && o1 >= 1) zb = mutate16(zb, 16 * i, (uint32_t)cb, kg, I, k0, k1, a.O, o1);
+      xa[i] = za;
+      xb[i] = zb;
+    }
+    // children Y, 8 genes per lane-word; suffix duplicates take the missing
+    // values in gene order (lane order inside a step, steps ascending)
+    int da = 0, db = 0;
+    for (int i0 = 0; i0 < nyv; i0 += 32) {
+      const int i = i0 + lane;
+      uint4 va = make_uint4(0, 0, 0, 0), vb = va;
+      if (i < nyv) { va = YA[i]; vb = YB[i]; }
+      uint4 za, zb;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t m = mask_y(kc - 8 * i, k), wa_ = wsel(va, k), wb_ = wsel(vb, k);
+        wset(za, k, (wa_ & m) | (wb_ & ~m));
+        wset(zb, k, (wb_ & m) | (wa_ & ~m));
+      }
+      if (repair) {
+        uint32_t fa = 0, fb = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int g = 8 * i + j;
+          if (g >= kc && g < K) {
+            const int sh = 16 * (j & 1);
+            const int ta = (int)((wsel(za, j >> 1) >> sh) & 0xFFFFu) - 1;
+            const int tb = (int)((wsel(zb, j >> 1) >> sh) & 0xFFFFu) - 1;
+            if ((unsigned)ta < (unsigned)K && ((PA[ta >> 5] >> (ta & 31)) & 1u)) fa |= 1u << j;
+            if ((unsigned)tb < (unsigned)K && ((PB[tb >> 5] >> (tb & 31)) & 1u)) fb |= 1u << j;
+          }
+        }
+        const int na = __popc(fa), nb = __popc(fb);
+        int ia = na | (nb << 16);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int t1 = __shfl_up_sync(FULL, ia, d);
+          if (lane >= d) ia += t1;
+        }
+        int ra = da + (ia & 0xFFFF) - na, rb = db + (ia >> 16) - nb;
+        const int tot = __shfl_sync(FULL, ia, 31);
+        da += tot & 0xFFFF;
+        db += tot >> 16;
+        while (fa) {
+          const int j = __ffs(fa) - 1;
+          fa &= fa - 1;
+          const int sh = 16 * (j & 1);
+          const uint32_t w = wsel(za, j >> 1);
+          wset(za, j >> 1, (w & ~(0xFFFFu << sh)) | ((uint32_t)LA[ra++] << sh));
+        }
+        while (fb) {
+          const int j = __ffs(fb) - 1;
+          fb &= fb - 1;
+          const int sh = 16 * (j & 1);
+          const uint32_t w = wsel(zb, j >> 1);
+          wset(zb, j >> 1, (w & ~(0xFFFFu << sh)) | ((uint32_t)LB[rb++] << sh));
         }
       }
-      uint32_t ba = __ballot_sync(FULL, dupa), bb = __ballot_sync(FULL, dupb);
-      uint32_t lt = (1u << lane) - 1u;
-      if (dupa) yav = LA[da + __popc(ba & lt)];
-      if (dupb) ybv = LB[db + __popc(bb & lt)];
-      da += __popc(ba);
-      db += __popc(bb);
-      if (v) {
-        // a8: every gene's machine resampled among the other o-1 (R15)
-        if ((ma || mb) && o1 >= 1) {
-          if (ma) {
-            u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)ca, kg, I, k0, k1);
-            xav += 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1);   // < 2o: one conditional subtract
-            if (xav >= a.O) xav -= a.O;
-          }
-          if (mb) {
-            u32x4 r = philox((RNG_MUT_X << 24) | (uint32_t)(g >> 2), (uint32_t)cb, kg, I, k0, k1);
-            xbv += 1 + (int)bounded(word_of(r, g & 3), (uint32_t)o1);
-            if (xbv >= a.O) xbv -= a.O;
-          }
-        }
-        xa[g] = (int8_t)xav;
-        xb[g] = (int8_t)xbv;
-        ya[g] = (int16_t)yav;
-        yb[g] = (int16_t)ybv;
+      if (i < nyv) {
+        ya[i] = za;
+        yb[i] = zb;
       }
     }
     __syncwarp();
@@ -468,7 +552,7 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
     if (K >= 2 && lane < 2) {
       const u32x4 &rm = lane == 0 ? rma : rmb;
       const bool fire = lane == 0 ? ma : mb;
-      int16_t *yy = lane == 0 ? ya : yb;
+      int16_t *yy = (int16_t *)(lane == 0 ? ya : yb);
       if (fire) {
         int g1 = (int)bounded(rm.y, (uint32_t)K);
         int g2 = (int)bounded(rm.z, (uint32_t)(K - 1));
@@ -499,6 +583,7 @@ static ffs_status evaluate_population(Run &r, int buf, bool with_fitness) {
   a.x = r.x[buf];
   a.y = r.y[buf];
   a.obj = r.obj[buf];
+  a.row = r.row;
   a.fstart = r.st->fstart_dev;
   if (with_fitness) {
     a.emax = r.scal;
@@ -515,7 +600,7 @@ static ffs_status ga_init(Run &r) {
   if (smem > (size_t)kSmemLimit) return fail(FFS_ERR_INVALID_ARG, "K too large for initialisation");
   FFS_CUDA(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = std::min<int64_t>((r.nloc + warps - 1) / warps, (int64_t)st.num_sms * 8);
-  init_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(r.K, st.inst->o, r.nloc, r.tile, r.cfg.island_begin,
+  init_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(r.K, r.row, st.inst->o, r.nloc, r.tile, r.cfg.island_begin,
                                                          r.cfg.seed, r.x[0], r.y[0]);
   FFS_CUDA(cudaGetLastError());
   r.launches++;
@@ -532,8 +617,8 @@ static ffs_status ga_init(Run &r) {
   emax_fitness_kernel<<<(unsigned)std::min<int64_t>((r.nloc + 255) / 256, 1024), 256, 0, r.s>>>(
       r.scal, r.obj[0], r.fit[0], r.nloc, st.real_wt);
   FFS_CUDA(cudaGetLastError());
-  history_init_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.x[0], r.y[0], r.obj[0], r.fit[0], r.hx, r.hy, r.hobj,
-                                               r.hfit);
+  history_init_kernel<<<r.nisl, 256, 0, r.s>>>(r.row, r.tile, r.x[0], r.y[0], r.obj[0], r.fit[0], r.hx, r.hy,
+                                               r.hobj, r.hfit);
   FFS_CUDA(cudaGetLastError());
   trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.tmin, r.tsum, 0, st.real_wt);
   FFS_CUDA(cudaGetLastError());
@@ -553,6 +638,7 @@ static ffs_status ga_generation(Run &r) {
   g.xo_thr = r.cfg.xo_threshold; g.mut_thr = r.cfg.mut_threshold; g.seed = r.cfg.seed;
   g.npairs = r.nloc / 2;
   g.cut = st.cut_dev;
+  g.row = r.row;
   g.xp = r.x[r.cur]; g.yp = r.y[r.cur]; g.fp = r.fit[r.cur];
   g.xn = r.x[nb]; g.yn = r.y[nb];
   const int warps = 8;
@@ -568,13 +654,13 @@ static ffs_status ga_generation(Run &r) {
   r.launches++;
   ffs_status e = evaluate_population(r, nb, true);
   if (e != FFS_OK) return e;
-  replace_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.hx, r.hy, r.hobj,
-                                          r.hfit);
+  replace_kernel<<<r.nisl, 256, 0, r.s>>>(r.row, r.tile, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.hx, r.hy,
+                                          r.hobj, r.hfit);
   FFS_CUDA(cudaGetLastError());
   r.launches++;
   if (k % r.cfg.migration_interval == 0 && r.cfg.islands_total >= 2) {
-    donor_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.tile, r.rec, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.donor,
-                                          r.worst_idx);
+    donor_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb],
+                                          r.donor, r.worst_idx);
     FFS_CUDA(cudaGetLastError());
     r.launches++;
     const unsigned char *incoming = r.donor + (size_t)(r.nisl - 1) * r.rec;
@@ -584,8 +670,8 @@ static ffs_status ga_generation(Run &r) {
         return fail(FFS_ERR_COMM, "allgather hook failed");
       incoming = r.recv + (size_t)((r.cfg.rank + r.cfg.world - 1) % r.cfg.world) * r.rec;
     }
-    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.rec, r.donor, incoming, r.worst_idx, r.x[nb], r.y[nb], r.obj[nb],
-                                           r.fit[nb]);
+    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.rec, r.donor, incoming, r.worst_idx, r.x[nb], r.y[nb],
+                                           r.obj[nb], r.fit[nb]);
     FFS_CUDA(cudaGetLastError());
     r.launches++;
   }
@@ -628,7 +714,8 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
   r.K = st.K;
   r.cells = st.cells;
   r.rec = ((size_t)3 * r.K + 16 + 15) & ~(size_t)15;
-  const size_t genes = (size_t)r.nloc * std::max(r.K, 1);
+  r.row = ((int64_t)std::max(r.K, 1) + 15) & ~(int64_t)15;
+  const size_t genes = (size_t)r.nloc * r.row;
   ffs_status e = FFS_OK;
   for (int b = 0; b < 2 && e == FFS_OK; ++b) {
     if (e == FFS_OK) e = r.alloc(&r.x[b], genes);
@@ -636,8 +723,14 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
     if (e == FFS_OK) e = r.alloc(&r.obj[b], (size_t)r.nloc);
     if (e == FFS_OK) e = r.alloc(&r.fit[b], (size_t)r.nloc);
   }
-  if (e == FFS_OK) e = r.alloc(&r.hx, (size_t)r.nisl * std::max(r.K, 1));
-  if (e == FFS_OK) e = r.alloc(&r.hy, (size_t)r.nisl * std::max(r.K, 1));
+  if (e == FFS_OK) e = r.alloc(&r.hx, (size_t)r.nisl * r.row);
+  if (e == FFS_OK) e = r.alloc(&r.hy, (size_t)r.nisl * r.row);
+  // padding genes are never read as genes; zero them once for determinism
+  for (int b = 0; b < 2 && e == FFS_OK; ++b) {
+    cudaError_t ce = cudaMemsetAsync(r.x[b], 0, genes, r.s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(r.y[b], 0, genes * 2, r.s);
+    if (ce != cudaSuccess) e = cuda_fail(ce, "population memset");
+  }
   if (e == FFS_OK) e = r.alloc(&r.hobj, (size_t)r.nisl);
   if (e == FFS_OK) e = r.alloc(&r.hfit, (size_t)r.nisl);
   if (e == FFS_OK) e = r.alloc(&r.worst_idx, (size_t)r.nisl);
@@ -702,8 +795,8 @@ ffs_status ffs_best(ffs_run *h, int8_t *x, int16_t *y, int32_t *assign, int32_t 
     int b = 0;
     for (int i = 1; i < r.nisl; ++i)
       if (hf[i] > hf[b]) b = i;  // ties -> lowest island
-    FFS_CUDA(cudaMemcpy(bx.data(), r.hx + (size_t)b * K, (size_t)K, cudaMemcpyDeviceToHost));
-    FFS_CUDA(cudaMemcpy(by.data(), r.hy + (size_t)b * K, (size_t)K * 2, cudaMemcpyDeviceToHost));
+    FFS_CUDA(cudaMemcpy(bx.data(), r.hx + (size_t)b * r.row, (size_t)K, cudaMemcpyDeviceToHost));
+    FFS_CUDA(cudaMemcpy(by.data(), r.hy + (size_t)b * r.row, (size_t)K * 2, cudaMemcpyDeviceToHost));
   }
   // decode the elite once more to emit its schedule
   int8_t *dx = nullptr;
@@ -763,9 +856,10 @@ ffs_status ffs_run_population(ffs_run *h, int8_t *x, int16_t *y, int64_t *object
   cudaSetDevice(r.st->inst->dev);
   FFS_CUDA(cudaStreamSynchronize(r.s));
   if (r.K == 0) return FFS_OK;
-  const size_t genes = (size_t)r.nloc * r.K;
-  if (x) FFS_CUDA(cudaMemcpy(x, r.x[r.cur], genes, cudaMemcpyDeviceToHost));
-  if (y) FFS_CUDA(cudaMemcpy(y, r.y[r.cur], genes * 2, cudaMemcpyDeviceToHost));
+  if (x) FFS_CUDA(cudaMemcpy2D(x, (size_t)r.K, r.x[r.cur], (size_t)r.row, (size_t)r.K, (size_t)r.nloc,
+                               cudaMemcpyDeviceToHost));
+  if (y) FFS_CUDA(cudaMemcpy2D(y, (size_t)r.K * 2, r.y[r.cur], (size_t)r.row * 2, (size_t)r.K * 2, (size_t)r.nloc,
+                               cudaMemcpyDeviceToHost));
   if (objective) FFS_CUDA(cudaMemcpy(objective, r.obj[r.cur], (size_t)r.nloc * 8, cudaMemcpyDeviceToHost));
   if (fitness) FFS_CUDA(cudaMemcpy(fitness, r.fit[r.cur], (size_t)r.nloc * 8, cudaMemcpyDeviceToHost));
   return FFS_OK;
@@ -777,8 +871,10 @@ ffs_status ffs_run_history(ffs_run *h, int8_t *x, int16_t *y, int64_t *objective
   cudaSetDevice(r.st->inst->dev);
   FFS_CUDA(cudaStreamSynchronize(r.s));
   if (r.K == 0) return FFS_OK;
-  if (x) FFS_CUDA(cudaMemcpy(x, r.hx, (size_t)r.nisl * r.K, cudaMemcpyDeviceToHost));
-  if (y) FFS_CUDA(cudaMemcpy(y, r.hy, (size_t)r.nisl * r.K * 2, cudaMemcpyDeviceToHost));
+  if (x) FFS_CUDA(cudaMemcpy2D(x, (size_t)r.K, r.hx, (size_t)r.row, (size_t)r.K, (size_t)r.nisl,
+                               cudaMemcpyDeviceToHost));
+  if (y) FFS_CUDA(cudaMemcpy2D(y, (size_t)r.K * 2, r.hy, (size_t)r.row * 2, (size_t)r.K * 2, (size_t)r.nisl,
+                               cudaMemcpyDeviceToHost));
   if (objective) FFS_CUDA(cudaMemcpy(objective, r.hobj, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
   if (fitness) FFS_CUDA(cudaMemcpy(fitness, r.hfit, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
   return FFS_OK;

@@ -83,6 +83,8 @@ struct OrdArgs {
   const int8_t *x;
   const int16_t *y;
   int64_t first, count;
+  int64_t row;             // genes between chromosomes (>= K)
+  int32_t vec;             // row % 4 == 0 and 16-B aligned bases: 4-gene vector loads
   int32_t K;
   const uint32_t *head;    // [ceil(K/32)] bit g: first pending gene of its job
   const uint32_t *gbase;   // [K] (j*G + s)*O
@@ -120,10 +122,19 @@ __device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, i
   }
 }
 
+template <bool VEC>
 __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *head, int K, int g0, int y[4],
                                           uint32_t &h) {
+  if (VEC) {   // the row's genes g0..g0+3 are one aligned 8-byte word (padding genes past K are masked)
+    const uint2 w = g0 < K ? __ldg((const uint2 *)(yr + g0)) : make_uint2(0, 0);
+    const int v[4] = {(int)(int16_t)(w.x & 0xFFFFu), (int)(int16_t)(w.x >> 16), (int)(int16_t)(w.y & 0xFFFFu),
+                      (int)(int16_t)(w.y >> 16)};
 #pragma unroll
-  for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? (int)__ldg(yr + g0 + k) : INT_MAX;
+    for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? v[k] : INT_MAX;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? (int)__ldg(yr + g0 + k) : INT_MAX;
+  }
   const uint32_t hw = g0 < K ? head[g0 >> 5] : 0u;
   h = (hw >> (g0 & 31)) & 0xFu;
   // genes past the end are their own segments (never merge into valid ones)
@@ -131,13 +142,19 @@ __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *hea
   if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
 }
 
+template <bool VEC>
 __device__ __forceinline__ void load_xquad(const int8_t *xr, int K, int g0, uint32_t &xw) {
+  if (VEC) {
+    xw = g0 < K ? __ldg((const uint32_t *)(xr + g0)) : 0u;
+    return;
+  }
   xw = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (g0 + k < K) xw |= (uint32_t)(uint8_t)__ldg(xr + g0 + k) << (8 * k);
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
@@ -161,8 +178,8 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     const int64_t c = tile * 32 + warp;
     if (c < a.count) {
-      const int16_t *yr = a.y + (a.first + c) * K;
-      const int8_t *xr = a.x + (a.first + c) * K;
+      const int16_t *yr = a.y + (a.first + c) * a.row;
+      const int8_t *xr = a.x + (a.first + c) * a.row;
       // hist/start are indexed by u = K - pm (descending prefix minimum), with
       // a dummy slot u = K for genes past the end (no branches around atomics)
       for (int i = lane; i < ((K + 2 + 127) >> 7) << 6; i += 32) hist[i] = 0u;
@@ -172,8 +189,8 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       // software pipeline: tile t+1's genes are loaded while tile t is scanned
       int yq[4];
       uint32_t hq, xq;
-      load_quad(yr, headS, K, 4 * lane, yq, hq);
-      load_xquad(xr, K, 4 * lane, xq);
+      load_quad<VEC>(yr, headS, K, 4 * lane, yq, hq);
+      load_xquad<VEC>(xr, K, 4 * lane, xq);
       for (int t = 0; t < NT; ++t) {
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
@@ -182,8 +199,8 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         for (int k = 0; k < 4; ++k) y[k] = yq[k];
         *(uint32_t *)(xs + g0) = xq;
         if (t + 1 < NT) {
-          load_quad(yr, headS, K, g0 + 128, yq, hq);
-          load_xquad(xr, K, g0 + 128, xq);
+          load_quad<VEC>(yr, headS, K, g0 + 128, yq, hq);
+          load_xquad<VEC>(xr, K, g0 + 128, xq);
         }
         pm_quad(y, h, carry, lane, pm);
         uint32_t pk[4];
@@ -665,8 +682,9 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     FFS_CUDA(cudaMalloc(&scr.ordg, (size_t)elems * 2));
     scr.ordg_elems = elems;
   }
-  static size_t a_ord = 0;
-  ffs_status e = smem_attr(order_warp_kernel, st.ord_smem, a_ord);
+  static size_t a_ord = 0, a_ord_v = 0;
+  ffs_status e = smem_attr(order_warp_kernel<false>, st.ord_smem, a_ord);
+  if (e == FFS_OK) e = smem_attr(order_warp_kernel<true>, st.ord_smem, a_ord_v);
   if (e != FFS_OK) return e;
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
@@ -690,6 +708,8 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.y = a0.y;
     oa.first = first;
     oa.count = a.count;
+    oa.row = a0.row > 0 ? a0.row : K;
+    oa.vec = (oa.row % 4 == 0) && ((uintptr_t)a0.x % 16 == 0) && ((uintptr_t)a0.y % 16 == 0);
     oa.K = K;
     oa.head = (const uint32_t *)((const unsigned char *)st.image_dev +
                                  ((const ImageHdr *)st.image_host.data())->off_head);
@@ -699,7 +719,10 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
-    order_warp_kernel<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
+    if (oa.vec)
+      order_warp_kernel<true><<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
+    else
+      order_warp_kernel<false><<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
     FFS_CUDA(cudaGetLastError());
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);
