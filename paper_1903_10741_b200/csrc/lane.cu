@@ -457,10 +457,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   L.MW = NIB ? (GO + 2) / 3 : (GO + 1) >> 1;
   constexpr uint32_t TM = NIB ? 0x3FFu : 0xFFFFu;   // time field mask
   L.hcap = a.h_cap;
-  // mode 2: per 32-tick word w, five words at LB + 5w: the four bit planes of
-  // the headroom Q_max - Q_t and the blocked bits (headroom == 0); two
-  // sentinel tick-words past the horizon are free
-  L.LW = NIB ? 5 * ((a.h_cap >> 5) + 2) : a.h_cap >> 2;
+  // mode 2: per 32-tick word w, the four bit planes of the headroom
+  // Q_max - Q_t at LB + 4w .. 4w+3; blocked bits (headroom == 0) at BB + w as
+  // in modes 0/1, with the same two free sentinel words past the horizon
+  L.LW = NIB ? 4 * (a.h_cap >> 5) : a.h_cap >> 2;
   L.BW = a.h_cap >> 5;
   const int LB = L.RW + L.MW, BB = LB + L.LW;
   const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
@@ -487,12 +487,13 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     if (NIB) {
       const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
       const uint32_t qm = (uint32_t)h.q_max;
-      for (int w = 0; w < L.LW; w += 5)
+      for (int tw = 0; tw < BW; ++tw) {
+        const bool init = 5 * tw < h.hn_words0;
 #pragma unroll
-        for (int b = 0; b < 5; ++b) {
-          const uint32_t v = w < h.hn_words0 ? pl0[w + b] : (b < 4 && ((qm >> b) & 1u) ? 0xFFFFFFFFu : 0u);
-          sts(waddr(L, LB + w + b), v);
-        }
+        for (int b = 0; b < 4; ++b)
+          sts(waddr(L, LB + 4 * tw + b), init ? pl0[5 * tw + b] : (((qm >> b) & 1u) ? 0xFFFFFFFFu : 0u));
+        sts(waddr(L, BB + tw), init ? pl0[5 * tw + 4] : 0u);
+      }
     } else {
       for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
       for (int w = 0; w < BW; ++w) {
@@ -501,10 +502,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         sts(waddr(L, BB + w), bits);
       }
     }
-    if (!NIB) {
-      sts(waddr(L, BB + BW), 0u);
-      sts(waddr(L, BB + BW + 1), 0u);
-    }
+    sts(waddr(L, BB + BW), 0u);
+    sts(waddr(L, BB + BW + 1), 0u);
     int32_t *srow = nullptr;
     if (SCHED && active) {
       srow = a.start_out + gc * h.cells;
@@ -534,9 +533,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
           const int t0 = max((int)(field_at<NIB>(rw, A.rsh) & TM), (int)(field_at<NIB>(mw, A.msh) & TM));
           // C: first run of p un-blocked ticks in the 32-tick window at t0
           //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
-          constexpr uint32_t BST = NIB ? 5 * 128 : 128;     // bytes between consecutive blocked words
-          const uint32_t bwa = NIB ? waddr(L, LB + 5 * min(t0 >> 5, BW) + 4) : waddr(L, BB + min(t0 >> 5, BW));
-          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + BST), t0 & 31), A);
+          const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
+          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), A);
           int S;
           if (UQ) {
             // window miss: slide by 33 - p ticks (a run starting in the last
@@ -545,8 +543,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             int t = t0;
             while (f == 0u) {
               t += 33 - A.p;
-              const uint32_t bwb = NIB ? waddr(L, LB + 5 * min(t >> 5, BW) + 4) : waddr(L, BB + min(t >> 5, BW));
-              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + BST), t & 31), A);
+              const uint32_t bwb = waddr(L, BB + min(t >> 5, BW));
+              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31), A);
             }
             S = t + __ffs(f) - 1;
           } else {
@@ -566,7 +564,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
               // bit planes under the p-bit mask (a second tick-word only when
               // the interval crosses a 32-tick boundary); blocked = headroom 0
               const int sh = S & 31;
-              const uint32_t a0 = waddr(L, LB + 5 * (S >> 5));
+              const uint32_t a0 = waddr(L, LB + 4 * (S >> 5));
+              const uint32_t b0 = waddr(L, BB + (S >> 5));
               uint32_t bm = A.nmo << sh;
               const uint32_t bhi = __funnelshift_l(A.nmo, 0u, (uint32_t)sh);
               {
@@ -582,11 +581,11 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
                 sts(a0 + 128, n1);
                 sts(a0 + 256, n2);
                 sts(a0 + 384, n3);
-                sts(a0 + 512, ~(n0 | n1 | n2 | n3));
+                sts(b0, ~(n0 | n1 | n2 | n3));
               }
               if (bhi) {
                 uint32_t b2 = bhi;
-                const uint32_t a1 = a0 + 640;
+                const uint32_t a1 = a0 + 512;
                 const uint32_t h0 = lds(a1), h1 = lds(a1 + 128), h2 = lds(a1 + 256), h3 = lds(a1 + 384);
                 const uint32_t n0 = h0 ^ b2;
                 b2 &= ~h0;
@@ -599,7 +598,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
                 sts(a1 + 128, n1);
                 sts(a1 + 256, n2);
                 sts(a1 + 384, n3);
-                sts(a1 + 512, ~(n0 | n1 | n2 | n3));
+                sts(b0 + 128, ~(n0 | n1 | n2 | n3));
               }
               if (SCHED) srow[A.e / h.O] = S + h.rs;
               continue;
