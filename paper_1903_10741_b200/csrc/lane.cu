@@ -84,7 +84,7 @@ struct OrdArgs {
   const int16_t *y;
   int64_t first, count;
   int64_t row;             // genes between chromosomes (>= K)
-  int32_t vec;             // row % 4 == 0 and 16-B aligned bases: 4-gene vector loads
+  int32_t vec;             // row % 16 == 0 and 16-B aligned bases: TMA bulk row staging
   int32_t K;
   const uint32_t *head;    // [ceil(K/32)] bit g: first pending gene of its job
   const uint32_t *gbase;   // [K] (j*G + s)*O
@@ -122,11 +122,12 @@ __device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, i
   }
 }
 
-template <bool VEC>
+// BULK: the row was staged in shared memory (the genes g0..g0+3 are one 8-byte word)
+template <bool BULK>
 __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *head, int K, int g0, int y[4],
                                           uint32_t &h) {
-  if (VEC) {   // the row's genes g0..g0+3 are one aligned 8-byte word (padding genes past K are masked)
-    const uint2 w = g0 < K ? __ldg((const uint2 *)(yr + g0)) : make_uint2(0, 0);
+  if (BULK) {
+    const uint2 w = *(const uint2 *)(yr + g0);
     const int v[4] = {(int)(int16_t)(w.x & 0xFFFFu), (int)(int16_t)(w.x >> 16), (int)(int16_t)(w.y & 0xFFFFu),
                       (int)(int16_t)(w.y >> 16)};
 #pragma unroll
@@ -142,19 +143,29 @@ __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *hea
   if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
 }
 
-template <bool VEC>
 __device__ __forceinline__ void load_xquad(const int8_t *xr, int K, int g0, uint32_t &xw) {
-  if (VEC) {
-    xw = g0 < K ? __ldg((const uint32_t *)(xr + g0)) : 0u;
-    return;
-  }
   xw = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (g0 + k < K) xw |= (uint32_t)(uint8_t)__ldg(xr + g0 + k) << (8 * k);
 }
 
-template <bool VEC>
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// BULK (row % 16 == 0, 16-B aligned bases -- the GA's padded population):
+// each warp stages its chromosome's whole y row into pmv and x row into xs
+// with two TMA bulk copies (one elected lane, per-warp mbarrier) instead of
+// per-lane global loads; pass A then reads y from shared memory and writes
+// the prefix minima over it in place.
+template <bool BULK>
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
@@ -173,6 +184,13 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;
   for (int i = threadIdx.x; i < K; i += blockDim.x) gtab[i] = __ldg(a.gbase + i);
   for (int i = threadIdx.x; i < 4 * NT; i += blockDim.x) headS[i] = i < ((K + 31) >> 5) ? __ldg(a.head + i) : 0u;
+  __shared__ __align__(8) uint64_t obar[32];
+  const uint32_t bar = smem_u32(&obar[warp]);
+  uint32_t phase = 0;
+  if (BULK && lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const int64_t ntile = (a.count + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
@@ -180,27 +198,53 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
     if (c < a.count) {
       const int16_t *yr = a.y + (a.first + c) * a.row;
       const int8_t *xr = a.x + (a.first + c) * a.row;
+      if (BULK && lane == 0) {
+        const uint32_t yb = (uint32_t)a.row * 2u, xb = (uint32_t)a.row;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the previous row's generic writes
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(yb + xb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(pmv)),
+                     "l"(yr), "r"(yb), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(xs)),
+                     "l"(xr), "r"(xb), "r"(bar)
+                     : "memory");
+      }
       // hist/start are indexed by u = K - pm (descending prefix minimum), with
       // a dummy slot u = K for genes past the end (no branches around atomics)
       for (int i = lane; i < ((K + 2 + 127) >> 7) << 6; i += 32) hist[i] = 0u;
       __syncwarp();
+      if (BULK) {
+        while (!mbar_try(bar, phase)) {
+        }
+        phase ^= 1u;
+      }
       // ---- pass A: prefix minima (kept with a leader flag in bit 15), histogram
       int carry = INT_MAX;
-      // software pipeline: tile t+1's genes are loaded while tile t is scanned
+      // software pipeline (global loads): tile t+1's genes are loaded while
+      // tile t is scanned
       int yq[4];
-      uint32_t hq, xq;
-      load_quad<VEC>(yr, headS, K, 4 * lane, yq, hq);
-      load_xquad<VEC>(xr, K, 4 * lane, xq);
+      uint32_t hq = 0, xq = 0;
+      if (!BULK) {
+        load_quad<false>(yr, headS, K, 4 * lane, yq, hq);
+        load_xquad(xr, K, 4 * lane, xq);
+      }
       for (int t = 0; t < NT; ++t) {
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
-        uint32_t h = hq;
+        uint32_t h;
+        if (BULK) {
+          load_quad<true>((const int16_t *)pmv, headS, K, g0, y, h);
+        } else {
+          h = hq;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) y[k] = yq[k];
-        *(uint32_t *)(xs + g0) = xq;
-        if (t + 1 < NT) {
-          load_quad<VEC>(yr, headS, K, g0 + 128, yq, hq);
-          load_xquad<VEC>(xr, K, g0 + 128, xq);
+          for (int k = 0; k < 4; ++k) y[k] = yq[k];
+          *(uint32_t *)(xs + g0) = xq;
+          if (t + 1 < NT) {
+            load_quad<false>(yr, headS, K, g0 + 128, yq, hq);
+            load_xquad(xr, K, g0 + 128, xq);
+          }
         }
         pm_quad(y, h, carry, lane, pm);
         uint32_t pk[4];
@@ -708,7 +752,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.first = first;
     oa.count = a.count;
     oa.row = a0.row > 0 ? a0.row : K;
-    oa.vec = (oa.row % 4 == 0) && ((uintptr_t)a0.x % 16 == 0) && ((uintptr_t)a0.y % 16 == 0);
+    oa.vec = (oa.row % 16 == 0) && ((uintptr_t)a0.x % 16 == 0) && ((uintptr_t)a0.y % 16 == 0);
     oa.K = K;
     oa.head = (const uint32_t *)((const unsigned char *)st.image_dev +
                                  ((const ImageHdr *)st.image_host.data())->off_head);

@@ -293,7 +293,7 @@ ffs_status State::build_image() {
                  32 * ntl * 128;                                                                  // x staging
     }
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
-    if (warps < 2 || hc < 32 || ord_smem > (size_t)kSmemLimit || K > 65535) {
+    if (warps < 2 || hc < 32 || ord_smem + 2048 > (size_t)kSmemLimit || K > 65535) {   // + static smem
       lane_ok = false;
     } else {
       lane_hcap = (int32_t)hc;
