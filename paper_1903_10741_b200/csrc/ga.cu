@@ -335,16 +335,17 @@ struct GenArgs {
   int8_t *xn; int16_t *yn;                     // next generation
 };
 
-__device__ __forceinline__ void argmax5(int lane, int sub, const int64_t *fitI, int cell, int w, int h,
+__device__ __forceinline__ void argmax5(int lane, int sub, const int64_t *fitI, int row, int col, int w, int h,
                                         int &winner) {
-  // lanes sub*16 + k, k < 5: candidate k of `cell` in the order self, N, S, E, W
-  int row = cell / w, col = cell % w;
+  // lanes sub*16 + k, k < 5: candidate k of cell (row, col) in the order
+  // self, N, S, E, W (torus inside the island, R17)
+  const int cell = row * w + col;
   int k = lane - sub * 16;
   int nb = cell;
-  if (k == 1) nb = ((row + h - 1) % h) * w + col;
-  else if (k == 2) nb = ((row + 1) % h) * w + col;
-  else if (k == 3) nb = row * w + (col + 1) % w;
-  else if (k == 4) nb = row * w + (col + w - 1) % w;
+  if (k == 1) nb = (row == 0 ? h - 1 : row - 1) * w + col;
+  else if (k == 2) nb = (row + 1 == h ? 0 : row + 1) * w + col;
+  else if (k == 3) nb = row * w + (col + 1 == w ? 0 : col + 1);
+  else if (k == 4) nb = row * w + (col == 0 ? w - 1 : col - 1);
   long long f = (k >= 0 && k < 5) ? (long long)fitI[nb] : -1;  // fitness >= 0
   int kk = (k >= 0 && k < 5) ? k : 99;
 #pragma unroll
@@ -407,28 +408,34 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
   const int nxv = (int)(row >> 4), nyv = (int)(row >> 3);   // 16-B words of a row
   for (int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; pi < a.npairs; pi += nw) {
     const int64_t li = pi / half;
-    const int pr = (int)(pi % half);
-    const int ca = (pr / wh) * a.w + 2 * (pr % wh), cb = ca + 1;
+    const int pr = (int)(pi - li * half);
+    const int prow = pr / wh, pcol = 2 * (pr - prow * wh);
+    const int ca = prow * a.w + pcol, cb = ca + 1;
     const uint32_t I = (uint32_t)(a.island0 + li), kg = (uint32_t)a.k;
     const int64_t base = li * a.tile;
     // a6: asteroid selection on the previous generation's fitness
     int wa, wb;
-    argmax5(lane, 0, a.fp + base, ca, a.w, a.h, wa);
-    argmax5(lane, 1, a.fp + base, cb, a.w, a.h, wb);
+    argmax5(lane, 0, a.fp + base, prow, pcol, a.w, a.h, wa);
+    argmax5(lane, 1, a.fp + base, prow, pcol + 1, a.w, a.h, wb);
     const uint4 *XA = (const uint4 *)(a.xp + (base + wa) * row), *XB = (const uint4 *)(a.xp + (base + wb) * row);
     const uint4 *YA = (const uint4 *)(a.yp + (base + wa) * row), *YB = (const uint4 *)(a.yp + (base + wb) * row);
     uint4 *xa = (uint4 *)(a.xn + (base + ca) * row), *xb = (uint4 *)(a.xn + (base + cb) * row);
     uint4 *ya = (uint4 *)(a.yn + (base + ca) * row), *yb = (uint4 *)(a.yn + (base + cb) * row);
+    // the pair's three Philox blocks, one per lane 0..2, then broadcast:
+    // lane 0 = crossover (a7), lanes 1, 2 = mutation of children a, b (a8)
+    const u32x4 rl = philox(lane == 0 ? (RNG_XO << 24) : (RNG_MUT << 24), (uint32_t)(lane == 2 ? cb : ca), kg, I,
+                            k0, k1);
+    const uint32_t xo0 = __shfl_sync(FULL, rl.x, 0), xo1 = __shfl_sync(FULL, rl.y, 0);
+    u32x4 rma, rmb;
+    rma.x = __shfl_sync(FULL, rl.x, 1); rma.y = __shfl_sync(FULL, rl.y, 1); rma.z = __shfl_sync(FULL, rl.z, 1);
+    rmb.x = __shfl_sync(FULL, rl.x, 2); rmb.y = __shfl_sync(FULL, rl.y, 2); rmb.z = __shfl_sync(FULL, rl.z, 2);
+    rma.w = rmb.w = 0u;
     // a7: crossover fires with p_c; one row-major cut shared by X and Y (R13)
-    u32x4 rxo = philox((RNG_XO << 24), (uint32_t)ca, kg, I, k0, k1);
     int kc = K;
-    if (rxo.x < a.xo_thr) {
-      int p = 1 + (int)bounded(rxo.y, (uint32_t)(a.cells - 1));
+    if (xo0 < a.xo_thr) {
+      int p = 1 + (int)bounded(xo1, (uint32_t)(a.cells - 1));
       kc = a.cut[p];
     }
-    // a8 draws for both children
-    u32x4 rma = philox((RNG_MUT << 24), (uint32_t)ca, kg, I, k0, k1);
-    u32x4 rmb = philox((RNG_MUT << 24), (uint32_t)cb, kg, I, k0, k1);
     const bool ma = rma.x < a.mut_thr, mb = rmb.x < a.mut_thr;
     const bool repair = kc > 0 && kc < K;
     if (repair) {
@@ -527,19 +534,11 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
         const int tot = __shfl_sync(FULL, ia, 31);
         da += tot & 0xFFFF;
         db += tot >> 16;
-        while (fa) {
-          const int j = __ffs(fa) - 1;
-          fa &= fa - 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
           const int sh = 16 * (j & 1);
-          const uint32_t w = wsel(za, j >> 1);
-          wset(za, j >> 1, (w & ~(0xFFFFu << sh)) | ((uint32_t)LA[ra++] << sh));
-        }
-        while (fb) {
-          const int j = __ffs(fb) - 1;
-          fb &= fb - 1;
-          const int sh = 16 * (j & 1);
-          const uint32_t w = wsel(zb, j >> 1);
-          wset(zb, j >> 1, (w & ~(0xFFFFu << sh)) | ((uint32_t)LB[rb++] << sh));
+          if ((fa >> j) & 1u) wset(za, j >> 1, (wsel(za, j >> 1) & ~(0xFFFFu << sh)) | ((uint32_t)LA[ra++] << sh));
+          if ((fb >> j) & 1u) wset(zb, j >> 1, (wsel(zb, j >> 1) & ~(0xFFFFu << sh)) | ((uint32_t)LB[rb++] << sh));
         }
       }
       if (i < nyv) {
@@ -550,12 +549,12 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
     __syncwarp();
     // a8: swap two priorities
     if (K >= 2 && lane < 2) {
-      const u32x4 &rm = lane == 0 ? rma : rmb;
+      const uint32_t r1 = lane == 0 ? rma.y : rmb.y, r2 = lane == 0 ? rma.z : rmb.z;
       const bool fire = lane == 0 ? ma : mb;
       int16_t *yy = (int16_t *)(lane == 0 ? ya : yb);
       if (fire) {
-        int g1 = (int)bounded(rm.y, (uint32_t)K);
-        int g2 = (int)bounded(rm.z, (uint32_t)(K - 1));
+        int g1 = (int)bounded(r1, (uint32_t)K);
+        int g2 = (int)bounded(r2, (uint32_t)(K - 1));
         g2 += g2 >= g1;
         int16_t t = yy[g1];
         yy[g1] = yy[g2];
