@@ -14,7 +14,9 @@
 //   replace_kernel     CTA per island: elitist replacement
 //   donor/import       ring migration every migration_interval,
 //                      allgather hook across processes
-//   trace_kernel       min objective and sum of objectives
+//   trace              min objective and sum of objectives: per-island partials in
+//                      replace_kernel (import_kernel on migration generations),
+//                      reduced by the last island block to finish
 // Random draws: Philox4x32-10 keyed by the seed, counter
 // (purpose << 24 | block, individual, generation, island) -- DESIGN.md "RNG".
 #include <algorithm>
@@ -47,6 +49,8 @@ struct Run {
   size_t rec = 0;
   int64_t *scal = nullptr;          // [0] emax, [1] max objective
   int64_t *tmin = nullptr, *tsum = nullptr;
+  int64_t *parts = nullptr;         // [islands][2] per-island trace partials
+  unsigned *tcounter = nullptr;     // islands finished in the current trace
   OvfScratch scr;
   int64_t evaluations = 0;
   int launches = 0;
@@ -209,8 +213,18 @@ __global__ void history_init_kernel(int64_t row, int tile, const int8_t *x, cons
 
 // elitist replacement (R21): strict improvement updates the history;
 // the island's worst cell is overwritten by the history elite.
+struct TraceArgs {
+  int64_t *parts;
+  unsigned *counter;
+  int64_t *tmin, *tsum;
+  int k, real, nisl, on;
+};
+
+__device__ void island_trace(const int64_t *obj_isl, int tile, int real, int li, int nisl, int64_t *parts,
+                             unsigned *counter, int64_t *tmin, int64_t *tsum, int k);
+
 __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
-                               int16_t *hy, int64_t *hobj, int64_t *hfit) {
+                               int16_t *hy, int64_t *hobj, int64_t *hfit, TraceArgs tr) {
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
@@ -227,6 +241,10 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
   __syncthreads();
   copy_row(x + cw * row, y + cw * row, hxr, hyr, row);
   if (threadIdx.x == 0) { obj[cw] = hobj[li]; fit[cw] = hfit[li]; }
+  if (tr.on) {   // no migration this generation: the trace is final now
+    __syncthreads();
+    island_trace(obj + base, tile, tr.real, li, tr.nisl, tr.parts, tr.counter, tr.tmin, tr.tsum, tr.k);
+  }
 }
 
 // ring migration, part 1: snapshot every island's best (after replacement)
@@ -251,9 +269,9 @@ __global__ void donor_kernel(int K, int64_t row, int tile, size_t rec, const int
 
 // part 2: island li's worst cell <- best of island li-1; island 0 of the shard
 // <- `incoming` (the last island of the previous shard, or of this shard)
-__global__ void import_kernel(int K, int64_t row, size_t rec, const unsigned char *donor,
+__global__ void import_kernel(int K, int64_t row, int tile, size_t rec, const unsigned char *donor,
                               const unsigned char *incoming, const int32_t *worst_idx, int8_t *x, int16_t *y,
-                              int64_t *obj, int64_t *fit) {
+                              int64_t *obj, int64_t *fit, TraceArgs tr) {
   const int li = blockIdx.x;
   const unsigned char *src = li == 0 ? incoming : donor + (size_t)(li - 1) * rec;
   const int64_t cw = worst_idx[li];
@@ -266,61 +284,114 @@ __global__ void import_kernel(int K, int64_t row, size_t rec, const unsigned cha
     obj[cw] = o;
     fit[cw] = f;
   }
+  __syncthreads();
+  island_trace(obj + (int64_t)li * tile, tile, tr.real, li, tr.nisl, tr.parts, tr.counter, tr.tmin, tr.tsum, tr.k);
 }
 
 // trace[k] = (min objective, sum of objectives).  Real-WT words (f3): the min
 // works on the words (non-negative doubles), the sum is a binary64 sum in a
-// fixed order (per-thread strided partials, then a fixed shuffle tree), so it
-// is deterministic but rounds differently from a sequential sum.
-__global__ void trace_kernel(const int64_t *obj, int64_t n, int64_t *tmin, int64_t *tsum, int k, int real) {
-  __shared__ long long smin[32];
-  __shared__ long long ssum[32];
-  __shared__ double dsum[32];
-  long long mn = LLONG_MAX, sm = 0;
-  if (real) {
-    double ds = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      mn = min(mn, (long long)obj[i]);
-      ds += __longlong_as_double(obj[i]);
-    }
-    for (int d = 16; d > 0; d >>= 1) {
-      mn = min(mn, __shfl_xor_sync(FULL, mn, d));
-      ds += __shfl_xor_sync(FULL, ds, d);
-    }
-    if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = mn; dsum[threadIdx.x >> 5] = ds; }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int nw = blockDim.x >> 5;
-      mn = threadIdx.x < nw ? smin[threadIdx.x] : LLONG_MAX;
-      ds = threadIdx.x < nw ? dsum[threadIdx.x] : 0.0;
-      for (int d = 16; d > 0; d >>= 1) {
-        mn = min(mn, __shfl_xor_sync(FULL, mn, d));
-        ds += __shfl_xor_sync(FULL, ds, d);
-      }
-      if (threadIdx.x == 0) { tmin[k] = mn; tsum[k] = __double_as_longlong(ds); }
-    }
-    return;
-  }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    mn = min(mn, (long long)obj[i]);
-    sm += obj[i];
+// fixed order (strided per-thread partials, a fixed shuffle tree, islands in
+// index order), so it is deterministic but rounds differently from a
+// sequential sum.
+// Block reduction of (min, sum) over v[0..n) (all threads get the result).
+__device__ void block_min_sum(const int64_t *v, int64_t n, int real, long long &mn, long long &sm) {
+  __shared__ long long smin[32], ssum[32];
+  mn = LLONG_MAX;
+  long long si = 0;
+  double sd = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {   // L2 loads: partials written by other blocks
+    const long long a = __ldcg((const long long *)v + 2 * i), b = __ldcg((const long long *)v + 2 * i + 1);
+    mn = min(mn, a);
+    if (real) sd += __longlong_as_double(b);
+    else si += b;
   }
   for (int d = 16; d > 0; d >>= 1) {
     mn = min(mn, __shfl_xor_sync(FULL, mn, d));
-    sm += __shfl_xor_sync(FULL, sm, d);
+    if (real) sd += __shfl_xor_sync(FULL, sd, d);
+    else si += __shfl_xor_sync(FULL, si, d);
   }
-  if ((threadIdx.x & 31) == 0) { smin[threadIdx.x >> 5] = mn; ssum[threadIdx.x >> 5] = sm; }
+  if ((threadIdx.x & 31) == 0) {
+    smin[threadIdx.x >> 5] = mn;
+    ssum[threadIdx.x >> 5] = real ? __double_as_longlong(sd) : si;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
-    int nw = blockDim.x >> 5;
+    const int nw = blockDim.x >> 5;
     mn = threadIdx.x < nw ? smin[threadIdx.x] : LLONG_MAX;
-    sm = threadIdx.x < nw ? ssum[threadIdx.x] : 0;
+    long long s2 = threadIdx.x < nw ? ssum[threadIdx.x] : 0;
+    double d2 = threadIdx.x < nw ? __longlong_as_double(ssum[threadIdx.x]) : 0.0;
     for (int d = 16; d > 0; d >>= 1) {
       mn = min(mn, __shfl_xor_sync(FULL, mn, d));
-      sm += __shfl_xor_sync(FULL, sm, d);
+      if (real) d2 += __shfl_xor_sync(FULL, d2, d);
+      else s2 += __shfl_xor_sync(FULL, s2, d);
     }
-    if (threadIdx.x == 0) { tmin[k] = mn; tsum[k] = sm; }
+    if (threadIdx.x == 0) { smin[0] = mn; ssum[0] = real ? __double_as_longlong(d2) : s2; }
   }
+  __syncthreads();
+  mn = smin[0];
+  sm = ssum[0];
+  __syncthreads();
+}
+
+// Island partial (min, sum) of the final objectives of generation k into
+// parts[li]; the last island block to finish (ticket counter) reduces the
+// partials in island order into trace[k] and re-arms the counter.
+__device__ void island_trace(const int64_t *obj_isl, int tile, int real, int li, int nisl, int64_t *parts,
+                             unsigned *counter, int64_t *tmin, int64_t *tsum, int k) {
+  __shared__ unsigned ticket;
+  long long mn, sm;
+  // per-island reduction over the objective words (min and sum of the same values)
+  {
+    __shared__ long long smin[32], ssum[32];
+    mn = LLONG_MAX;
+    long long si = 0;
+    double sd = 0.0;
+    for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+      const long long o = obj_isl[i];
+      mn = min(mn, o);
+      if (real) sd += __longlong_as_double(o);
+      else si += o;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+      if (real) sd += __shfl_xor_sync(FULL, sd, d);
+      else si += __shfl_xor_sync(FULL, si, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      smin[threadIdx.x >> 5] = mn;
+      ssum[threadIdx.x >> 5] = real ? __double_as_longlong(sd) : si;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int nw = blockDim.x >> 5;
+      long long m0 = LLONG_MAX, s0 = 0;
+      double d0 = 0.0;
+      for (int w = 0; w < nw; ++w) {
+        m0 = min(m0, smin[w]);
+        if (real) d0 += __longlong_as_double(ssum[w]);
+        else s0 += ssum[w];
+      }
+      parts[2 * li] = m0;
+      parts[2 * li + 1] = real ? __double_as_longlong(d0) : s0;
+      __threadfence();
+      ticket = atomicAdd(counter, 1u);
+    }
+    __syncthreads();
+  }
+  if (ticket != (unsigned)(nisl - 1)) return;
+  __threadfence();
+  block_min_sum(parts, nisl, real, mn, sm);
+  if (threadIdx.x == 0) {
+    tmin[k] = mn;
+    tsum[k] = sm;
+    *counter = 0u;
+  }
+}
+
+// trace of generation 0 (after the history initialisation): one block per island
+__global__ void trace0_kernel(const int64_t *obj, int tile, int real, int nisl, int64_t *parts, unsigned *counter,
+                              int64_t *tmin, int64_t *tsum) {
+  island_trace(obj + (int64_t)blockIdx.x * tile, tile, real, blockIdx.x, nisl, parts, counter, tmin, tsum, 0);
 }
 
 // ---- one generation's breeding for one horizontal pair (a, b = a + 1)
@@ -619,7 +690,7 @@ static ffs_status ga_init(Run &r) {
   history_init_kernel<<<r.nisl, 256, 0, r.s>>>(r.row, r.tile, r.x[0], r.y[0], r.obj[0], r.fit[0], r.hx, r.hy,
                                                r.hobj, r.hfit);
   FFS_CUDA(cudaGetLastError());
-  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[0], r.nloc, r.tmin, r.tsum, 0, st.real_wt);
+  trace0_kernel<<<r.nisl, 256, 0, r.s>>>(r.obj[0], r.tile, st.real_wt, r.nisl, r.parts, r.tcounter, r.tmin, r.tsum);
   FFS_CUDA(cudaGetLastError());
   r.launches += 3;
   r.cur = 0;
@@ -653,11 +724,13 @@ static ffs_status ga_generation(Run &r) {
   r.launches++;
   ffs_status e = evaluate_population(r, nb, true);
   if (e != FFS_OK) return e;
+  const bool migrate = k % r.cfg.migration_interval == 0 && r.cfg.islands_total >= 2;
+  TraceArgs tr{r.parts, r.tcounter, r.tmin, r.tsum, k, st.real_wt, r.nisl, migrate ? 0 : 1};
   replace_kernel<<<r.nisl, 256, 0, r.s>>>(r.row, r.tile, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.hx, r.hy,
-                                          r.hobj, r.hfit);
+                                          r.hobj, r.hfit, tr);
   FFS_CUDA(cudaGetLastError());
   r.launches++;
-  if (k % r.cfg.migration_interval == 0 && r.cfg.islands_total >= 2) {
+  if (migrate) {
     donor_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb],
                                           r.donor, r.worst_idx);
     FFS_CUDA(cudaGetLastError());
@@ -669,14 +742,11 @@ static ffs_status ga_generation(Run &r) {
         return fail(FFS_ERR_COMM, "allgather hook failed");
       incoming = r.recv + (size_t)((r.cfg.rank + r.cfg.world - 1) % r.cfg.world) * r.rec;
     }
-    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.rec, r.donor, incoming, r.worst_idx, r.x[nb], r.y[nb],
-                                           r.obj[nb], r.fit[nb]);
+    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.donor, incoming, r.worst_idx, r.x[nb],
+                                           r.y[nb], r.obj[nb], r.fit[nb], tr);
     FFS_CUDA(cudaGetLastError());
     r.launches++;
   }
-  trace_kernel<<<1, 1024, 0, r.s>>>(r.obj[nb], r.nloc, r.tmin, r.tsum, k, st.real_wt);
-  FFS_CUDA(cudaGetLastError());
-  r.launches++;
   r.cur = nb;
   r.gen = k;
   return FFS_OK;
@@ -738,6 +808,12 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
   if (e == FFS_OK) e = r.alloc(&r.scal, 2);
   if (e == FFS_OK) e = r.alloc(&r.tmin, (size_t)cfg->generations + 1);
   if (e == FFS_OK) e = r.alloc(&r.tsum, (size_t)cfg->generations + 1);
+  if (e == FFS_OK) e = r.alloc(&r.parts, (size_t)2 * r.nisl);
+  if (e == FFS_OK) e = r.alloc(&r.tcounter, 1);
+  if (e == FFS_OK) {
+    cudaError_t ce = cudaMemsetAsync(r.tcounter, 0, sizeof(unsigned), r.s);
+    if (ce != cudaSuccess) e = cuda_fail(ce, "trace counter");
+  }
   if (e == FFS_OK && r.K > 0) e = ga_init(r);
   if (e != FFS_OK) {
     delete h;
