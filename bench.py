@@ -180,6 +180,17 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def latest_traffic():
+    """DRAM bytes per evaluate launch (order + decode) from the newest committed
+    ncu --set full capture (profiles/<tag>_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1]))
+    return float(d["dram_bytes_per_evaluate"]), "profiles/" + os.path.basename(files[-1])
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -450,11 +461,14 @@ def run_ours(args):
             alg_ops = 7.1 * K  # per-dispatch average measured by the instrumented oracle
         achieved = eval_only * alg_ops
         out["roofline"] = {"bound": "alu", "achieved": achieved / 1e9, "peak": ISSUE_PEAK / 1e9,
-                           "unit": "Gop/s", "frac": achieved / ISSUE_PEAK, "traffic": None,
+                           "unit": "Gop/s", "frac": achieved / ISSUE_PEAK,
+                           "traffic": (latest_traffic() or (None, None))[0],
+                           "traffic_source": (latest_traffic() or (None, None))[1],
+                           "algorithmic_bytes": float(pop_local * (3 * K + 20)),
                            "note": "algorithmic ops (oracle-counted dispatches + power checks + delay jumps + "
                                    "profile updates per evaluation) / evaluate-kernel time, against the issue "
                                    "rate 148 SM x 4 SMSP x 1.965 GHz (one warp-instruction per op)",
-                           "kernel": "evaluate_kernel", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
+                           "kernel": "evaluate launch (order_warp_kernel + lane_decode_kernel)", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
         out["e2e"] = {"value": e2e_value, "unit": "evals/s",
                       "h2d_bytes_per_step": int(pop_local * K * 3),
                       "d2h_bytes_per_step": int(pop_local * (8 + 8 + 4)),

@@ -80,6 +80,7 @@ want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active
         "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
         "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__average_warp_latency_per_inst_issued.ratio"]
+traffic = None
 for rep in ("prof_eval", "prof_gen"):
     p = os.path.join(src, rep + ".ncu-rep")
     if not os.path.exists(p):
@@ -87,6 +88,16 @@ for rep in ("prof_eval", "prof_gen"):
     raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
+    if rep == "prof_eval" and "dram__bytes_read.sum" in h:
+        # one evaluate launch = the order + decode kernels of the capture
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += sum(float(r[i].replace(",", "")) * scale.get(units[i], 1.0) for r in rows[2:])
+        traffic = {"kernels": [r[h.index("Kernel Name")].split("(")[0] for r in rows[2:]],
+                   "dram_bytes_per_evaluate": tot, "population": 65536,
+                   "source": f"ncu --set full, gpurun_out/{tag}/prof_eval.ncu-rep (scripts/prof_eval.py 65536)"}
     out.append(f"## ncu --set full: {rep}\n")
     out.append("| metric | " + " | ".join(r[h.index("Kernel Name")].split("(")[0][-40:] for r in rows[2:]) + " |")
     out.append("|---|" + "---|" * (len(rows) - 2))
@@ -95,6 +106,9 @@ for rep in ("prof_eval", "prof_gen"):
             i = h.index(w)
             out.append(f"| {w} ({units[i]}) | " + " | ".join(r[i] for r in rows[2:]) + " |")
     out.append("")
+if traffic is not None:
+    json.dump(traffic, open(os.path.join("profiles", f"{tag}_traffic.json"), "w"), indent=1)
+    out.append(f"DRAM traffic per evaluate launch (order + decode): {traffic['dram_bytes_per_evaluate'] / 1e6:.1f} MB\n")
 dst = os.path.join("profiles", f"{tag}_summary.md")
 open(dst, "w").write("\n".join(out) + "\n")
 print(dst)
