@@ -703,6 +703,271 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// Mode 2 (every Q_jsm == 1, Q_max <= 15: the paper's Table 5 setting), one
+// lane per chromosome, SOFTWARE-PIPELINED across dispatches:
+//   iteration r:  commit-1 of op r (job / machine times)
+//                 load op r+1's job / machine words
+//                 commit-2 of op r (headroom planes, blocked bits)
+//                 stage A of op r+2 (table fields, run-test shifts)
+//                 search of op r+1 (earliest power-feasible start)
+// so op r+1's t0 arithmetic overlaps op r's plane update; op r+1's blocked
+// words are read after op r's stores (program order of the shared accesses).
+// Bit order is REVERSED (tick t at bit 31 - t%32 of word t/32): the earliest
+// run is the highest set bit of the run mask, found by one clz.  The two
+// sentinel words past the horizon are BLOCKED, so a run found in the first
+// window always ends inside the horizon (C <= hcap); only the window-slide
+// path can overflow.
+// ---------------------------------------------------------------------------
+struct Op2 {
+  uint32_t ra, ma;        // shared addresses of the job's ready word and the machine word
+  uint32_t rsh, msh;      // wrap-shift amounts of the two 10-bit fields (low 5 bits)
+  uint32_t s1, s2, s4;    // run-test shifts for p
+  uint32_t top;           // the p ticks of an interval starting a 16-tick window: bits 15..16-p
+  int p;
+  uint32_t e;             // table index (SCHED: cell = e / O)
+};
+
+__device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint32_t mbase, uint32_t pt_base,
+                                      uint32_t e) {
+  // host-packed: rsh[0:5] | msh[5:10] | ready word[10:21] | machine word[21:29] | p-1[29:32]
+  const uint32_t tv = pqt[e];
+  Op2 A;
+  A.e = e;
+  A.rsh = tv;
+  A.msh = tv >> 5;
+  A.ra = lbase + ((tv >> 3) & 0x3FF80u);
+  A.ma = mbase + ((tv >> 14) & 0x7F80u);
+  const uint32_t pm1 = tv >> 29;
+  A.p = (int)pm1 + 1;
+  uint4 pt;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(pt.x), "=r"(pt.y), "=r"(pt.z), "=r"(pt.w)
+               : "r"(pt_base + (pm1 << 4)));
+  A.s1 = pt.x;
+  A.s2 = pt.y;
+  A.s4 = pt.z;
+  A.top = pt.w;
+  return A;
+}
+
+// earliest start >= t0 of p free ticks (reversed bit order), or -1 (overflow)
+__device__ __forceinline__ int search2(const Op2 &A, uint32_t rw, uint32_t mw, uint32_t bb_base, int hcap) {
+  const int t0 = (int)max(__funnelshift_r(rw, 0u, A.rsh) & 0x3FFu, __funnelshift_r(mw, 0u, A.msh) & 0x3FFu);
+  const uint32_t wa = bb_base + ((uint32_t)(t0 >> 5) << 7);
+  uint32_t f = ~__funnelshift_l(lds(wa + 128), lds(wa), (uint32_t)t0);
+  f &= f << A.s1;
+  f &= f << A.s2;
+  f &= f << A.s4;
+  int t = t0;
+  if (f == 0u) {
+    // window miss: slide by 33 - p ticks (a run starting in the last p - 1
+    // ticks of the window was not testable); blocked sentinels end it
+    do {
+      t += 33 - A.p;
+      if (t + A.p > hcap) return -1;
+      const uint32_t wb = bb_base + ((uint32_t)(t >> 5) << 7);
+      f = ~__funnelshift_l(lds(wb + 128), lds(wb), (uint32_t)t);
+      f &= f << A.s1;
+      f &= f << A.s2;
+      f &= f << A.s4;
+    } while (f == 0u);
+  }
+  return t + __clz(f);
+}
+
+// Headroom Q_max - Q_t (every Q == 1) of 8 ticks in one word: byte b
+// = bit plane b, tick i of the group at bit 7 - i.  Decrement by one on the
+// ticks of the 8-bit mask m (each has headroom >= 1): plane b flips where m
+// and every lower plane is 0 (borrow chain), i.e. under m & AND_{b'<b} ~h_b'.
+__device__ __forceinline__ uint32_t dec8(uint32_t W, uint32_t mrep) {   // mrep: mask in all four bytes
+  const uint32_t E = ~(W << 8) | 0xFFu;                  // byte b: ~h_{b-1}; byte 0: ones
+  const uint32_t E1 = E & ((E << 8) | 0xFFu);
+  const uint32_t E2 = E1 & ((E1 << 16) | 0xFFFFu);      // byte b: AND_{b'<b} ~h_b'
+  return W ^ (mrep & E2);
+}
+// blocked flags of the group (headroom 0 <=> every plane 0), tick i at bit 7 - i
+__device__ __forceinline__ uint32_t blk8(uint32_t W) {
+  uint32_t x = W | (W >> 16);
+  x |= x >> 8;
+  return ~x;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// min(field, cap) for the three 10-bit fields of a word
+__device__ __forceinline__ uint32_t clamp3(uint32_t w, uint32_t cap) {
+  uint32_t o = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o |= min((w >> (10 * i)) & 0x3FFu, cap) << (10 * i);
+  return o;
+}
+
+template <bool SCHED>
+__global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_t lane_wpt) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint4 ptab[8];      // by p-1: run-test shifts (a, b, c), p ticks at bits 15..16-p
+  if (threadIdx.x < 8) {
+    const int p = threadIdx.x + 1;
+    const uint32_t sa = p >= 2 ? 1u : 0u;
+    const uint32_t sb = p >= 4 ? 2u : (p == 3 ? 1u : 0u);
+    const uint32_t sc = p >= 5 ? (uint32_t)(p - 4) : 0u;
+    ptab[threadIdx.x] = make_uint4(sa, sb, sc, ((1u << p) - 1u) << (16 - p));
+  }
+  const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
+  stage_image(smem, a.image, img_bytes, &bar);
+  uint32_t pt_base = smem_u32(ptab);
+  pin(pt_base);
+  const ImageHdr &h = *(const ImageHdr *)smem;
+  const int K = h.K, KQ = (K + 3) >> 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lbase = smem_u32(smem + img_bytes + (size_t)warp * lane_wpt * 128) + lane * 4;
+  const int RW = (h.NJ + 2) / 3, MW = (h.G * h.O + 2) / 3;
+  const int hcap = a.h_cap, BW = hcap >> 5;
+  const int LB = RW + MW, BB = LB + 4 * BW + 1;   // 4 plane words per 32 ticks + one dummy group
+  uint32_t mbase = lbase + ((uint32_t)RW << 7), pl_base = lbase + ((uint32_t)LB << 7),
+           bb_base = lbase + ((uint32_t)BB << 7);
+  pin(mbase);
+  pin(pl_base);
+  pin(bb_base);
+  const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
+  const uint32_t *r10 = (const uint32_t *)(smem + h.off_ready16);
+  const uint32_t *m10 = (const uint32_t *)(smem + h.off_mfree16);
+  const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
+  const int64_t ntile = (a.count + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
+    const int64_t c = tile * 32 + lane;
+    const bool active = c < a.count;
+    const int64_t gc = a.first + c;
+    // --- initial state: times clamped to the horizon (an op that cannot start
+    // before it overflows either way), RUNNING ops' headroom, sentinels
+    for (int w = 0; w < RW; ++w) sts(lbase + ((uint32_t)w << 7), clamp3(r10[w], (uint32_t)hcap));
+    for (int w = 0; w < MW; ++w) sts(mbase + ((uint32_t)w << 7), clamp3(m10[w], (uint32_t)hcap));
+    {
+      // host image: per 32 ticks four plane words + blocked word, tick t at bit t%32
+      const uint32_t qm = (uint32_t)h.q_max;
+      for (int tw = 0; tw < BW; ++tw) {
+        const bool init = 5 * tw < h.hn_words0;
+        uint32_t pr[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) pr[b] = init ? __brev(pl0[5 * tw + b]) : (((qm >> b) & 1u) ? 0xFFFFFFFFu : 0u);
+        // group k (ticks 32tw + 8k ..) = byte 3-k of every reversed plane
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t sel = 3u - (uint32_t)k;
+          const uint32_t lo = __byte_perm(pr[0], pr[1], sel | ((sel + 4u) << 4));
+          const uint32_t hi = __byte_perm(pr[2], pr[3], sel | ((sel + 4u) << 4));
+          sts(pl_base + ((uint32_t)(4 * tw + k) << 7), __byte_perm(lo, hi, 0x5410));
+        }
+        sts(bb_base + ((uint32_t)tw << 7), init ? __brev(pl0[5 * tw + 4]) : 0u);
+      }
+      sts(pl_base + ((uint32_t)(4 * BW) << 7), 0u);   // dummy group past the horizon: blocked
+      sts(bb_base + ((uint32_t)BW << 7), 0xFFFFFFFFu);
+      sts(bb_base + ((uint32_t)(BW + 1) << 7), 0xFFFFFFFFu);
+    }
+    int32_t *srow = nullptr;
+    if (SCHED && active) {
+      srow = a.start_out + gc * h.cells;
+      for (int k = 0; k < h.cells; ++k) srow[k] = a.fstart[k];
+    }
+    bool live = active;
+    bool ovf = false;
+    const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
+    const int kq_pref = active ? KQ : 0;
+    uint2 cur = active ? op[0] : make_uint2(0, 0);
+    uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
+    // prologue: ops 0 and 1 staged, op 0 searched
+    Op2 A = stage2(pqt, lbase, mbase, pt_base, cur.x & 0xFFFFu);
+    Op2 An = stage2(pqt, lbase, mbase, pt_base, K > 1 ? cur.x >> 16 : 0u);
+    uint32_t rw = lds(A.ra), mw = lds(A.ma);
+    int S = search2(A, rw, mw, bb_base, hcap);
+    if (S < 0) { live = false; ovf = active; }
+    // one pipelined step: commit op r (A, S, rw, mw), load + search op r+1 (An),
+    // stage op r+2 (table index e2); MORE: op r+1 exists
+    auto step = [&](const int r, const uint32_t e2, const bool more) {
+      // commit-1 of op r: job / machine times
+      const int Sx = live ? S : 0;
+      const uint32_t C = live ? (uint32_t)(S + A.p) : 0u;
+      sts(A.ra, (rw & ~__funnelshift_l(0u, 0x3FFu, A.rsh)) | __funnelshift_l(0u, C, A.rsh));
+      sts(A.ma, (mw & ~__funnelshift_l(0u, 0x3FFu, A.msh)) | __funnelshift_l(0u, C, A.msh));
+      if (more) {
+        rw = lds(An.ra);
+        mw = lds(An.ma);
+      }
+      // commit-2 of op r: headroom of the 8-tick groups w = S/8 and w+1, their
+      // blocked bytes (byte 3 - w%4 of blocked word w/4)
+      {
+        const uint32_t w = (uint32_t)Sx >> 3;
+        const uint32_t m16 = live ? A.top >> ((uint32_t)Sx & 7u) : 0u;   // ticks 8w.. at bits 15..
+        const uint32_t pa = pl_base + (w << 7);
+        const uint32_t W0 = lds(pa), W1 = lds(pa + 128);
+        const uint32_t N0 = dec8(W0, __byte_perm(m16, 0u, 0x1111)), N1 = dec8(W1, __byte_perm(m16, 0u, 0x0000));
+        sts(pa, N0);
+        sts(pa + 128, N1);
+        const uint32_t ba = bb_base + ((w >> 2) << 7) + (~w & 3u);
+        sts8(ba, blk8(N0));
+        sts8((w & 3u) == 3u ? ba + 131u : ba - 1u, blk8(N1));
+      }
+      if (SCHED && live) srow[A.e / h.O] = S + h.rs;
+      // stage A of op r+2 (ranks >= K carry the padding index 0: harmless)
+      const Op2 A2 = stage2(pqt, lbase, mbase, pt_base, e2);
+      A = An;
+      An = A2;
+      // search of op r+1
+      if (more) {
+        const int Sn = live ? search2(A, rw, mw, bb_base, hcap) : 0;
+        if (Sn < 0) { live = false; ovf = true; }
+        S = Sn;
+      }
+    };
+    // main loop: whole quads whose every op has a successor (no exits inside)
+    int qd = 0;
+    for (; 4 * qd + 4 < K; ++qd) {
+      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      step(4 * qd + 0, cur.y & 0xFFFFu, true);
+      step(4 * qd + 1, cur.y >> 16, true);
+      step(4 * qd + 2, nxt.x & 0xFFFFu, true);
+      step(4 * qd + 3, nxt.x >> 16, true);
+      cur = nxt;
+      nxt = pre;
+    }
+    // tail: the last 1..4 ops
+    for (int r = 4 * qd; r < K; ++r) {
+      const int k = r & 3;
+      const uint32_t e2 = k == 0 ? cur.y & 0xFFFFu : k == 1 ? cur.y >> 16 : k == 2 ? nxt.x & 0xFFFFu : nxt.x >> 16;
+      step(r, e2, r + 1 < K);
+    }
+    if (!active) continue;
+    if (ovf) {
+      int pos = atomicAdd(&a.ovf[0], 1);
+      a.ovf[1 + pos] = (int32_t)gc;
+      continue;
+    }
+    // Eqs. (1)-(3) over every job (R9); frozen jobs are constants of the state
+    const int32_t *pj = (const int32_t *)(smem + h.off_pjob);
+    const int32_t *pd = (const int32_t *)(smem + h.off_pdue);
+    int64_t T = 0;
+    int cm = h.frozen_cmax;
+    for (int k = 0; k < h.n_pjobs; ++k) {
+      const int j = pj[k];
+      const int wj = (j * 0xAAAB) >> 17;
+      const int Cr = (int)((lds(lbase + ((uint32_t)wj << 7)) >> ((j - 3 * wj) * 10)) & 0x3FFu);
+      const int tj = Cr - pd[k];
+      T += tj > 0 ? tj : 0;
+      cm = max(cm, Cr + h.rs);
+    }
+    T += h.frozen_T;
+    const int64_t obj = objective_word(h.real_wt, h.wt, h.wt_f, T, cm);
+    if (a.obj) a.obj[gc] = obj;
+    if (a.tard) a.tard[gc] = T;
+    if (a.cmax) a.cmax[gc] = cm;
+    if (a.fit) a.fit[gc] = fitness_word(h.real_wt, *a.emax, obj);   // Eq. (13)
+  }
+}
+
 template <typename KERN>
 ffs_status smem_attr(KERN k, size_t bytes, size_t &done) {
   if (bytes > done) {
@@ -732,7 +997,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
   void (*kern)(EvalArgs, int32_t) =
-      mode == 2 ? (sched ? lane_decode_kernel<2, true> : lane_decode_kernel<2, false>)
+      mode == 2 ? (sched ? lane_decode2_kernel<true> : lane_decode2_kernel<false>)
       : mode == 1 ? (sched ? lane_decode_kernel<1, true> : lane_decode_kernel<1, false>)
                   : (sched ? lane_decode_kernel<0, true> : lane_decode_kernel<0, false>);
   static size_t attr[6] = {0, 0, 0, 0, 0, 0};

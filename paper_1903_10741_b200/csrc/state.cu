@@ -269,15 +269,15 @@ ffs_status State::build_image() {
   if (lane_ok) {
     const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 3072;   // static smem: mask tables + mbarrier
     const int64_t fixed_words = lmode == 2 ? (NJ + 2) / 3 + (G * O + 2) / 3 : (NJ + 1) / 2 + (G * O + 1) / 2;
-    auto words = [&](int64_t hc) {   // + 2 sentinel words / tick-words of `blocked`
-      return lmode == 2 ? fixed_words + 5 * (hc / 32) + 2 : fixed_words + hc / 4 + hc / 32 + 2;
+    auto words = [&](int64_t hc) {   // + 2 sentinel words of `blocked` (+ mode 2: one dummy plane group)
+      return lmode == 2 ? fixed_words + 5 * (hc / 32) + 3 : fixed_words + hc / 4 + hc / 32 + 2;
     };
     // horizon: the proven bound if it fits, else as large as keeps >= 8
     // warps (overflowing chromosomes are re-decoded exactly by the fallback)
     int64_t hc = h_bound;
     const int target_warps = lmode == 2 ? 14 : 8;
     if (words(hc) * 128 * target_warps > lbudget)
-      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - 2) * 32 / (lmode == 2 ? 5 : 9) /
+      hc = std::max<int64_t>(128, (lbudget / (128 * target_warps) - fixed_words - 3) * 32 / (lmode == 2 ? 5 : 9) /
                                       32 * 32);
     if (h_cap_user > 0) hc = std::min<int64_t>(hc, ((int64_t)h_cap_user + 31) / 32 * 32);
     hc = std::min<int64_t>(hc, lmode == 2 ? 992 : 65504);   // 10-bit times in mode 2
