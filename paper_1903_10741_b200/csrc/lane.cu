@@ -179,10 +179,13 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   // CTA-shared copies of the per-gene table base and the segment-head bits,
   // and per-warp staging of the chromosome's machines (read once, in pass A)
   unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
+  // gene table TRANSPOSED inside each 128-gene tile: gene 128t + 4l + k at
+  // 128t + 32k + l, so pass D's reads (lane l, gene k) hit 32 distinct banks
   uint32_t *gtab = (uint32_t *)tail;
-  uint32_t *headS = gtab + ((K + 3) & ~3);
+  uint32_t *headS = gtab + 128 * NT;
   uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) gtab[i] = __ldg(a.gbase + i);
+  for (int i = threadIdx.x; i < K; i += blockDim.x)
+    gtab[(i & ~127) | ((i & 3) << 5) | ((i >> 2) & 31)] = __ldg(a.gbase + i);
   for (int i = threadIdx.x; i < 4 * NT; i += blockDim.x) headS[i] = i < ((K + 31) >> 5) ? __ldg(a.head + i) : 0u;
   __shared__ __align__(8) uint64_t obar[32];
   const uint32_t bar = smem_u32(&obar[warp]);
@@ -220,8 +223,9 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         }
         phase ^= 1u;
       }
-      // ---- pass A: prefix minima (kept with a leader flag in bit 15), histogram
+      // ---- pass A: prefix minima (kept with a leader flag in bit 15), run lengths
       int carry = INT_MAX;
+      int open_u = -1, open_pos = 0;   // the last run seen, length not yet known (warp-uniform)
       // software pipeline (global loads): tile t+1's genes are loaded while
       // tile t is scanned
       int yq[4];
@@ -247,18 +251,47 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           }
         }
         pm_quad(y, h, carry, lane, pm);
-        uint32_t pk[4];
+        // leaders = new prefix minima (pm == y); each distinct pm is one run
+        // (a leader and the non-leaders after it in its job), and a run's
+        // length is stored once, by its leader, at u = K - pm: hist[u] = len
+        uint32_t pk[4], lm = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
           const bool ok = g0 + k < K && v < (unsigned)K;
           const unsigned u = ok ? (unsigned)K - 1u - v : (unsigned)K;
-          atomicAdd(&hist[u >> 1], 1u << ((u & 1u) << 4));
-          pk[k] = ok ? (u | (pm[k] == y[k] ? 0x8000u : 0u)) : (unsigned)K;
+          const bool ld = ok && pm[k] == y[k];
+          lm |= (ld ? 1u : 0u) << k;
+          pk[k] = u | (ld ? 0x8000u : 0u);
         }
         *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
+        // next leader after each of the lane's leaders: inside the quad, else
+        // the first leader of the next lane holding one, else (the tile's
+        // last leader) still open: closed by a later tile or by K
+        const uint32_t B = __ballot_sync(FULL, lm != 0u);
+        const int fpos = g0 + __ffs(lm) - 1;
+        const uint32_t hiB = B & (0xFFFFFFFEu << lane);
+        const int nxl = __shfl_sync(FULL, fpos, hiB ? __ffs(hiB) - 1 : 0);
+        if (B) {
+          const int fl = __ffs(B) - 1;
+          const int first = __shfl_sync(FULL, fpos, fl);
+          if (open_u >= 0 && lane == fl) h16[open_u] = (uint16_t)(first - open_pos);
+          const int ll = 31 - __clz(B);
+          const int kl = 31 - __clz(lm | 1u);
+          const int lpos = __shfl_sync(FULL, g0 + kl, ll);
+          open_u = __shfl_sync(FULL, (int)((kl == 0 ? pk[0] : kl == 1 ? pk[1] : kl == 2 ? pk[2] : pk[3]) & 0x7FFFu), ll);
+          open_pos = lpos;
+        }
+        int nx = hiB ? nxl : -1;
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+          if ((lm >> k) & 1u) {
+            if (nx >= 0) h16[pk[k] & 0x7FFFu] = (uint16_t)(nx - (g0 + k));
+            nx = g0 + k;
+          }
         carry = __shfl_sync(FULL, pm[3], 31);
       }
+      if (open_u >= 0 && lane == 0) h16[open_u] = (uint16_t)(K - open_pos);
       __syncwarp();
       // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u)
       uint32_t acc = 0;
@@ -278,37 +311,36 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
-      // ---- pass D: rank(g) = start[u(g)] + (g - leader(g)); scatter (padding
-      // genes write to the dummy rank K)
-      int carry_lp = -1;
+      // ---- pass D: a leader at g ranks start[u(g)]; the genes after it in its
+      // run follow consecutively: rank(g) = base + g with base = start - g_leader
+      int carry_b = 0;
       for (int t = 0; t < NT; ++t) {
         const int g0 = (t << 7) + 4 * lane;
         const uint2 w = *(const uint2 *)(pmv + g0);
         const uint32_t pk[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
-        int lp = -1;
+        int bk[4], lastb = 0;
+        uint32_t lm = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (pk[k] & 0x8000u) lp = g0 + k;
-        // last leader before this lane's quad: the highest lower lane holding one
-        const uint32_t lb = __ballot_sync(FULL, lp >= 0) & ((1u << lane) - 1u);
-        const int src = lb ? 31 - __clz(lb) : 0;
-        const int lpx = __shfl_sync(FULL, lp, src);
-        int run = lb ? lpx : carry_lp;
+        for (int k = 0; k < 4; ++k) {
+          bk[k] = 0;
+          if (pk[k] & 0x8000u) {   // leaders only: padding genes carry u = K, no flag
+            bk[k] = (int)h16[pk[k] & 0x7FFFu] - (g0 + k);
+            lastb = bk[k];
+            lm |= 1u << k;
+          }
+        }
+        const uint32_t B = __ballot_sync(FULL, lm != 0u);
+        const uint32_t lb = B & ((1u << lane) - 1u);
+        const int inb = __shfl_sync(FULL, lastb, lb ? 31 - __clz(lb) : 0);
+        int base = lb ? inb : carry_b;
+        const int tb = (int)(t << 7) + lane;   // transposed gene-table column of gene k: tb + 32k
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
-          const bool ok = g < K;
-          if (pk[k] & 0x8000u) run = g;
-          const unsigned u = pk[k] & 0x7FFFu;          // K (dummy) for padding genes
-          const unsigned r = ok ? min((unsigned)h16[u] + (unsigned)(g - run), (unsigned)K) : (unsigned)K;
-          const int gg = ok ? g : 0;
-          ord[r] = (uint16_t)(gtab[gg] + (uint32_t)xs[gg]);
+          if ((lm >> k) & 1u) base = bk[k];
+          if (g < K) ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
         }
-        {
-          const uint32_t all = __ballot_sync(FULL, lp >= 0);
-          const int last = __shfl_sync(FULL, lp, all ? 31 - __clz(all) : 0);
-          if (all) carry_lp = last;
-        }
+        if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
       }
     }
     __syncthreads();
@@ -722,12 +754,16 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
 struct Op2 {
   uint32_t ra, ma;        // shared addresses of the job's ready word and the machine word
   uint32_t rsh, msh;      // wrap-shift amounts of the two 10-bit fields (low 5 bits)
-  uint32_t s1, s2, s4;    // run-test shifts for p
+  uint32_t rmul, mmul;    // 1 << rsh, 1 << msh: field updates by IMAD (fma pipe)
+  uint32_t m1n, m2, m4;   // run-test multipliers: -(1 << s1), 1 << s2, 1 << s4
   uint32_t top;           // the p ticks of an interval starting a 16-tick window: bits 15..16-p
   int p;
   uint32_t e;             // table index (SCHED: cell = e / O)
 };
 
+// The integer ALU pipe (LOP3/SHF/IADD3/SEL/...) issues every other cycle per
+// SMSP and bounds this kernel; multiplies by powers of two run on the fma
+// pipe, so left shifts by per-op amounts are written as IMADs.
 __device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint32_t mbase, uint32_t pt_base,
                                       uint32_t e) {
   // host-packed: rsh[0:5] | msh[5:10] | ready word[10:21] | machine word[21:29] | p-1[29:32]
@@ -736,6 +772,8 @@ __device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint3
   A.e = e;
   A.rsh = tv;
   A.msh = tv >> 5;
+  A.rmul = 1u << (tv & 31u);
+  A.mmul = 1u << ((tv >> 5) & 31u);
   A.ra = lbase + ((tv >> 3) & 0x3FF80u);
   A.ma = mbase + ((tv >> 14) & 0x7F80u);
   const uint32_t pm1 = tv >> 29;
@@ -744,33 +782,46 @@ __device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint3
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(pt.x), "=r"(pt.y), "=r"(pt.z), "=r"(pt.w)
                : "r"(pt_base + (pm1 << 4)));
-  A.s1 = pt.x;
-  A.s2 = pt.y;
-  A.s4 = pt.z;
+  A.m1n = pt.x;
+  A.m2 = pt.y;
+  A.m4 = pt.z;
   A.top = pt.w;
   return A;
 }
 
-// earliest start >= t0 of p free ticks (reversed bit order), or -1 (overflow)
-__device__ __forceinline__ int search2(const Op2 &A, uint32_t rw, uint32_t mw, uint32_t bb_base, int hcap) {
-  const int t0 = (int)max(__funnelshift_r(rw, 0u, A.rsh) & 0x3FFu, __funnelshift_r(mw, 0u, A.msh) & 0x3FFu);
+// runs of p free ticks in the window w of blocked bits (reversed order): bit
+// i set iff the ticks of bits i, i-1, .., i-p+1 are free.  ~w * m = w * (-m) - m.
+__device__ __forceinline__ uint32_t runs2(uint32_t w, const Op2 &A) {
+  uint32_t f = ~w & (w * A.m1n + A.m1n);
+  f &= f * A.m2;
+  f &= f * A.m4;
+  return f;
+}
+
+// Earliest start >= t0 of p free ticks (reversed bit order).  Overflow (no
+// run inside the horizon, rare path): the lane's result is void (sgn = -1,
+// the fallback re-decodes the chromosome) and its job / machine times are
+// reset to 0, so it goes on with every later access inside its own words and
+// every field update non-negative; the op is committed at 0.
+__device__ __forceinline__ int search2(const Op2 &A, int t0, uint32_t bb_base, int hcap, uint32_t lbase,
+                                       int nfield_words, uint32_t &rw, uint32_t &mw, uint32_t &rf, uint32_t &mf,
+                                       int &sgn) {
   const uint32_t wa = bb_base + ((uint32_t)(t0 >> 5) << 7);
-  uint32_t f = ~__funnelshift_l(lds(wa + 128), lds(wa), (uint32_t)t0);
-  f &= f << A.s1;
-  f &= f << A.s2;
-  f &= f << A.s4;
+  uint32_t f = runs2(__funnelshift_l(lds(wa + 128), lds(wa), (uint32_t)t0), A);
   int t = t0;
   if (f == 0u) {
     // window miss: slide by 33 - p ticks (a run starting in the last p - 1
     // ticks of the window was not testable); blocked sentinels end it
     do {
       t += 33 - A.p;
-      if (t + A.p > hcap) return -1;
+      if (t + A.p > hcap) {
+        for (int w = 0; w < nfield_words; ++w) sts(lbase + ((uint32_t)w << 7), 0u);
+        rw = mw = rf = mf = 0u;
+        sgn = -1;
+        return 0;
+      }
       const uint32_t wb = bb_base + ((uint32_t)(t >> 5) << 7);
-      f = ~__funnelshift_l(lds(wb + 128), lds(wb), (uint32_t)t);
-      f &= f << A.s1;
-      f &= f << A.s2;
-      f &= f << A.s4;
+      f = runs2(__funnelshift_l(lds(wb + 128), lds(wb), (uint32_t)t), A);
     } while (f == 0u);
   }
   return t + __clz(f);
@@ -808,13 +859,13 @@ template <bool SCHED>
 __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_t lane_wpt) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ uint4 ptab[8];      // by p-1: run-test shifts (a, b, c), p ticks at bits 15..16-p
+  __shared__ uint4 ptab[8];      // by p-1: run-test multipliers (-2^a, 2^b, 2^c), p ticks at bits 15..16-p
   if (threadIdx.x < 8) {
     const int p = threadIdx.x + 1;
     const uint32_t sa = p >= 2 ? 1u : 0u;
     const uint32_t sb = p >= 4 ? 2u : (p == 3 ? 1u : 0u);
     const uint32_t sc = p >= 5 ? (uint32_t)(p - 4) : 0u;
-    ptab[threadIdx.x] = make_uint4(sa, sb, sc, ((1u << p) - 1u) << (16 - p));
+    ptab[threadIdx.x] = make_uint4(0u - (1u << sa), 1u << sb, 1u << sc, ((1u << p) - 1u) << (16 - p));
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
@@ -873,8 +924,6 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       srow = a.start_out + gc * h.cells;
       for (int k = 0; k < h.cells; ++k) srow[k] = a.fstart[k];
     }
-    bool live = active;
-    bool ovf = false;
     const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
     const int kq_pref = active ? KQ : 0;
     uint2 cur = active ? op[0] : make_uint2(0, 0);
@@ -883,16 +932,17 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     Op2 A = stage2(pqt, lbase, mbase, pt_base, cur.x & 0xFFFFu);
     Op2 An = stage2(pqt, lbase, mbase, pt_base, K > 1 ? cur.x >> 16 : 0u);
     uint32_t rw = lds(A.ra), mw = lds(A.ma);
-    int S = search2(A, rw, mw, bb_base, hcap);
-    if (S < 0) { live = false; ovf = active; }
+    uint32_t rf = __funnelshift_r(rw, 0u, A.rsh) & 0x3FFu, mf = __funnelshift_r(mw, 0u, A.msh) & 0x3FFu;
+    int sgn = 0;
+    int S = search2(A, (int)max(rf, mf), bb_base, hcap, lbase, RW + MW, rw, mw, rf, mf, sgn);
     // one pipelined step: commit op r (A, S, rw, mw), load + search op r+1 (An),
     // stage op r+2 (table index e2); MORE: op r+1 exists
     auto step = [&](const int r, const uint32_t e2, const bool more) {
-      // commit-1 of op r: job / machine times
-      const int Sx = live ? S : 0;
-      const uint32_t C = live ? (uint32_t)(S + A.p) : 0u;
-      sts(A.ra, (rw & ~__funnelshift_l(0u, 0x3FFu, A.rsh)) | __funnelshift_l(0u, C, A.rsh));
-      sts(A.ma, (mw & ~__funnelshift_l(0u, 0x3FFu, A.msh)) | __funnelshift_l(0u, C, A.msh));
+      // commit-1 of op r: job / machine times, field += (C - field) << shift
+      const int Sx = S;
+      const uint32_t C = (uint32_t)(Sx + A.p);
+      sts(A.ra, rw + (C - rf) * A.rmul);
+      sts(A.ma, mw + (C - mf) * A.mmul);
       if (more) {
         rw = lds(An.ra);
         mw = lds(An.ma);
@@ -901,7 +951,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       // blocked bytes (byte 3 - w%4 of blocked word w/4)
       {
         const uint32_t w = (uint32_t)Sx >> 3;
-        const uint32_t m16 = live ? A.top >> ((uint32_t)Sx & 7u) : 0u;   // ticks 8w.. at bits 15..
+        const uint32_t m16 = A.top >> ((uint32_t)Sx & 7u);   // ticks 8w.. at bits 15..
         const uint32_t pa = pl_base + (w << 7);
         const uint32_t W0 = lds(pa), W1 = lds(pa + 128);
         const uint32_t N0 = dec8(W0, __byte_perm(m16, 0u, 0x1111)), N1 = dec8(W1, __byte_perm(m16, 0u, 0x0000));
@@ -911,16 +961,16 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
         sts8(ba, blk8(N0));
         sts8((w & 3u) == 3u ? ba + 131u : ba - 1u, blk8(N1));
       }
-      if (SCHED && live) srow[A.e / h.O] = S + h.rs;
+      if (SCHED && active) srow[A.e / h.O] = Sx + h.rs;
       // stage A of op r+2 (ranks >= K carry the padding index 0: harmless)
       const Op2 A2 = stage2(pqt, lbase, mbase, pt_base, e2);
       A = An;
       An = A2;
       // search of op r+1
       if (more) {
-        const int Sn = live ? search2(A, rw, mw, bb_base, hcap) : 0;
-        if (Sn < 0) { live = false; ovf = true; }
-        S = Sn;
+        rf = __funnelshift_r(rw, 0u, A.rsh) & 0x3FFu;
+        mf = __funnelshift_r(mw, 0u, A.msh) & 0x3FFu;
+        S = search2(A, (int)max(rf, mf), bb_base, hcap, lbase, RW + MW, rw, mw, rf, mf, sgn);
       }
     };
     // main loop: whole quads whose every op has a successor (no exits inside)
@@ -941,7 +991,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       step(r, e2, r + 1 < K);
     }
     if (!active) continue;
-    if (ovf) {
+    if (sgn < 0) {
       int pos = atomicAdd(&a.ovf[0], 1);
       a.ovf[1 + pos] = (int32_t)gc;
       continue;

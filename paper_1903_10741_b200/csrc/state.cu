@@ -289,7 +289,7 @@ ffs_status State::build_image() {
     {
       const size_t ntl = (size_t)(K + 127) / 128;
       ord_smem = 32 * (ord_hist_bytes + ord_stride + ((ntl * 128 * 2 + 15) & ~(size_t)15)) +   // per warp
-                 (size_t)((K + 3) & ~3) * 4 + ntl * 16 +                                          // gtab, head
+                 ntl * 128 * 4 + ntl * 16 +                                                      // gtab (transposed), head
                  32 * ntl * 128;                                                                  // x staging
     }
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers

@@ -9,3 +9,7 @@ import json,sys
 d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 print({k:d.get(k) for k in ('value','ms_per_step','gens_per_s')}, 'eval_only', d.get('eval_only'))
 PY
+if [ -n "$LAUNCHES" ]; then
+ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/$TAG/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python scripts/launch_table.py gpurun_out/$TAG/launches.csv
+fi
