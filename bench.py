@@ -21,6 +21,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 import numpy as np
@@ -38,7 +39,7 @@ ISSUE_PEAK = 148 * 4 * 1.965e9
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -72,24 +73,42 @@ class ClockSampler:
         self.p = None
 
     def __enter__(self):
+        # nvidia-smi's start-up (NVML init) can stall the GPU for milliseconds:
+        # start it and wait for its first sample BEFORE the timed region
+        self.lines = []
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+            return self
+        self._first = threading.Event()
+
+        def reader():
+            for l in self.p.stdout:
+                if l.strip():
+                    self.lines.append(l.strip())
+                    self._first.set()
+            self._first.set()
+
+        self._t = threading.Thread(target=reader, daemon=True)
+        self._t.start()
+        self._first.wait(timeout=10)
+        time.sleep(0.2)
+        self._skip = len(self.lines)   # samples taken before the timed region
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.p is not None:
             time.sleep(0.25)
             self.p.terminate()
             try:
-                out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+                pass
+            self._t.join(timeout=5)
+            self.lines = self.lines[max(self._skip - 1, 0):]
 
     def summary(self):
         sm, mx, reasons = [], [], set()

@@ -133,6 +133,7 @@ struct State {
   int lane_warps_per_cta = 0, lane_ctas_per_sm = 1;
   size_t lane_smem = 0;
   size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0;   // order kernel (32 warps per CTA)
+  int32_t max_pending = 0;                                   // most pending genes of one job
   int ord_ctas_per_sm = 1;
   OvfScratch scratch;
   HostStage stage;

@@ -27,6 +27,8 @@
 //   of `blocked` (run test by shifts/ands); ops with q > min Q verify the bytes.
 //   Commit adds q to p bytes (byte SIMD, no carries since Q_max <= 127) and
 //   ORs their bit-7 flags into `blocked`.
+#include <type_traits>
+
 #include "device_util.cuh"
 
 namespace edffs {
@@ -94,7 +96,11 @@ struct OrdArgs {
   uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
 };
 
-// prefix minima of the lane's four genes given the running min before the tile
+// prefix minima of the lane's four genes given the running min before the tile.
+// A job's pending genes (<= G of them, consecutive) span at most
+// floor((G+2)/4) + 1 lanes, so the segmented scan needs only SCAN doubling
+// steps with 2^SCAN > that span - 1 (SCAN = 2 for G <= 13).
+template <int SCAN>
 __device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, int lane, int pm[4]) {
   // v = min over the lane's genes from its last segment head (or all four)
   int v = y[0];
@@ -106,7 +112,8 @@ __device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, i
   const uint32_t below = hb & (0xFFFFFFFFu >> (31 - lane));      // head lanes <= lane
   const int s0 = below ? 31 - __clz(below) : -1;                    // -1: no head in this tile yet
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
+  for (int i = 0; i < SCAN; ++i) {
+    const int d = 1 << i;
     const int vn = __shfl_up_sync(FULL, v, d);
     if (lane - d >= s0 && lane >= d) v = min(v, vn);
   }
@@ -122,25 +129,28 @@ __device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, i
   }
 }
 
-// BULK: the row was staged in shared memory (the genes g0..g0+3 are one 8-byte word)
-template <bool BULK>
+// BULK: the row was staged in shared memory (the genes g0..g0+3 are one 8-byte
+// word).  FULL: every gene of the tile is < K (no bounds tests).  y is in
+// [1, K] (a permutation), so the halves need no sign extension.
+template <bool BULK, bool FULL = false>
 __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *head, int K, int g0, int y[4],
                                           uint32_t &h) {
   if (BULK) {
     const uint2 w = *(const uint2 *)(yr + g0);
-    const int v[4] = {(int)(int16_t)(w.x & 0xFFFFu), (int)(int16_t)(w.x >> 16), (int)(int16_t)(w.y & 0xFFFFu),
-                      (int)(int16_t)(w.y >> 16)};
+    const int v[4] = {(int)(w.x & 0xFFFFu), (int)(w.x >> 16), (int)(w.y & 0xFFFFu), (int)(w.y >> 16)};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? v[k] : INT_MAX;
+    for (int k = 0; k < 4; ++k) y[k] = (FULL || g0 + k < K) ? v[k] : INT_MAX;
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = g0 + k < K ? (int)__ldg(yr + g0 + k) : INT_MAX;
+    for (int k = 0; k < 4; ++k) y[k] = (FULL || g0 + k < K) ? (int)__ldg(yr + g0 + k) : INT_MAX;
   }
-  const uint32_t hw = g0 < K ? head[g0 >> 5] : 0u;
+  const uint32_t hw = (FULL || g0 < K) ? head[g0 >> 5] : 0u;
   h = (hw >> (g0 & 31)) & 0xFu;
-  // genes past the end are their own segments (never merge into valid ones)
-  const int valid = K - g0;
-  if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
+  if (!FULL) {
+    // genes past the end are their own segments (never merge into valid ones)
+    const int valid = K - g0;
+    if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
+  }
 }
 
 __device__ __forceinline__ void load_xquad(const int8_t *xr, int K, int g0, uint32_t &xw) {
@@ -165,7 +175,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // with two TMA bulk copies (one elected lane, per-warp mbarrier) instead of
 // per-lane global loads; pass A then reads y from shared memory and writes
 // the prefix minima over it in place.
-template <bool BULK>
+template <bool BULK, int SCAN>
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
@@ -214,9 +224,8 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
                      "l"(xr), "r"(xb), "r"(bar)
                      : "memory");
       }
-      // hist/start are indexed by u = K - pm (descending prefix minimum), with
-      // a dummy slot u = K for genes past the end (no branches around atomics)
-      for (int i = lane; i < ((K + 2 + 127) >> 7) << 6; i += 32) hist[i] = 0u;
+      // hist/start are indexed by u = K - pm (descending prefix minimum)
+      for (int i = lane; i < ((K + 255) >> 8) << 7; i += 32) hist[i] = 0u;
       __syncwarp();
       if (BULK) {
         while (!mbar_try(bar, phase)) {
@@ -234,12 +243,13 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         load_quad<false>(yr, headS, K, 4 * lane, yq, hq);
         load_xquad(xr, K, 4 * lane, xq);
       }
-      for (int t = 0; t < NT; ++t) {
+      auto tileA = [&](const int t, auto fullc) {
+        constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
         uint32_t h;
         if (BULK) {
-          load_quad<true>((const int16_t *)pmv, headS, K, g0, y, h);
+          load_quad<true, FT>((const int16_t *)pmv, headS, K, g0, y, h);
         } else {
           h = hq;
 #pragma unroll
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
             load_xquad(xr, K, g0 + 128, xq);
           }
         }
-        pm_quad(y, h, carry, lane, pm);
+        pm_quad<SCAN>(y, h, carry, lane, pm);
         // leaders = new prefix minima (pm == y); each distinct pm is one run
         // (a leader and the non-leaders after it in its job), and a run's
         // length is stored once, by its leader, at u = K - pm: hist[u] = len
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
-          const bool ok = g0 + k < K && v < (unsigned)K;
+          const bool ok = FT || (g0 + k < K && v < (unsigned)K);
           const unsigned u = ok ? (unsigned)K - 1u - v : (unsigned)K;
           const bool ld = ok && pm[k] == y[k];
           lm |= (ld ? 1u : 0u) << k;
@@ -290,31 +300,44 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
             nx = g0 + k;
           }
         carry = __shfl_sync(FULL, pm[3], 31);
-      }
+      };
+      for (int t = 0; t + 1 < NT; ++t) tileA(t, std::true_type{});
+      tileA(NT - 1, std::false_type{});
       if (open_u >= 0 && lane == 0) h16[open_u] = (uint16_t)(K - open_pos);
       __syncwarp();
-      // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u)
+      // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u),
+      // 8 counts per lane per step (entries >= K are written but never read)
       uint32_t acc = 0;
-      for (int t = 0; t < NT; ++t) {
-        const int u0 = (t << 7) + 4 * lane;
-        const uint2 w = *(const uint2 *)(h16 + u0);   // u0 % 4 == 0: 8-byte aligned
-        const uint32_t c0 = w.x & 0xFFFFu, c1 = w.x >> 16, c2 = w.y & 0xFFFFu, c3 = w.y >> 16;
-        const uint32_t sum = c0 + c1 + c2 + c3;
+      for (int ub = 0; ub < K; ub += 256) {   // warp-uniform trip count (shuffles inside)
+        const int u0 = ub + 8 * lane;
+        const uint4 w = *(const uint4 *)(h16 + u0);   // u0 % 8 == 0: 16-byte aligned
+        const uint32_t p0 = w.x + (w.x << 16);        // pairwise inclusive sums in the high halves
+        const uint32_t p1 = w.y + (w.y << 16), p2 = w.z + (w.z << 16), p3 = w.w + (w.w << 16);
+        const uint32_t s01 = (p0 >> 16) + (p1 >> 16), s012 = s01 + (p2 >> 16);
+        const uint32_t sum = s012 + (p3 >> 16);
         uint32_t incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const uint32_t n = __shfl_up_sync(FULL, incl, d);
           if (lane >= d) incl += n;
         }
-        const uint32_t s0 = acc + incl - sum, s1 = s0 + c0, s2 = s1 + c1, s3 = s2 + c2;
-        if (u0 < K) *(uint2 *)(h16 + u0) = make_uint2(s0 | (s1 << 16), s2 | (s3 << 16));
+        const uint32_t e0 = acc + incl - sum;         // exclusive start of the lane's 8 counts
+        const uint32_t e1 = e0 + (p0 >> 16), e2 = e0 + s01, e3 = e0 + s012;
+        // start of count 2i = e_i, of count 2i+1 = e_i + count 2i
+        uint4 o;
+        o.x = e0 | ((e0 + (w.x & 0xFFFFu)) << 16);
+        o.y = e1 | ((e1 + (w.y & 0xFFFFu)) << 16);
+        o.z = e2 | ((e2 + (w.z & 0xFFFFu)) << 16);
+        o.w = e3 | ((e3 + (w.w & 0xFFFFu)) << 16);
+        *(uint4 *)(h16 + u0) = o;
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
       // ---- pass D: a leader at g ranks start[u(g)]; the genes after it in its
       // run follow consecutively: rank(g) = base + g with base = start - g_leader
       int carry_b = 0;
-      for (int t = 0; t < NT; ++t) {
+      auto tileD = [&](const int t, auto fullc) {
+        constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
         const int g0 = (t << 7) + 4 * lane;
         const uint2 w = *(const uint2 *)(pmv + g0);
         const uint32_t pk[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
@@ -338,10 +361,12 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
           if ((lm >> k) & 1u) base = bk[k];
-          if (g < K) ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
+          if (FT || g < K) ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
         }
         if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
-      }
+      };
+      for (int t = 0; t + 1 < NT; ++t) tileD(t, std::true_type{});
+      tileD(NT - 1, std::false_type{});
     }
     __syncthreads();
     // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome cc
@@ -1040,9 +1065,26 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     FFS_CUDA(cudaMalloc(&scr.ordg, (size_t)elems * 2));
     scr.ordg_elems = elems;
   }
-  static size_t a_ord = 0, a_ord_v = 0;
-  ffs_status e = smem_attr(order_warp_kernel<false>, st.ord_smem, a_ord);
-  if (e == FFS_OK) e = smem_attr(order_warp_kernel<true>, st.ord_smem, a_ord_v);
+  // the segmented min-scan's doubling steps: 2^SCAN > lanes a job's pending
+  // genes can span - 1 (pm_quad)
+  const int span = (st.max_pending + 2) / 4 + 1;
+  const int scan = span <= 4 ? 2 : span <= 8 ? 3 : 5;
+  void (*okern)(OrdArgs) = nullptr, (*okern_v)(OrdArgs) = nullptr;
+  static size_t attr_o[6] = {0, 0, 0, 0, 0, 0};
+  ffs_status e = FFS_OK;
+  if (scan == 2) {
+    okern = order_warp_kernel<false, 2>; okern_v = order_warp_kernel<true, 2>;
+    e = smem_attr(okern, st.ord_smem, attr_o[0]);
+    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[1]);
+  } else if (scan == 3) {
+    okern = order_warp_kernel<false, 3>; okern_v = order_warp_kernel<true, 3>;
+    e = smem_attr(okern, st.ord_smem, attr_o[2]);
+    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[3]);
+  } else {
+    okern = order_warp_kernel<false, 5>; okern_v = order_warp_kernel<true, 5>;
+    e = smem_attr(okern, st.ord_smem, attr_o[4]);
+    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[5]);
+  }
   if (e != FFS_OK) return e;
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
@@ -1077,10 +1119,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
-    if (oa.vec)
-      order_warp_kernel<true><<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
-    else
-      order_warp_kernel<false><<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
+    (oa.vec ? okern_v : okern)<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
     FFS_CUDA(cudaGetLastError());
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);
