@@ -857,16 +857,17 @@ __device__ __forceinline__ int search2(const Op2 &A, int t0, uint32_t bb_base, i
 // ticks of the 8-bit mask m (each has headroom >= 1): plane b flips where m
 // and every lower plane is 0 (borrow chain), i.e. under m & AND_{b'<b} ~h_b'.
 __device__ __forceinline__ uint32_t dec8(uint32_t W, uint32_t mrep) {   // mrep: mask in all four bytes
-  const uint32_t E = ~(W << 8) | 0xFFu;                  // byte b: ~h_{b-1}; byte 0: ones
-  const uint32_t E1 = E & ((E << 8) | 0xFFu);
-  const uint32_t E2 = E1 & ((E1 << 16) | 0xFFFFu);      // byte b: AND_{b'<b} ~h_b'
-  return W ^ (mrep & E2);
+  // byte b of W<<8, W<<16, W<<24 holds planes b-1, b-2, b-3 (zero-filled), so
+  // ~(W<<8 | W<<16 | W<<24) is AND_{b'<b} ~h_b' in byte b; the shifts are
+  // multiplies (fma pipe)
+  const uint32_t lower = (W * 0x100u) | (W * 0x10000u) | (W * 0x1000000u);
+  return W ^ (mrep & ~lower);
 }
-// blocked flags of the group (headroom 0 <=> every plane 0), tick i at bit 7 - i
-__device__ __forceinline__ uint32_t blk8(uint32_t W) {
-  uint32_t x = W | (W >> 16);
-  x |= x >> 8;
-  return ~x;
+// blocked flags (headroom 0 <=> every plane 0) of two groups, tick i at bit
+// 7 - i: group N0 in byte 0, group N1 in byte 2
+__device__ __forceinline__ uint32_t blk2(uint32_t N0, uint32_t N1) {
+  const uint32_t z = __byte_perm(N0, N1, 0x5410) | __byte_perm(N0, N1, 0x7632);   // planes 0|2, 1|3
+  return ~(z | (z >> 8));
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -983,8 +984,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
         sts(pa, N0);
         sts(pa + 128, N1);
         const uint32_t ba = bb_base + ((w >> 2) << 7) + (~w & 3u);
-        sts8(ba, blk8(N0));
-        sts8((w & 3u) == 3u ? ba + 131u : ba - 1u, blk8(N1));
+        const uint32_t bk = blk2(N0, N1);
+        sts8(ba, bk);
+        sts8((w & 3u) == 3u ? ba + 131u : ba - 1u, bk >> 16);
       }
       if (SCHED && active) srow[A.e / h.O] = Sx + h.rs;
       // stage A of op r+2 (ranks >= K carry the padding index 0: harmless)
