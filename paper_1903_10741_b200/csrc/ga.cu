@@ -463,15 +463,19 @@ __device__ __forceinline__ uint4 mutate16(uint4 v, int g0, uint32_t cell, uint32
   return v;
 }
 
-__global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
+__global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, nwd = (K + 31) >> 5;
-  const size_t per_warp = (size_t)2 * nwd * 4 + (size_t)2 * ((K * 2 + 15) & ~15);
+  const int fmb = (K + 1 + 15) & ~15;   // byte maps indexed by value 0..K (slot 0: padding genes)
+  const size_t pbm = ((size_t)2 * nwd * 4 + 15) & ~(size_t)15;   // both bit maps, 16-B multiple
+  const size_t per_warp = pbm + (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * fmb;
   uint32_t *PA = (uint32_t *)(gsm + warp * per_warp);
   uint32_t *PB = PA + nwd;
-  uint16_t *LA = (uint16_t *)(PB + nwd);
+  uint16_t *LA = (uint16_t *)((unsigned char *)PA + pbm);
   uint16_t *LB = LA + ((K * 2 + 15) & ~15) / 2;
+  uint8_t *FA = (uint8_t *)(LB + ((K * 2 + 15) & ~15) / 2);   // FA[v] = 1 iff v is in A's prefix
+  uint8_t *FB = FA + fmb;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int half = a.tile >> 1, wh = a.w >> 1;
@@ -514,17 +518,23 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
       // whose value occurs in A's prefix; missing values = in B's prefix, not
       // in A's prefix; assigned in ascending order to duplicates in gene order.
       for (int i = lane; i < nwd; i += 32) { PA[i] = 0u; PB[i] = 0u; }
+      for (int i = lane; i < (fmb >> 4); i += 32) {
+        ((uint4 *)FA)[i] = make_uint4(0, 0, 0, 0);
+        ((uint4 *)FB)[i] = make_uint4(0, 0, 0, 0);
+      }
       __syncwarp();
       for (int i = lane; i < ((kc + 7) >> 3); i += 32) {
         const uint4 va = YA[i], vb = YB[i];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (8 * i + j < kc) {
+          if (8 * i + j < kc) {   // prefix genes: values in [1, K]
             const int sh = 16 * (j & 1);
-            const int ta = (int)((wsel(va, j >> 1) >> sh) & 0xFFFFu) - 1;
-            const int tb = (int)((wsel(vb, j >> 1) >> sh) & 0xFFFFu) - 1;
-            if ((unsigned)ta < (unsigned)K) atomicOr(&PA[ta >> 5], 1u << (ta & 31));
-            if ((unsigned)tb < (unsigned)K) atomicOr(&PB[tb >> 5], 1u << (tb & 31));
+            const int va1 = (int)((wsel(va, j >> 1) >> sh) & 0xFFFFu), vb1 = (int)((wsel(vb, j >> 1) >> sh) & 0xFFFFu);
+            const int ta = va1 - 1, tb = vb1 - 1;
+            atomicOr(&PA[ta >> 5], 1u << (ta & 31));
+            atomicOr(&PB[tb >> 5], 1u << (tb & 31));
+            FA[va1] = 1;
+            FB[vb1] = 1;
           }
         }
       }
@@ -582,18 +592,21 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
         wset(zb, k, (wb_ & m) | (wa_ & ~m));
       }
       if (repair) {
+        // duplicates: suffix genes (kc <= g < K) whose value is in the own
+        // parent's prefix -- one byte-map load per gene, no bit arithmetic
+        // (padding genes hold value 0, slot 0 of the maps)
+        const int lo = min(max(kc - 8 * i, 0), 8), hi = min(max(K - 8 * i, 0), 8);
+        const uint32_t sfx = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
         uint32_t fa = 0, fb = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int g = 8 * i + j;
-          if (g >= kc && g < K) {
-            const int sh = 16 * (j & 1);
-            const int ta = (int)((wsel(za, j >> 1) >> sh) & 0xFFFFu) - 1;
-            const int tb = (int)((wsel(zb, j >> 1) >> sh) & 0xFFFFu) - 1;
-            if ((unsigned)ta < (unsigned)K && ((PA[ta >> 5] >> (ta & 31)) & 1u)) fa |= 1u << j;
-            if ((unsigned)tb < (unsigned)K && ((PB[tb >> 5] >> (tb & 31)) & 1u)) fb |= 1u << j;
-          }
+          const int sh = 16 * (j & 1);
+          const uint32_t ta = (wsel(za, j >> 1) >> sh) & 0xFFFFu, tb = (wsel(zb, j >> 1) >> sh) & 0xFFFFu;
+          fa += (uint32_t)FA[ta] << j;
+          fb += (uint32_t)FB[tb] << j;
         }
+        fa &= sfx;
+        fb &= sfx;
         const int na = __popc(fa), nb = __popc(fb);
         int ia = na | (nb << 16);
 #pragma unroll
@@ -606,10 +619,10 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
         da += tot & 0xFFFF;
         db += tot >> 16;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int sh = 16 * (j & 1);
-          if ((fa >> j) & 1u) wset(za, j >> 1, (wsel(za, j >> 1) & ~(0xFFFFu << sh)) | ((uint32_t)LA[ra++] << sh));
-          if ((fb >> j) & 1u) wset(zb, j >> 1, (wsel(zb, j >> 1) & ~(0xFFFFu << sh)) | ((uint32_t)LB[rb++] << sh));
+        for (int j = 0; j < 8; ++j) {   // half j&1 of word j/2 <- next missing value (byte permute)
+          const uint32_t sel = (j & 1) ? 0x5410u : 0x3254u;
+          if ((fa >> j) & 1u) wset(za, j >> 1, __byte_perm(wsel(za, j >> 1), (uint32_t)LA[ra++], sel));
+          if ((fb >> j) & 1u) wset(zb, j >> 1, __byte_perm(wsel(zb, j >> 1), (uint32_t)LB[rb++], sel));
         }
       }
       if (i < nyv) {
@@ -638,7 +651,7 @@ __global__ void __launch_bounds__(256) generation_kernel(GenArgs a) {
 
 size_t gen_smem_per_warp(int K) {
   int nwd = (K + 31) >> 5;
-  return (size_t)2 * nwd * 4 + (size_t)2 * ((K * 2 + 15) & ~15);
+  return (((size_t)2 * nwd * 4 + 15) & ~(size_t)15) + (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * ((K + 1 + 15) & ~15);
 }
 
 }  // namespace
