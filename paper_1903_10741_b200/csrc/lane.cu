@@ -52,6 +52,20 @@ __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
 [[maybe_unused]] __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
+// predicated shared u16 store / load (no branch, no reconvergence barrier)
+__device__ __forceinline__ void sts16_if(bool p, const void *a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u16 [%0], %1;\n}\n" ::"r"(smem_u32(a)),
+               "h"((unsigned short)v), "r"((uint32_t)p)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t lds16_if(bool p, const void *a) {
+  unsigned short v = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}\n"
+               : "+h"(v)
+               : "r"(smem_u32(a)), "r"((uint32_t)p)
+               : "memory");
+  return v;
+}
 // lane-interleaved u16 element v: word v/2, half v%2
 [[maybe_unused]] __device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
   return base + ((v >> 1) << 7) + ((v & 1u) << 1);
@@ -264,7 +278,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         // leaders = new prefix minima (pm == y); each distinct pm is one run
         // (a leader and the non-leaders after it in its job), and a run's
         // length is stored once, by its leader, at u = K - pm: hist[u] = len
-        uint32_t pk[4], lm = 0;
+        uint32_t pk[4], lm = 0, lu = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
@@ -273,6 +287,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const bool ld = ok && pm[k] == y[k];
           lm |= (ld ? 1u : 0u) << k;
           pk[k] = u | (ld ? 0x8000u : 0u);
+          lu = ld ? u : lu;   // the lane's last leader
         }
         *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
         // next leader after each of the lane's leaders: inside the quad, else
@@ -285,20 +300,18 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         if (B) {
           const int fl = __ffs(B) - 1;
           const int first = __shfl_sync(FULL, fpos, fl);
-          if (open_u >= 0 && lane == fl) h16[open_u] = (uint16_t)(first - open_pos);
+          sts16_if(open_u >= 0 && lane == fl, h16 + open_u, (uint32_t)(first - open_pos));
           const int ll = 31 - __clz(B);
-          const int kl = 31 - __clz(lm | 1u);
-          const int lpos = __shfl_sync(FULL, g0 + kl, ll);
-          open_u = __shfl_sync(FULL, (int)((kl == 0 ? pk[0] : kl == 1 ? pk[1] : kl == 2 ? pk[2] : pk[3]) & 0x7FFFu), ll);
-          open_pos = lpos;
+          open_pos = __shfl_sync(FULL, g0 + 31 - __clz(lm | 1u), ll);
+          open_u = __shfl_sync(FULL, (int)lu, ll);
         }
         int nx = hiB ? nxl : -1;
 #pragma unroll
-        for (int k = 3; k >= 0; --k)
-          if ((lm >> k) & 1u) {
-            if (nx >= 0) h16[pk[k] & 0x7FFFu] = (uint16_t)(nx - (g0 + k));
-            nx = g0 + k;
-          }
+        for (int k = 3; k >= 0; --k) {
+          const bool ldk = (lm >> k) & 1u;
+          sts16_if(ldk && nx >= 0, h16 + (pk[k] & 0x7FFFu), (uint32_t)(nx - (g0 + k)));
+          nx = ldk ? g0 + k : nx;
+        }
         carry = __shfl_sync(FULL, pm[3], 31);
       };
       for (int t = 0; t + 1 < NT; ++t) tileA(t, std::true_type{});
@@ -344,13 +357,11 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         int bk[4], lastb = 0;
         uint32_t lm = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          bk[k] = 0;
-          if (pk[k] & 0x8000u) {   // leaders only: padding genes carry u = K, no flag
-            bk[k] = (int)h16[pk[k] & 0x7FFFu] - (g0 + k);
-            lastb = bk[k];
-            lm |= 1u << k;
-          }
+        for (int k = 0; k < 4; ++k) {   // leaders only: padding genes carry u = K, no flag
+          const bool ldk = (pk[k] & 0x8000u) != 0u;
+          bk[k] = (int)lds16_if(ldk, h16 + (pk[k] & 0x7FFFu)) - (g0 + k);
+          lastb = ldk ? bk[k] : lastb;
+          lm |= (ldk ? 1u : 0u) << k;
         }
         const uint32_t B = __ballot_sync(FULL, lm != 0u);
         const uint32_t lb = B & ((1u << lane) - 1u);
@@ -360,8 +371,11 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
-          if ((lm >> k) & 1u) base = bk[k];
-          if (FT || g < K) ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
+          base = ((lm >> k) & 1u) ? bk[k] : base;
+          if (FT)
+            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
+          else
+            sts16_if(g < K, ord + base + g, gtab[tb + 32 * k] + (uint32_t)xs[g]);
         }
         if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
       };
