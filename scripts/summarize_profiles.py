@@ -62,6 +62,8 @@ if os.path.exists(lc) and '"ID"' in open(lc).read():
         # run.best() after the timed steps decodes one chromosome with its schedule
         # (lane_decode_kernel<., 1>, preceded by its order kernel): not a step
         def is_sched(nm):
+            if nm.startswith("lane_decode2_kernel"):
+                return nm.endswith("<1>")
             if nm.startswith("lane_decode_kernel"):
                 return nm.endswith(", 1>")
             if nm.startswith("evaluate_kernel"):

@@ -199,3 +199,29 @@ def test_full_size_sampled_parity(path):
     # every chromosome is a valid permutation (device generator property)
     ysort = torch.sort(y.to(torch.int32), dim=1).values
     assert bool((ysort == torch.arange(1, st.K + 1, device=y.device, dtype=torch.int32)).all())
+
+
+@pytest.mark.parametrize("g,n,o,q_max", [(16, 12, 3, 5), (40, 5, 2, 4), (70, 3, 2, 3)])
+def test_long_jobs(g, n, o, q_max, path):
+    """Jobs with up to G pending genes span more lanes of the order kernel's
+    tiles: G = 16 and 40 take the 3- and 5-step segmented min-scans (G <= 13
+    takes 2), G = 70 lets one job cover a whole 128-gene tile boundary."""
+    wl = wlmod.gen_v1(f"G{g}", n, g, o, q_max, arrivals_per_event=[2], ratios=[0.3], seed=g)
+    octx, st, arr = both_event_ctx(wl)
+    check_gene_order(octx, st)
+    x, y = wlmod.random_chromosomes(300, st.K, wl.o, seed=13)
+    compare(octx, st, x, y, n_sched=20)
+
+
+@pytest.mark.parametrize("n,g", [(16, 8), (32, 8), (43, 6), (16, 16), (65, 4)])
+def test_tile_boundary_K(n, g, path):
+    """Static problems (RS = 0, K = n g) with K = 128, 256, 258, 256, 260:
+    full and partial 128-gene tiles, 256-entry prefix-sum steps and the last
+    quad of ranks."""
+    wl = wlmod.gen_v1(f"K{n * g}", n, g, 3, 6, seed=n + g)
+    a = wl.original_instance()
+    octx = orc.Ctx(fx.workload_instance(a), 0)
+    st = gpu_state(a, 0)
+    assert st.K == n * g
+    x, y = wlmod.random_chromosomes(200, st.K, 3, seed=17)
+    compare(octx, st, x, y, n_sched=20)

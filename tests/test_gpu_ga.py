@@ -126,3 +126,19 @@ def test_two_shard_run_equals_single_gpu_run():
     tmin = np.minimum(out[0][1]["trace_min"], out[1][1]["trace_min"])
     assert (tmin == ref_best["trace_min"]).all()
     assert (out[0][1]["trace_sum"] + out[1][1]["trace_sum"] == ref_best["trace_sum"]).all()
+
+
+def test_trajectory_parity_long_jobs():
+    """GA trajectory with G = 16 (3-step min-scan in the order kernel) and a
+    row length that is not a multiple of the crossover's 8-gene words."""
+    from paper_1903_10741_b200 import workload as wlmod
+    wl = wlmod.gen_v1("G16ga", 9, 16, 3, 5, arrivals_per_event=[2], ratios=[0.3], seed=16)
+    octx, st, _ = both_event_ctx(wl)
+    G = 12
+    run = ffs.Run(st, 4, 4, 4, G, 4242)
+    run.step(G)
+    ga = orc.GA(octx, 4, 4, 4, G, 4242)
+    for _ in range(G + 1):
+        ga.step()
+    for u, v in zip(run.population(), ga.population()):
+        assert (u == v).all()
