@@ -487,7 +487,10 @@ def run_ours(args):
                            "note": "algorithmic ops (oracle-counted dispatches + power checks + delay jumps + "
                                    "profile updates per evaluation) / evaluate-kernel time, against the issue "
                                    "rate 148 SM x 4 SMSP x 1.965 GHz (one warp-instruction per op)",
-                           "kernel": "evaluate launch (order_warp_kernel + lane_decode_kernel)", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
+                           "pipes": "measured on B200 (scripts/micro/pipes.cu): LOP3/SHF/PRMT/IMNMX issue 2 "
+                                    "warp-instr/clk/SM on the alu pipe, IMAD 2 on the fma pipe; ncu: the decode "
+                                    "kernel keeps the alu pipe ~67% busy",
+                           "kernel": "evaluate launch (order_warp_kernel + lane_decode2_kernel)", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
         out["e2e"] = {"value": e2e_value, "unit": "evals/s",
                       "h2d_bytes_per_step": int(pop_local * K * 3),
                       "d2h_bytes_per_step": int(pop_local * (8 + 8 + 4)),
