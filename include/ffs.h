@@ -166,7 +166,10 @@ FFS_API ffs_status ffs_evaluate(const ffs_state *st, int64_t count, const int8_t
                         int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                         int32_t *start_out, void *cuda_stream);
 /* Same with HOST buffers (pageable or pinned): copies in, evaluates, copies
- * out, synchronises.  Used for end-to-end timing. */
+ * out, synchronises.  Ordered after earlier work on cuda_stream.  Large
+ * batches run as a pipeline of up to 4 chunks on two internal streams (chunk
+ * i's host->device copy overlaps chunk i-1's decode and result copy-out);
+ * results are identical to ffs_evaluate.  Used for end-to-end timing. */
 FFS_API ffs_status ffs_evaluate_host(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
                              int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                              void *cuda_stream);

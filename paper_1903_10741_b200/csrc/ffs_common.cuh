@@ -95,10 +95,19 @@ struct HostStage {
   int32_t *M = nullptr;
   int64_t cap = 0;
   size_t gene_cap = 0;
+  cudaStream_t copy = nullptr, comp = nullptr;   // H2D stream, compute + D2H stream
+  cudaEvent_t ev[9] = {};                         // [0..7] chunk uploaded, [8] entry / exit
   void release() {
     cudaFree(x); cudaFree(y); cudaFree(obj); cudaFree(T); cudaFree(M);
     x = nullptr; y = nullptr; obj = nullptr; T = nullptr; M = nullptr;
     cap = 0; gene_cap = 0;
+  }
+  void release_streams() {
+    for (cudaEvent_t &e : ev)
+      if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (copy) cudaStreamDestroy(copy);
+    if (comp) cudaStreamDestroy(comp);
+    copy = comp = nullptr;
   }
 };
 

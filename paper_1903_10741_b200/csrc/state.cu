@@ -557,6 +557,7 @@ void ffs_state_destroy(ffs_state *h) {
   if (st.gbase_dev) cudaFree(st.gbase_dev);
   st.scratch.release();
   st.stage.release();
+  st.stage.release_streams();
   delete h;
 }
 
@@ -600,16 +601,40 @@ ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x,
     hs.cap = (int64_t)c;
     hs.gene_cap = g;
   }
-  if (gb) {
-    FFS_CUDA(cudaMemcpyAsync(hs.x, x, gb, cudaMemcpyHostToDevice, s));
-    FFS_CUDA(cudaMemcpyAsync(hs.y, y, gb * 2, cudaMemcpyHostToDevice, s));
+  if (!hs.copy) {
+    FFS_CUDA(cudaStreamCreateWithFlags(&hs.copy, cudaStreamNonBlocking));
+    FFS_CUDA(cudaStreamCreateWithFlags(&hs.comp, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : hs.ev) FFS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  ffs_status rc = ffs_evaluate(h, count, hs.x, hs.y, hs.obj, hs.T, hs.M, nullptr, stream);
-  if (rc != FFS_OK) return rc;
-  if (objective) FFS_CUDA(cudaMemcpyAsync(objective, hs.obj, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
-  if (total_tardiness) FFS_CUDA(cudaMemcpyAsync(total_tardiness, hs.T, (size_t)count * 8, cudaMemcpyDeviceToHost, s));
-  if (makespan) FFS_CUDA(cudaMemcpyAsync(makespan, hs.M, (size_t)count * 4, cudaMemcpyDeviceToHost, s));
-  FFS_CUDA(cudaStreamSynchronize(s));
+  // Chunked pipeline: chunk i's host->device copy (copy stream) overlaps chunk
+  // i-1's decode and its results' device->host copy (compute stream); the
+  // call is ordered after earlier work on `stream` and synchronous on return.
+  const int K = st.K;
+  const int nch = count >= 4 * 8192 ? 4 : (count >= 2 * 8192 ? 2 : 1);
+  FFS_CUDA(cudaEventRecord(hs.ev[8], s));
+  FFS_CUDA(cudaStreamWaitEvent(hs.copy, hs.ev[8], 0));
+  FFS_CUDA(cudaStreamWaitEvent(hs.comp, hs.ev[8], 0));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t a0 = count * c / nch, n = count * (c + 1) / nch - a0;
+    const size_t g0 = (size_t)a0 * K, gn = (size_t)n * K;
+    if (gn) {
+      FFS_CUDA(cudaMemcpyAsync(hs.x + g0, x + g0, gn, cudaMemcpyHostToDevice, hs.copy));
+      FFS_CUDA(cudaMemcpyAsync(hs.y + g0, y + g0, gn * 2, cudaMemcpyHostToDevice, hs.copy));
+    }
+    FFS_CUDA(cudaEventRecord(hs.ev[c], hs.copy));
+    FFS_CUDA(cudaStreamWaitEvent(hs.comp, hs.ev[c], 0));
+    ffs_status rc = ffs_evaluate(h, n, hs.x + g0, hs.y + g0, hs.obj + a0, hs.T + a0, hs.M + a0, nullptr, hs.comp);
+    if (rc != FFS_OK) return rc;
+    if (objective)
+      FFS_CUDA(cudaMemcpyAsync(objective + a0, hs.obj + a0, (size_t)n * 8, cudaMemcpyDeviceToHost, hs.comp));
+    if (total_tardiness)
+      FFS_CUDA(cudaMemcpyAsync(total_tardiness + a0, hs.T + a0, (size_t)n * 8, cudaMemcpyDeviceToHost, hs.comp));
+    if (makespan)
+      FFS_CUDA(cudaMemcpyAsync(makespan + a0, hs.M + a0, (size_t)n * 4, cudaMemcpyDeviceToHost, hs.comp));
+  }
+  FFS_CUDA(cudaEventRecord(hs.ev[8], hs.comp));
+  FFS_CUDA(cudaStreamWaitEvent(s, hs.ev[8], 0));
+  FFS_CUDA(cudaStreamSynchronize(hs.comp));
   return FFS_OK;
 }
 
