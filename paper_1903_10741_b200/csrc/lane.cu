@@ -1,11 +1,8 @@
-// lane.cu -- the fast evaluate path: ONE LANE PER CHROMOSOME, 32 chromosomes
-// per warp, for Algorithm 1 (order_lane_kernel) and Algorithm 2
-// (lane_decode_kernel).
-//
-// Why: both algorithms are dependent chains per chromosome whose per-step
-// work is scalar.  With a warp per chromosome 31 lanes duplicate that work
-// (measured: 96 warp instructions per dispatched op, 87% issue-active).  Here
-// one warp instruction advances 32 chromosomes.
+// lane.cu -- the fast evaluate path.  Algorithm 1 (order_warp_kernel): ONE
+// WARP per chromosome (the sort is parallel work); Algorithm 2 (the decode
+// kernels): ONE LANE per chromosome, 32 chromosomes per warp (its per-op work
+// is a scalar dependent chain; with a warp per chromosome 31 lanes duplicated
+// it: 96 warp instructions per dispatched op at 87% issue).
 //
 // Layouts
 //   per-thread arrays live in shared memory LANE-INTERLEAVED: 32-bit word w of
@@ -13,20 +10,22 @@
 //   ordg (global) [tile][ceil(K/4)][32 lanes][4] u16: P/Q-table index of the op
 //   at each rank (4 ranks per lane per 8-byte load, 256 B per warp, coalesced).
 // Algorithm 1 (greedy reading R1) = stable sort by (prefix-min of y
-// over the job's pending stages desc, stage asc): per lane a sequential pass
-// marks runs ("leaders" = new prefix minima) and writes each run length at its
-// leader's priority, a suffix sum over priorities gives run starts, and a
-// second pass scatters every gene to start + offset.
-// Algorithm 2 (R2, R5): per lane state
+// over the job's pending stages desc, stage asc): a counting sort by the
+// prefix minimum -- see order_warp_kernel.
+// Algorithm 2 (R2, R5):
+//   lane_decode2_kernel  every Q == 1, Q_max <= 15 (the paper's Table 5
+//     setting): 10-bit job / machine times, headroom Q_max - Q_t as bit planes
+//     in 8-tick groups, blocked bits, software-pipelined dispatches (below)
+//   lane_decode_kernel (modes 0/1) otherwise: per lane
 //     ready[j]  u16 pairs  earliest start of job j's next op (rel. to RS)
 //     mfree[m]  u16 pairs  machine free time (append-only sequencing, R6)
 //     level[t]  u8 x4      Q_t per tick + bias, bias = 0x7F - (Q_max - min Q):
 //                          bit 7 of a byte  <=>  Q_t > Q_max - min Q
 //     blocked   1 bit/tick copy of those bits: no op fits at that tick
 //   The earliest t >= t0 with p un-blocked ticks is found on a 32-tick window
-//   of `blocked` (run test by shifts/ands); ops with q > min Q verify the bytes.
-//   Commit adds q to p bytes (byte SIMD, no carries since Q_max <= 127) and
-//   ORs their bit-7 flags into `blocked`.
+//   of `blocked` (run test by shifts/ands); ops with q > min Q verify the
+//   bytes.  Commit adds q to p bytes (byte SIMD, no carries since Q_max <=
+//   127) and ORs their bit-7 flags into `blocked`.
 #include <type_traits>
 
 #include "device_util.cuh"
@@ -448,44 +447,16 @@ __device__ __noinline__ int lane_search(const LaneCtx L, int t, int p, int dq, u
 // one op ahead): table fields, ready/machine word addresses, and the masks of
 // the branch-free run test for this p (1 <= p <= 8).
 struct OpA {
-  uint32_t e, ra, ma, QQ, M1, M2, M4, nmo;
+  uint32_t e, ra, ma, QQ, M1, M2, M4;
   int p, q, rsh, msh, sft;
 };
 // keep a staged value in a register (no rematerialisation on the critical path)
 __device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
 __device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
-template <bool NIB>
-__device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, uint32_t mbase, uint32_t pt_base,
-                                       int GO, uint32_t e) {
+__device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
   OpA A;
   const uint32_t tv = pqt[e];
   A.e = e;
-  if (NIB) {
-    // host-packed (mode 2): rsh[0:5] | msh[5:10] | ready word[10:21] |
-    // machine word[21:29] | p-1[29:32].  The field shifts are used by wrap
-    // (mod 32) funnel shifts, so they need no extraction; the p-dependent
-    // run-test shifts and the nibble-mask column come from ptab[p-1].
-    const uint32_t pm1 = tv >> 29;
-    A.p = (int)pm1 + 1;
-    A.q = 1;
-    A.rsh = (int)tv;
-    A.msh = (int)(tv >> 5);
-    A.ra = L.base + ((tv >> 3) & 0x3FF80u);
-    A.ma = mbase + ((tv >> 14) & 0x7F80u);
-    uint4 pt;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(pt.x), "=r"(pt.y), "=r"(pt.z), "=r"(pt.w)
-                 : "r"(pt_base + (pm1 << 4)));
-    A.M1 = pt.x;
-    A.M2 = pt.y;
-    A.M4 = pt.z;
-    A.nmo = pt.w;                               // (1 << p) - 1
-    A.sft = 0;
-    A.QQ = 0x01010101u;
-    pin(A.ra); pin(A.ma); pin(A.rsh); pin(A.msh); pin(A.M1); pin(A.M2); pin(A.M4); pin(A.p);
-    pin(A.nmo);
-    return A;
-  }
   A.p = (int)(tv & 0xFFu);
   A.q = (int)((tv >> 8) & 0xFFu);
   const int j = (int)(tv >> 16);
@@ -500,44 +471,23 @@ __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, ui
   A.M2 = (uint32_t)((pp - 4) >> 31);
   A.M4 = (uint32_t)((pp - 8) >> 31);
   A.sft = pp - (1 << (31 - __clz(pp)));
-  A.nmo = 0;
   return A;
 }
 
-// first run of p free ticks: mode 2 shifts by ptab's (a, b, c) with
-// runs(p) = ((f & f>>a) & ..>>b) & ..>>c; modes 0/1 use the doubling masks
-template <bool NIB>
+// first run of p free ticks: doubling masks (bit i set iff bits i..i+p-1 set)
 __device__ __forceinline__ uint32_t run_test(uint32_t f, const OpA &A) {
-  if (NIB) {
-    f &= __funnelshift_r(f, 0u, A.M1);
-    f &= __funnelshift_r(f, 0u, A.M2);
-    f &= __funnelshift_r(f, 0u, A.M4);
-    return f;
-  }
   f &= (f >> 1) | A.M1;
   f &= (f >> 2) | A.M2;
   f &= (f >> 4) | A.M4;
   return f & (f >> A.sft);
 }
-// field extraction / placement at a per-op shift (mode 2: wrap shifts of the
-// raw table word)
-template <bool NIB>
-__device__ __forceinline__ uint32_t field_at(uint32_t w, int sh) {
-  return NIB ? __funnelshift_r(w, 0u, (uint32_t)sh) : w >> sh;
-}
-template <bool NIB>
-__device__ __forceinline__ uint32_t place_at(uint32_t v, int sh) {
-  return NIB ? __funnelshift_l(0u, v, (uint32_t)sh) : v << sh;
-}
 
-// MODE 0: byte levels, general Q; MODE 1: byte levels, uniform Q;
-// MODE 2: HEADROOM Q_max - Q_t in four bit planes per 32 ticks (every Q_jsm
-//         == 1, Q_max <= 15): blocked <=> headroom == 0, commit subtracts 1
-//         per tick with a borrow chain across the planes.
+// MODE 0: byte levels, general Q; MODE 1: byte levels, uniform Q (every
+// Q == 1 with Q_max <= 15 is mode 2: lane_decode2_kernel below).
 template <int MODE, bool SCHED>
 __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t lane_wpt) {
+  static_assert(MODE == 0 || MODE == 1, "mode 2 has its own kernel");
   constexpr bool UQ = MODE != 0;
-  constexpr bool NIB = MODE == 2;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint4 cmask[32];    // byte masks of [S, S+p) over words S/4 .. S/4+2, by (S%4, p-1)
@@ -550,32 +500,20 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     m.w = 0u;
     cmask[threadIdx.x] = m;
   }
-  __shared__ uint4 ptab[8];      // mode 2, by p-1: run-test shifts (a, b, c), p-bit mask
-  if (NIB && threadIdx.x < 8) {
-    const int p = threadIdx.x + 1;
-    const uint32_t sa = p >= 2 ? 1u : 0u;
-    const uint32_t sb = p >= 4 ? 2u : (p == 3 ? 1u : 0u);
-    const uint32_t sc = p >= 5 ? (uint32_t)(p - 4) : 0u;
-    ptab[threadIdx.x] = make_uint4(sa, sb, sc, (1u << p) - 1u);
-  }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
-  uint32_t cm_base = smem_u32(cmask), pt_base = smem_u32(ptab);
+  uint32_t cm_base = smem_u32(cmask);
   pin(cm_base);
-  pin(pt_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
   const int K = h.K, KQ = (K + 3) >> 2, GO = h.G * h.O;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   LaneCtx L;
   L.base = smem_u32(smem + img_bytes + (size_t)warp * lane_wpt * 128) + lane * 4;
-  L.RW = NIB ? (h.NJ + 2) / 3 : (h.NJ + 1) >> 1;
-  L.MW = NIB ? (GO + 2) / 3 : (GO + 1) >> 1;
-  constexpr uint32_t TM = NIB ? 0x3FFu : 0xFFFFu;   // time field mask
+  L.RW = (h.NJ + 1) >> 1;
+  L.MW = (GO + 1) >> 1;
+  constexpr uint32_t TM = 0xFFFFu;   // time field mask (u16 pairs)
   L.hcap = a.h_cap;
-  // mode 2: per 32-tick word w, the four bit planes of the headroom
-  // Q_max - Q_t at LB + 4w .. 4w+3; blocked bits (headroom == 0) at BB + w as
-  // in modes 0/1, with the same two free sentinel words past the horizon
-  L.LW = NIB ? 4 * (a.h_cap >> 5) : a.h_cap >> 2;
+  L.LW = a.h_cap >> 2;
   L.BW = a.h_cap >> 5;
   const int LB = L.RW + L.MW, BB = LB + L.LW;
   const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
@@ -585,10 +523,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   const int qmin = h.q_max - h.thr_min, lvw0 = h.lvl_words0;
   const uint32_t bias4 = (uint32_t)(0x7F - h.thr_min) * 0x01010101u;
   int hcap = L.hcap, BW = L.BW;
-  uint32_t mbase = waddr(L, L.RW);
   pin(hcap);
   pin(BW);
-  pin(mbase);
   const int64_t ntile = (a.count + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
@@ -599,23 +535,11 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     // --- initial state: ready/machine times, profile of the RUNNING ops
     for (int w = 0; w < L.RW; ++w) sts(waddr(L, w), r16[w]);
     for (int w = 0; w < L.MW; ++w) sts(waddr(L, L.RW + w), m16[w]);
-    if (NIB) {
-      const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
-      const uint32_t qm = (uint32_t)h.q_max;
-      for (int tw = 0; tw < BW; ++tw) {
-        const bool init = 5 * tw < h.hn_words0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          sts(waddr(L, LB + 4 * tw + b), init ? pl0[5 * tw + b] : (((qm >> b) & 1u) ? 0xFFFFFFFFu : 0u));
-        sts(waddr(L, BB + tw), init ? pl0[5 * tw + 4] : 0u);
-      }
-    } else {
-      for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
-      for (int w = 0; w < BW; ++w) {
-        uint32_t bits = 0;
-        for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
-        sts(waddr(L, BB + w), bits);
-      }
+    for (int w = 0; w < L.LW; ++w) sts(waddr(L, LB + w), (w < lvw0 ? lv0[w] : 0u) + bias4);
+    for (int w = 0; w < BW; ++w) {
+      uint32_t bits = 0;
+      for (int k = 0; k < 8 && 8 * w + k < lvw0; ++k) bits |= flag_nibble(lv0[8 * w + k] + bias4) << (4 * k);
+      sts(waddr(L, BB + w), bits);
     }
     sts(waddr(L, BB + BW), 0u);
     sts(waddr(L, BB + BW + 1), 0u);
@@ -631,7 +555,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     // constant (stage A) is computed while the current op runs (B..E)
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
-    OpA nA = stage_a<NIB>(pqt, L, mbase, pt_base, GO, cur.x & 0xFFFFu);
+    OpA nA = stage_a(pqt, L, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
       const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
@@ -640,16 +564,16 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
         const OpA A = nA;
         {   // stage A of rank 4*qd + k + 1
           const uint32_t en = k == 0 ? cur.x >> 16 : k == 1 ? cur.y : k == 2 ? cur.y >> 16 : nxt.x;
-          nA = stage_a<NIB>(pqt, L, mbase, pt_base, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
+          nA = stage_a(pqt, L, GO, 4 * qd + k + 1 < K ? en & 0xFFFFu : 0u);
         }
         if (live && k < nk) {
           // B: t0 = max(RS, release / predecessor completion, machine free)
           const uint32_t rw = lds(A.ra), mw = lds(A.ma);
-          const int t0 = max((int)(field_at<NIB>(rw, A.rsh) & TM), (int)(field_at<NIB>(mw, A.msh) & TM));
+          const int t0 = max((int)((rw >> A.rsh) & TM), (int)((mw >> A.msh) & TM));
           // C: first run of p un-blocked ticks in the 32-tick window at t0
           //    (blocked words BW, BW+1 are zero sentinels: no bounds test)
           const uint32_t bwa = waddr(L, BB + min(t0 >> 5, BW));
-          uint32_t f = run_test<NIB>(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), A);
+          uint32_t f = run_test(~__funnelshift_r(lds(bwa), lds(bwa + 128), t0 & 31), A);
           int S;
           if (UQ) {
             // window miss: slide by 33 - p ticks (a run starting in the last
@@ -659,7 +583,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             while (f == 0u) {
               t += 33 - A.p;
               const uint32_t bwb = waddr(L, BB + min(t >> 5, BW));
-              f = run_test<NIB>(~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31), A);
+              f = run_test(~__funnelshift_r(lds(bwb), lds(bwb + 128), t & 31), A);
             }
             S = t + __ffs(f) - 1;
           } else {
@@ -672,52 +596,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
             live = false;
           } else {
             // E: job / machine times (the next op's loads follow in program order)
-            sts(A.ra, (rw & ~place_at<NIB>(TM, A.rsh)) | place_at<NIB>((uint32_t)C, A.rsh));
-            sts(A.ma, (mw & ~place_at<NIB>(TM, A.msh)) | place_at<NIB>((uint32_t)C, A.msh));
-            if (NIB) {
-              // D: headroom -= 1 on [S, C): borrow chain through the four
-              // bit planes under the p-bit mask (a second tick-word only when
-              // the interval crosses a 32-tick boundary); blocked = headroom 0
-              const int sh = S & 31;
-              const uint32_t a0 = waddr(L, LB + 4 * (S >> 5));
-              const uint32_t b0 = waddr(L, BB + (S >> 5));
-              uint32_t bm = A.nmo << sh;
-              const uint32_t bhi = __funnelshift_l(A.nmo, 0u, (uint32_t)sh);
-              {
-                const uint32_t h0 = lds(a0), h1 = lds(a0 + 128), h2 = lds(a0 + 256), h3 = lds(a0 + 384);
-                const uint32_t n0 = h0 ^ bm;
-                bm &= ~h0;
-                const uint32_t n1 = h1 ^ bm;
-                bm &= ~h1;
-                const uint32_t n2 = h2 ^ bm;
-                bm &= ~h2;
-                const uint32_t n3 = h3 ^ bm;
-                sts(a0, n0);
-                sts(a0 + 128, n1);
-                sts(a0 + 256, n2);
-                sts(a0 + 384, n3);
-                sts(b0, ~(n0 | n1 | n2 | n3));
-              }
-              if (bhi) {
-                uint32_t b2 = bhi;
-                const uint32_t a1 = a0 + 512;
-                const uint32_t h0 = lds(a1), h1 = lds(a1 + 128), h2 = lds(a1 + 256), h3 = lds(a1 + 384);
-                const uint32_t n0 = h0 ^ b2;
-                b2 &= ~h0;
-                const uint32_t n1 = h1 ^ b2;
-                b2 &= ~h1;
-                const uint32_t n2 = h2 ^ b2;
-                b2 &= ~h2;
-                const uint32_t n3 = h3 ^ b2;
-                sts(a1, n0);
-                sts(a1 + 128, n1);
-                sts(a1 + 256, n2);
-                sts(a1 + 384, n3);
-                sts(b0 + 128, ~(n0 | n1 | n2 | n3));
-              }
-              if (SCHED) srow[A.e / h.O] = S + h.rs;
-              continue;
-            }
+            sts(A.ra, (rw & ~(TM << A.rsh)) | ((uint32_t)C << A.rsh));
+            sts(A.ma, (mw & ~(TM << A.msh)) | ((uint32_t)C << A.msh));
             // D: level += q on [S, C) (<= 3 words, p <= 8), refresh blocked bits
             const int w0 = S >> 2;
             uint4 mk;
@@ -759,8 +639,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     int cm = h.frozen_cmax;
     for (int k = 0; k < h.n_pjobs; ++k) {
       const int j = pj[k];
-      const int wj = NIB ? (j * 0xAAAB) >> 17 : j >> 1;
-      const int Cr = (int)((lds(waddr(L, wj)) >> (NIB ? (j - 3 * wj) * 10 : (j & 1) << 4)) & TM);
+      const int Cr = (int)((lds(waddr(L, j >> 1)) >> ((j & 1) << 4)) & TM);
       const int tj = Cr - pd[k];
       T += tj > 0 ? tj : 0;
       cm = max(cm, Cr + h.rs);

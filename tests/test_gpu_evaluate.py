@@ -225,3 +225,16 @@ def test_tile_boundary_K(n, g, path):
     assert st.K == n * g
     x, y = wlmod.random_chromosomes(200, st.K, 3, seed=17)
     compare(octx, st, x, y, n_sched=20)
+
+
+@pytest.mark.parametrize("q,q_max", [(1, 20), (2, 9), (3, 40)])
+def test_uniform_power_mode1(q, q_max, path):
+    """Uniform Q other than the mode-2 case (Q = 1, Q_max <= 15): the lane
+    kernel's byte-level mode 1."""
+    wl = wlmod.gen_v1(f"U{q}", 20, 5, 3, q_max, arrivals_per_event=[5], ratios=[0.3], seed=40 + q)
+    arr = wl.original_instance()
+    arr = dict(arr, Q=np.full_like(arr["Q"], q))
+    octx = orc.Ctx(fx.workload_instance(arr), 0)
+    st = gpu_state(arr, 0)
+    x, y = wlmod.random_chromosomes(300, st.K, wl.o, seed=19)
+    compare(octx, st, x, y, n_sched=20)
