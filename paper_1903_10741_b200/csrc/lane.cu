@@ -52,16 +52,16 @@ __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 // predicated shared u16 store / load (no branch, no reconvergence barrier)
-__device__ __forceinline__ void sts16_if(bool p, const void *a, uint32_t v) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u16 [%0], %1;\n}\n" ::"r"(smem_u32(a)),
+__device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {   // a: shared-window address
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u16 [%0], %1;\n}\n" ::"r"(a),
                "h"((unsigned short)v), "r"((uint32_t)p)
                : "memory");
 }
-__device__ __forceinline__ uint32_t lds16_if(bool p, const void *a) {
+__device__ __forceinline__ uint32_t lds16_if(bool p, uint32_t a) {
   unsigned short v = 0;
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}\n"
                : "+h"(v)
-               : "r"(smem_u32(a)), "r"((uint32_t)p)
+               : "r"(a), "r"((uint32_t)p)
                : "memory");
   return v;
 }
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
                                (size_t)warp * a.pm_bytes);                      // [K] pm-1 | leader<<15
   unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
+  const uint32_t h16s = smem_u32(h16), ords = smem_u32(ord);   // shared-window addresses
   // CTA-shared copies of the per-gene table base and the segment-head bits,
   // and per-warp staging of the chromosome's machines (read once, in pass A)
   unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         if (B) {
           const int fl = __ffs(B) - 1;
           const int first = __shfl_sync(FULL, fpos, fl);
-          sts16_if(open_u >= 0 && lane == fl, h16 + open_u, (uint32_t)(first - open_pos));
+          sts16_if(open_u >= 0 && lane == fl, h16s + 2u * (uint32_t)open_u, (uint32_t)(first - open_pos));
           const int ll = 31 - __clz(B);
           open_pos = __shfl_sync(FULL, g0 + 31 - __clz(lm | 1u), ll);
           open_u = __shfl_sync(FULL, (int)lu, ll);
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 3; k >= 0; --k) {
           const bool ldk = (lm >> k) & 1u;
-          sts16_if(ldk && nx >= 0, h16 + (pk[k] & 0x7FFFu), (uint32_t)(nx - (g0 + k)));
+          sts16_if(ldk && nx >= 0, h16s + 2u * (pk[k] & 0x7FFFu), (uint32_t)(nx - (g0 + k)));
           nx = ldk ? g0 + k : nx;
         }
         carry = __shfl_sync(FULL, pm[3], 31);
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {   // leaders only: padding genes carry u = K, no flag
           const bool ldk = (pk[k] & 0x8000u) != 0u;
-          bk[k] = (int)lds16_if(ldk, h16 + (pk[k] & 0x7FFFu)) - (g0 + k);
+          bk[k] = (int)lds16_if(ldk, h16s + 2u * (pk[k] & 0x7FFFu)) - (g0 + k);
           lastb = ldk ? bk[k] : lastb;
           lm |= (ldk ? 1u : 0u) << k;
         }
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           if (FT)
             ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
           else
-            sts16_if(g < K, ord + base + g, gtab[tb + 32 * k] + (uint32_t)xs[g]);
+            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + (uint32_t)xs[g]);
         }
         if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
       };

@@ -238,3 +238,18 @@ def test_uniform_power_mode1(q, q_max, path):
     st = gpu_state(arr, 0)
     x, y = wlmod.random_chromosomes(300, st.K, wl.o, seed=19)
     compare(octx, st, x, y, n_sched=20)
+
+
+@pytest.mark.parametrize("count", [16500, 33001])
+def test_evaluate_host_chunked_pipeline(count):
+    """ffs_evaluate_host splits large batches into 2 or 4 uneven chunks on two
+    internal streams; results equal the device call."""
+    wl = wlmod.config_A2()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(count, st.K, wl.o, seed=23)
+    obj, T, M = ffs.evaluate_host(st, x, y)
+    ref = gpu_eval(st, x, y)
+    assert (obj == ref[0]).all() and (T == ref[1]).all() and (M == ref[2]).all()
+    idx = np.random.default_rng(1).choice(count, 64, replace=False)
+    oo, oT, oM, _ = octx.evaluate_batch(x[idx], y[idx])
+    assert (obj[idx] == oo).all() and (T[idx] == oT).all() and (M[idx] == oM).all()
