@@ -222,9 +222,17 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank over NCCL (the product path); FFS_DIST_BACKEND=gloo lets
+    # the multi-rank code path be exercised with several ranks on one GPU
+    backend = os.environ.get("FFS_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     # ---- workload: plan decoded on the GPU at RS = 0, freeze at RS

@@ -73,11 +73,22 @@ def make_hooks(device_memory: bool = True):
         import contextlib
         return contextlib.nullcontext()
 
+    def _host_staged():
+        # gloo moves host tensors: device buffers are staged through the host
+        # (NCCL, the GPU path, reads and writes them in place)
+        import torch.distributed as dist
+        return device_memory and dist.get_backend() == "gloo"
+
     def allreduce(user, ptr, stream):
         try:
             with _stream_ctx(stream):
                 t = _dev_view(ptr, 1, "<i8") if device_memory else _host_view(ptr, 1, C.c_int64)
-                allreduce_max_tensor(t)
+                if _host_staged():
+                    h = t.cpu()
+                    allreduce_max_tensor(h)
+                    t.copy_(h)
+                else:
+                    allreduce_max_tensor(t)
             return 0
         except Exception:  # the C side turns non-zero into FFS_ERR_COMM
             return 1
@@ -90,7 +101,10 @@ def make_hooks(device_memory: bool = True):
                 if device_memory:
                     s = _dev_view(send, nbytes, "|u1")
                     r = _dev_view(recv, nbytes * world, "|u1")
-                    dist.all_gather_into_tensor(r, s)
+                    if _host_staged():
+                        r.copy_(allgather_bytes_tensor(s.cpu()))
+                    else:
+                        dist.all_gather_into_tensor(r, s)
                 else:
                     s = _host_view(send, nbytes, C.c_uint8)
                     r = _host_view(recv, nbytes * world, C.c_uint8)

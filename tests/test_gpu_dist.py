@@ -1,0 +1,72 @@
+"""The sharded island GA through the C-ABI's collective hooks on the GPU:
+two processes (gloo; both on cuda:0, since this box has one GPU), each owning
+half of the islands, exchanging E_max and the ring migrants through the
+callbacks of ffs_ga_config -- bit-identical to the single-process run (every
+random draw is keyed by the global island index; R22, R23)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+ISL_W, ISL_H, ISLANDS, G, SEED = 4, 4, 6, 23, 31
+
+
+def _state():
+    from paper_1903_10741_b200 import ffs
+    from paper_1903_10741_b200 import workload as wlmod
+    wl = wlmod.config_A2()
+    base = ffs.Instance.from_arrays(wl.original_instance(), device=0)
+    st0 = ffs.make_state(base, 0)
+    assign, start, _, _, M = ffs.decode_schedule(st0, wl.plan_x, wl.plan_y)
+    rs = wl.rs_from_makespan(wl.ratios[0], M)
+    inst = ffs.Instance.from_arrays(wl.instance_at(0, [rs]), device=0)
+    st = ffs.make_state(inst, rs, assign[: wl.n * wl.g], start[: wl.n * wl.g])
+    st._keep = (base, st0, inst)
+    return st
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1903_10741_b200 import dist as fdist
+        from paper_1903_10741_b200 import ffs
+        torch.cuda.set_device(0)
+        st = _state()
+        b, e = fdist.shard(ISLANDS, rank, world)
+        run = ffs.Run(st, ISL_W, ISL_H, ISLANDS, G, SEED, island_begin=b, island_end=e, rank=rank, world=world,
+                      hooks=fdist.make_hooks(device_memory=True))
+        run.step(G)
+        x, y, obj, fit = run.population()
+        hx, hy, hobj, hfit = run.history()
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=x, y=y, obj=obj, fit=fit, hx=hx, hy=hy, hobj=hobj,
+                 emax=run.info()["emax"])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_ga_equals_single_process(tmp_path):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    from paper_1903_10741_b200 import ffs
+    st = _state()
+    run = ffs.Run(st, ISL_W, ISL_H, ISLANDS, G, SEED)
+    run.step(G)
+    x, y, obj, fit = run.population()
+    hx, hy, hobj, _ = run.history()
+    parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(2)]
+    assert all(int(p["emax"]) == run.info()["emax"] for p in parts)
+    for key, ref in (("x", x), ("y", y), ("obj", obj), ("fit", fit), ("hx", hx), ("hy", hy), ("hobj", hobj)):
+        got = np.concatenate([p[key] for p in parts])
+        assert (got == ref).all(), key
