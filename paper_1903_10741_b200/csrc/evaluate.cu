@@ -190,13 +190,14 @@ __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
 }
 
 // Counter-based random chromosomes: x ~ U{0..o-1}, y = 1 + rank of a random
-// key (ties by gene index).  Warp per chromosome; keys in shared memory.
-__global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32_t O, int64_t count,
+// key (ties by gene index).  Warp per chromosome; ranks by a bitonic sort of
+// the keys in shared memory (rank_keys_warp).
+__global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32_t NP, int32_t O, int64_t count,
                                                                 uint64_t seed, int64_t first_id,
                                                                 int8_t *x, int16_t *y) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *keys = (uint32_t *)smem + (size_t)warp * K;
+  unsigned long long *buf = (unsigned long long *)smem + (size_t)warp * NP;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < count; c += nw) {
@@ -206,33 +207,9 @@ __global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32
       u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       x[c * K + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
-      keys[g] = word_of(ry, g & 3);
+      buf[g] = ((unsigned long long)word_of(ry, g & 3) << 32) | (uint32_t)g;
     }
-    __syncwarp();
-    for (int g0 = 0; g0 < K; g0 += 128) {
-      uint32_t mk[4];
-      int rk[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int gg = g0 + lane + 32 * u;
-        mk[u] = gg < K ? keys[gg] : 0u;
-        rk[u] = 0;
-      }
-      for (int hh = 0; hh < K; ++hh) {
-        uint32_t kh = keys[hh];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          int gg = g0 + lane + 32 * u;
-          rk[u] += (kh < mk[u]) | ((kh == mk[u]) & (hh < gg));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int gg = g0 + lane + 32 * u;
-        if (gg < K) y[c * K + gg] = (int16_t)(rk[u] + 1);
-      }
-    }
-    __syncwarp();
+    rank_keys_warp(buf, K, NP, lane, y + c * K);
   }
 }
 
@@ -301,9 +278,11 @@ ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, 
 ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id,
                                     int8_t *x, int16_t *y, cudaStream_t s) {
   if (count <= 0 || st.K == 0) return FFS_OK;
-  const int warps = 8;
-  size_t smem = (size_t)warps * st.K * sizeof(uint32_t);
-  if (smem > (size_t)kSmemLimit) return fail(FFS_ERR_INVALID_ARG, "K too large for random_population");
+  int NP = 64;
+  while (NP < st.K) NP <<= 1;
+  const int warps = (int)std::min<size_t>(8, (size_t)kSmemLimit / ((size_t)NP * 8));
+  if (warps < 1) return fail(FFS_ERR_INVALID_ARG, "K too large for random_population");
+  size_t smem = (size_t)warps * NP * 8;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     FFS_CUDA(cudaFuncSetAttribute(random_population_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -313,7 +292,7 @@ ffs_status launch_random_population(const State &st, int64_t count, uint64_t see
   int64_t grid = (count + warps - 1) / warps;
   int64_t cap = (int64_t)st.num_sms * 8;
   if (grid > cap) grid = cap;
-  random_population_kernel<<<(unsigned)grid, warps * 32, smem, s>>>(st.K, st.inst->o, count, seed, first_id,
+  random_population_kernel<<<(unsigned)grid, warps * 32, smem, s>>>(st.K, NP, st.inst->o, count, seed, first_id,
                                                                     x, y);
   FFS_CUDA(cudaGetLastError());
   return FFS_OK;

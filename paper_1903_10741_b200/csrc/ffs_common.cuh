@@ -226,6 +226,33 @@ __host__ __device__ __forceinline__ uint32_t bounded(uint32_t u, uint32_t n) {
   return (uint32_t)(((uint64_t)u * n) >> 32);
 }
 
+#ifdef __CUDACC__
+// The initialisation's priorities: y[g] = 1 + the rank of
+// gene g's key, ascending by (key, gene index).  One warp sorts the composite
+// keys key << 32 | g (distinct) with a bitonic network in shared memory
+// (buf: NP u64, NP = a power of two >= max(K, 64); buf[0..K) filled by the
+// caller) and scatters y.  O(K log^2 K) instead of O(K^2) comparisons.
+__device__ __forceinline__ void rank_keys_warp(unsigned long long *buf, int K, int NP, int lane, int16_t *y) {
+  for (int g = K + lane; g < NP; g += 32) buf[g] = ~0ull;
+  __syncwarp();
+  for (int k = 2; k <= NP; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < (NP >> 1); i += 32) {
+        const int a = 2 * i - (i & (j - 1)), b = a + j;   // comparator i of this step: (a, a + j)
+        const unsigned long long va = buf[a], vb = buf[b];
+        if ((va > vb) == ((a & k) == 0)) {
+          buf[a] = vb;
+          buf[b] = va;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int p = lane; p < K; p += 32) y[(uint32_t)buf[p]] = (int16_t)(p + 1);
+  __syncwarp();
+}
+#endif
+
 }  // namespace edffs
 
 struct ffs_instance { edffs::Instance v; };

@@ -74,11 +74,14 @@ namespace {
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
 // ---- initialisation: x ~ U{0..o-1}, y = 1 + rank of a random key
-__global__ void __launch_bounds__(256) init_kernel(int32_t K, int64_t row, int32_t O, int64_t count, int32_t tile,
-                                                   int32_t island0, uint64_t seed, int8_t *x, int16_t *y) {
-  extern __shared__ __align__(16) uint32_t keys_all[];
+// (warp per chromosome; the ranks by a bitonic sort in shared memory, NP u64
+// per warp)
+__global__ void __launch_bounds__(256) init_kernel(int32_t K, int32_t NP, int64_t row, int32_t O, int64_t count,
+                                                   int32_t tile, int32_t island0, uint64_t seed, int8_t *x,
+                                                   int16_t *y) {
+  extern __shared__ __align__(16) unsigned long long keys_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *keys = keys_all + (size_t)warp * K;
+  unsigned long long *buf = keys_all + (size_t)warp * NP;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; c < count; c += nw) {
@@ -87,30 +90,9 @@ __global__ void __launch_bounds__(256) init_kernel(int32_t K, int64_t row, int32
       u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       x[c * row + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
-      keys[g] = word_of(ry, g & 3);
+      buf[g] = ((unsigned long long)word_of(ry, g & 3) << 32) | (uint32_t)g;
     }
-    __syncwarp();
-    for (int g0 = 0; g0 < K; g0 += 128) {
-      uint32_t mk[4];
-      int rk[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int gg = g0 + lane + 32 * u;
-        mk[u] = gg < K ? keys[gg] : 0u;
-        rk[u] = 0;
-      }
-      for (int hh = 0; hh < K; ++hh) {
-        uint32_t kh = keys[hh];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) rk[u] += (kh < mk[u]) | ((kh == mk[u]) & (hh < g0 + lane + 32 * u));
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int gg = g0 + lane + 32 * u;
-        if (gg < K) y[c * row + gg] = (int16_t)(rk[u] + 1);
-      }
-    }
-    __syncwarp();
+    rank_keys_warp(buf, K, NP, lane, y + c * row);
   }
 }
 
@@ -678,13 +660,15 @@ static ffs_status evaluate_population(Run &r, int buf, bool with_fitness) {
 
 static ffs_status ga_init(Run &r) {
   const State &st = *r.st;
-  const int warps = 8;
-  size_t smem = (size_t)warps * r.K * 4;
-  if (smem > (size_t)kSmemLimit) return fail(FFS_ERR_INVALID_ARG, "K too large for initialisation");
+  int NP = 64;
+  while (NP < r.K) NP <<= 1;
+  const int warps = (int)std::min<size_t>(8, (size_t)kSmemLimit / ((size_t)NP * 8));
+  if (warps < 1) return fail(FFS_ERR_INVALID_ARG, "K too large for initialisation");
+  size_t smem = (size_t)warps * NP * 8;
   FFS_CUDA(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t grid = std::min<int64_t>((r.nloc + warps - 1) / warps, (int64_t)st.num_sms * 8);
-  init_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(r.K, r.row, st.inst->o, r.nloc, r.tile, r.cfg.island_begin,
-                                                         r.cfg.seed, r.x[0], r.y[0]);
+  init_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(r.K, NP, r.row, st.inst->o, r.nloc, r.tile,
+                                                         r.cfg.island_begin, r.cfg.seed, r.x[0], r.y[0]);
   FFS_CUDA(cudaGetLastError());
   r.launches++;
   ffs_status e = evaluate_population(r, 0, false);
