@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
                      : "memory");
       }
       // hist/start are indexed by u = K - pm (descending prefix minimum)
-      for (int i = lane; i < ((K + 255) >> 8) << 7; i += 32) hist[i] = 0u;
+      for (int i = lane; i < ((K + 511) >> 9) << 8; i += 32) hist[i] = 0u;
       __syncwarp();
       if (BULK) {
         while (!mbar_try(bar, phase)) {
@@ -319,30 +319,35 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       if (open_u >= 0 && lane == 0) h16[open_u] = (uint16_t)(K - open_pos);
       __syncwarp();
       // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u),
-      // 8 counts per lane per step (entries >= K are written but never read)
+      // 16 counts (u16 pairs) per lane per step of 512 (entries >= K are
+      // written but never read); W * 0x10001 puts a pair's sum in the high half
       uint32_t acc = 0;
-      for (int ub = 0; ub < K; ub += 256) {   // warp-uniform trip count (shuffles inside)
-        const int u0 = ub + 8 * lane;
-        const uint4 w = *(const uint4 *)(h16 + u0);   // u0 % 8 == 0: 16-byte aligned
-        const uint32_t p0 = w.x + (w.x << 16);        // pairwise inclusive sums in the high halves
-        const uint32_t p1 = w.y + (w.y << 16), p2 = w.z + (w.z << 16), p3 = w.w + (w.w << 16);
-        const uint32_t s01 = (p0 >> 16) + (p1 >> 16), s012 = s01 + (p2 >> 16);
-        const uint32_t sum = s012 + (p3 >> 16);
+      for (int ub = 0; ub < K; ub += 512) {   // warp-uniform trip count (shuffles inside)
+        const int u0 = ub + 16 * lane;
+        uint4 wa = *(const uint4 *)(h16 + u0), wb = *(const uint4 *)(h16 + u0 + 8);   // 32-byte aligned
+        const uint32_t W[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        uint32_t ex[8], run = 0;                      // exclusive in-lane prefix of the pair sums
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ex[i] = run;
+          run += (W[i] * 0x10001u) >> 16;
+        }
+        const uint32_t sum = run;
         uint32_t incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const uint32_t n = __shfl_up_sync(FULL, incl, d);
           if (lane >= d) incl += n;
         }
-        const uint32_t e0 = acc + incl - sum;         // exclusive start of the lane's 8 counts
-        const uint32_t e1 = e0 + (p0 >> 16), e2 = e0 + s01, e3 = e0 + s012;
-        // start of count 2i = e_i, of count 2i+1 = e_i + count 2i
-        uint4 o;
-        o.x = e0 | ((e0 + (w.x & 0xFFFFu)) << 16);
-        o.y = e1 | ((e1 + (w.y & 0xFFFFu)) << 16);
-        o.z = e2 | ((e2 + (w.z & 0xFFFFu)) << 16);
-        o.w = e3 | ((e3 + (w.w & 0xFFFFu)) << 16);
-        *(uint4 *)(h16 + u0) = o;
+        const uint32_t e0 = acc + incl - sum;         // exclusive start of the lane's 16 counts
+        uint32_t O[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {   // start of count 2i = e, of count 2i+1 = e + count 2i
+          const uint32_t e = e0 + ex[i];
+          O[i] = e | ((e + (W[i] & 0xFFFFu)) << 16);
+        }
+        *(uint4 *)(h16 + u0) = make_uint4(O[0], O[1], O[2], O[3]);
+        *(uint4 *)(h16 + u0 + 8) = make_uint4(O[4], O[5], O[6], O[7]);
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();

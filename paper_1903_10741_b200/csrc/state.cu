@@ -283,7 +283,7 @@ ffs_status State::build_image() {
     hc = std::min<int64_t>(hc, lmode == 2 ? 992 : 65504);   // 10-bit times in mode 2
     int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
     // order kernel: 32 warps, per warp hist[K] u16 + ord[K] u16 (stride 8*odd)
-    ord_hist_bytes = (size_t)((K + 255) / 256 * 256) * 2;                              // u16 [K], steps of 256
+    ord_hist_bytes = (size_t)((K + 511) / 512 * 512) * 2;                              // u16 [K], steps of 512
     max_pending = 0;
     for (int k = 0, run = 0; k < K; ++k) {   // longest run of one job's pending genes
       run = (k > 0 && gene_job[k] == gene_job[k - 1]) ? run + 1 : 1;
