@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         // leaders = new prefix minima (pm == y); each distinct pm is one run
         // (a leader and the non-leaders after it in its job), and a run's
         // length is stored once, by its leader, at u = K - pm: hist[u] = len
-        uint32_t pk[4], lm = 0, lu = 0;
+        uint32_t pk[4], ua[4], lm = 0, lu = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const bool ld = ok && pm[k] == y[k];
           lm |= (ld ? 1u : 0u) << k;
           pk[k] = u | (ld ? 0x8000u : 0u);
+          ua[k] = h16s + 2u * u;   // hist slot of the gene's run
           lu = ld ? u : lu;   // the lane's last leader
         }
         *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 3; k >= 0; --k) {
           const bool ldk = (lm >> k) & 1u;
-          sts16_if(ldk && nx >= 0, h16s + 2u * (pk[k] & 0x7FFFu), (uint32_t)(nx - (g0 + k)));
+          sts16_if(ldk && nx >= 0, ua[k], (uint32_t)(nx - (g0 + k)));
           nx = ldk ? g0 + k : nx;
         }
         carry = __shfl_sync(FULL, pm[3], 31);
