@@ -83,9 +83,19 @@ struct OvfScratch {
   int64_t ordg_elems = 0;
   void *level = nullptr;         // [fallback warps * hfull * sizeof(LVL)]
   int64_t level_bytes = 0;
+  // set (a GA run's scratch): allocations are stream-ordered from the
+  // device's default memory pool on this stream (cheap re-allocation across
+  // runs); unset: plain cudaMalloc
+  cudaStream_t pool = nullptr;
+  bool pooled = false;
   ffs_status ensure(int64_t count, int64_t level_bytes_needed);
+  ffs_status alloc(void **p, size_t bytes);
+  void free_(void *p);
   void release();
 };
+// keep freed blocks of the default memory pool cached (no release to the
+// driver at synchronisation points), once per device
+void pool_keep(int dev);
 
 // device staging of ffs_evaluate_host (grow-only)
 struct HostStage {

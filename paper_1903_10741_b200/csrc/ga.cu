@@ -55,14 +55,17 @@ struct Run {
   int64_t evaluations = 0;
   int launches = 0;
   std::vector<void *> allocs;
+  // buffers are stream-ordered allocations from the default memory pool (kept
+  // cached across runs: creating and destroying runs in a workflow does not
+  // synchronise the device)
   ~Run() {
-    for (void *p : allocs) cudaFree(p);
+    for (void *p : allocs) cudaFreeAsync(p, s);
     scr.release();
   }
   template <typename T>
   ffs_status alloc(T **p, size_t n) {
     void *q = nullptr;
-    FFS_CUDA(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)));
+    FFS_CUDA(cudaMallocAsync(&q, std::max<size_t>(n, 1) * sizeof(T), s));
     allocs.push_back(q);
     *p = (T *)q;
     return FFS_OK;
@@ -774,6 +777,9 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
   r.st = &st;
   r.cfg = *cfg;
   r.s = (cudaStream_t)stream;
+  pool_keep(st.inst->dev);
+  r.scr.pool = r.s;
+  r.scr.pooled = true;
   r.tile = cfg->island_w * cfg->island_h;
   r.nisl = cfg->island_end - cfg->island_begin;
   r.nloc = (int64_t)r.nisl * r.tile;

@@ -962,9 +962,10 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   const int64_t chunk = std::min<int64_t>((a0.count + 31) / 32 * 32, chunk_max);
   const int64_t elems = chunk / 32 * (int64_t)KQ * 128;
   if (elems > scr.ordg_elems) {
-    if (scr.ordg) cudaFree(scr.ordg);
+    scr.free_(scr.ordg);
     scr.ordg = nullptr;
-    FFS_CUDA(cudaMalloc(&scr.ordg, (size_t)elems * 2));
+    ffs_status ea = scr.alloc((void **)&scr.ordg, (size_t)elems * 2);
+    if (ea != FFS_OK) return ea;
     scr.ordg_elems = elems;
   }
   // the segmented min-scan's doubling steps: 2^SCAN > lanes a job's pending

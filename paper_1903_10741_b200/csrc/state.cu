@@ -25,33 +25,57 @@ ffs_status cuda_fail(cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? FFS_ERR_OOM : FFS_ERR_CUDA;
 }
 
+ffs_status OvfScratch::alloc(void **p, size_t bytes) {
+  if (pooled) FFS_CUDA(cudaMallocAsync(p, bytes, pool));
+  else FFS_CUDA(cudaMalloc(p, bytes));
+  return FFS_OK;
+}
+void OvfScratch::free_(void *p) {
+  if (!p) return;
+  if (pooled) cudaFreeAsync(p, pool);
+  else cudaFree(p);
+}
+
 ffs_status OvfScratch::ensure(int64_t count, int64_t level_bytes_needed) {
   if (count + 1 > cap) {
-    if (list) cudaFree(list);
+    free_(list);
     list = nullptr;
     int64_t c = std::max<int64_t>(count + 1, 1024);
-    FFS_CUDA(cudaMalloc(&list, (size_t)c * sizeof(int32_t)));
+    ffs_status e = alloc((void **)&list, (size_t)c * sizeof(int32_t));
+    if (e != FFS_OK) return e;
     cap = c;
   }
   if (level_bytes_needed > level_bytes) {
-    if (level) cudaFree(level);
+    free_(level);
     level = nullptr;
-    FFS_CUDA(cudaMalloc(&level, (size_t)level_bytes_needed));
+    ffs_status e = alloc(&level, (size_t)level_bytes_needed);
+    if (e != FFS_OK) return e;
     level_bytes = level_bytes_needed;
   }
   return FFS_OK;
 }
 
 void OvfScratch::release() {
-  if (list) cudaFree(list);
-  if (level) cudaFree(level);
-  if (ordg) cudaFree(ordg);
+  free_(list);
+  free_(level);
+  free_(ordg);
   list = nullptr;
   level = nullptr;
   ordg = nullptr;
   cap = 0;
   level_bytes = 0;
   ordg_elems = 0;
+}
+
+void pool_keep(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
 }
 
 static uint32_t r16(uint64_t v) { return (uint32_t)((v + 15) & ~(uint64_t)15); }
