@@ -723,6 +723,12 @@ __device__ __forceinline__ uint32_t runs2(uint32_t w, const Op2 &A) {
   return f;
 }
 
+// the overflow path's reset of a lane's job / machine times (out of line: it
+// is rare, and inlining it into every unrolled dispatch bloats the loop)
+__device__ __noinline__ void reset_fields(uint32_t lbase, int n) {
+  for (int w = 0; w < n; ++w) sts(lbase + ((uint32_t)w << 7), 0u);
+}
+
 // Earliest start >= t0 of p free ticks (reversed bit order).  Overflow (no
 // run inside the horizon, rare path): the lane's result is void (sgn = -1,
 // the fallback re-decodes the chromosome) and its job / machine times are
@@ -740,7 +746,7 @@ __device__ __forceinline__ int search2(const Op2 &A, int t0, uint32_t bb_base, i
     do {
       t += 33 - A.p;
       if (t + A.p > hcap) {
-        for (int w = 0; w < nfield_words; ++w) sts(lbase + ((uint32_t)w << 7), 0u);
+        reset_fields(lbase, nfield_words);
         rw = mw = rf = mf = 0u;
         sgn = -1;
         return 0;
