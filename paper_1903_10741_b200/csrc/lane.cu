@@ -697,8 +697,12 @@ __device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint3
   A.e = e;
   A.rsh = tv;
   A.msh = tv >> 5;
-  A.rmul = 1u << (tv & 31u);
-  A.mmul = 1u << ((tv >> 5) & 31u);
+  // 2^shift by a wrap funnel shift (no mask), kept opaque so the compiler
+  // does not turn the field updates' multiplies back into alu-pipe shifts
+  A.rmul = __funnelshift_l(0u, 1u, tv);
+  A.mmul = __funnelshift_l(0u, 1u, tv >> 5);
+  pin(A.rmul);
+  pin(A.mmul);
   A.ra = lbase + ((tv >> 3) & 0x3FF80u);
   A.ma = mbase + ((tv >> 14) & 0x7F80u);
   const uint32_t pm1 = tv >> 29;
