@@ -288,6 +288,10 @@ def run_ours(args):
     # ---- dominant kernel alone (decode + evaluate of the same 65,536 population,
     # same launch configuration), CUDA events on its stream
     x, y = ffs.random_population(st, pop_local, SEED, first_id=b << 20, stream=stream)
+    # the GA's own population layout: rows padded to 16 genes (TMA row staging)
+    KP = (K + 15) // 16 * 16
+    x = torch.nn.functional.pad(x, (0, KP - K)).contiguous()
+    y = torch.nn.functional.pad(y, (0, KP - K)).contiguous()
     obj = torch.empty(pop_local, dtype=torch.int64, device=dev)
     T = torch.empty(pop_local, dtype=torch.int64, device=dev)
     M = torch.empty(pop_local, dtype=torch.int32, device=dev)
@@ -308,8 +312,8 @@ def run_ours(args):
     # ---- end to end through the public API with host buffers (pinned), copies inside
     xh = torch.empty((pop_local, K), dtype=torch.int8, pin_memory=True)
     yh = torch.empty((pop_local, K), dtype=torch.int16, pin_memory=True)
-    xh.copy_(x.cpu())
-    yh.copy_(y.cpu())
+    xh.copy_(x[:, :K].cpu())
+    yh.copy_(y[:, :K].cpu())
     oh = torch.empty(pop_local, dtype=torch.int64, pin_memory=True).numpy()
     th = torch.empty(pop_local, dtype=torch.int64, pin_memory=True).numpy()
     mh = torch.empty(pop_local, dtype=torch.int32, pin_memory=True).numpy()

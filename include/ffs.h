@@ -165,6 +165,14 @@ FFS_API ffs_status ffs_state_set_objective_weight(ffs_state *st, double wt);
 FFS_API ffs_status ffs_evaluate(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
                         int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                         int32_t *start_out, void *cuda_stream);
+/* Same with a row stride: chromosome c's genes are x[c*row .. c*row+K) and
+ * y[c*row .. c*row+K) (row = 0 means K).  row >= K; with row % 16 == 0 and
+ * 16-byte aligned x, y the order kernel stages whole rows by TMA bulk copies
+ * (the GA's own padded population layout).  Errors: FFS_ERR_INVALID_ARG for
+ * 0 < row < K; otherwise as ffs_evaluate. */
+FFS_API ffs_status ffs_evaluate_strided(const ffs_state *st, int64_t count, const int8_t *x, const int16_t *y,
+                                        int64_t row, int64_t *objective, int64_t *total_tardiness,
+                                        int32_t *makespan, int32_t *start_out, void *cuda_stream);
 /* Same with HOST buffers (pageable or pinned): copies in, evaluates, copies
  * out, synchronises.  Ordered after earlier work on cuda_stream.  Large
  * batches run as a pipeline of up to 4 chunks on two internal streams (chunk

@@ -587,7 +587,14 @@ void ffs_state_destroy(ffs_state *h) {
 
 ffs_status ffs_evaluate(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y, int64_t *objective,
                         int64_t *total_tardiness, int32_t *makespan, int32_t *start_out, void *stream) {
+  return ffs_evaluate_strided(h, count, x, y, 0, objective, total_tardiness, makespan, start_out, stream);
+}
+
+ffs_status ffs_evaluate_strided(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y, int64_t row,
+                                int64_t *objective, int64_t *total_tardiness, int32_t *makespan, int32_t *start_out,
+                                void *stream) {
   if (!h || count < 0) return fail(FFS_ERR_INVALID_ARG, "bad state or count");
+  if (row != 0 && row < h->v.K) return fail(FFS_ERR_INVALID_ARG, "row stride must be 0 or >= K");
   if (count > 0 && h->v.K > 0 && (!x || !y)) return fail(FFS_ERR_INVALID_ARG, "null chromosome arrays");
   if (count > ((int64_t)1 << 31) - 2) return fail(FFS_ERR_INVALID_ARG, "count must be < 2^31");
   State &st = const_cast<State &>(h->v);
@@ -602,6 +609,7 @@ ffs_status ffs_evaluate(const ffs_state *h, int64_t count, const int8_t *x, cons
   a.cmax = makespan;
   a.start_out = start_out;
   a.fstart = st.fstart_dev;
+  a.row = row;
   return launch_evaluate(st, a, st.scratch, (cudaStream_t)stream, nullptr);
 }
 

@@ -26,7 +26,7 @@ EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
     "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
-    "ffs_evaluate_host", "ffs_brute_force", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
+    "ffs_evaluate_host", "ffs_evaluate_strided", "ffs_brute_force", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
     "ffs_run_destroy",
 ]
@@ -84,6 +84,7 @@ def lib():
             "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
             "ffs_evaluate": ([P, C.c_int64, P, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
+            "ffs_evaluate_strided": ([P, C.c_int64, P, P, C.c_int64, P, P, P, P, P], C.c_int),
             "ffs_random_population": ([P, C.c_int64, C.c_uint64, C.c_int64, P, P, P], C.c_int),
             "ffs_evolve_begin": ([P, C.POINTER(GAConfig), P, P], C.c_int),
             "ffs_evolve_step": ([P, C.c_int32], C.c_int),
@@ -210,9 +211,11 @@ class State:
 
 def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=None, start_out=None,
              with_schedule=False, stream=None):
-    """Decode + evaluate device chromosomes x:int8[count,K], y:int16[count,K]."""
+    """Decode + evaluate device chromosomes x:int8[count,R], y:int16[count,R]
+    (R = K, or a padded row R > K: ffs_evaluate_strided)."""
     import torch
     count = x.shape[0] if x.dim() == 2 else (x.numel() // max(state.K, 1))
+    row = x.shape[1] if (x.dim() == 2 and x.shape[1] != state.K) else 0
     dev = x.device
     if objective is None:
         objective = torch.empty(count, dtype=torch.int64, device=dev)
@@ -222,13 +225,14 @@ def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=
         makespan = torch.empty(count, dtype=torch.int32, device=dev)
     if with_schedule and start_out is None:
         start_out = torch.empty((count, state.cells), dtype=torch.int32, device=dev)
-    n = count * state.K
-    _check(lib().ffs_evaluate(state.h, count, _dev_ptr(x, torch.int8, n, "x"), _dev_ptr(y, torch.int16, n, "y"),
-                              _dev_ptr(objective, torch.int64, count, "objective"),
-                              _dev_ptr(total_tardiness, torch.int64, count, "total_tardiness"),
-                              _dev_ptr(makespan, torch.int32, count, "makespan"),
-                              _dev_ptr(start_out, torch.int32, count * state.cells, "start_out"),
-                              _stream(stream)), "ffs_evaluate")
+    n = count * (row or state.K)
+    _check(lib().ffs_evaluate_strided(state.h, count, _dev_ptr(x, torch.int8, n, "x"),
+                                      _dev_ptr(y, torch.int16, n, "y"), row,
+                                      _dev_ptr(objective, torch.int64, count, "objective"),
+                                      _dev_ptr(total_tardiness, torch.int64, count, "total_tardiness"),
+                                      _dev_ptr(makespan, torch.int32, count, "makespan"),
+                                      _dev_ptr(start_out, torch.int32, count * state.cells, "start_out"),
+                                      _stream(stream)), "ffs_evaluate_strided")
     if state.real_wt is not None:
         objective = objective.view(torch.float64)
     return objective, total_tardiness, makespan, start_out

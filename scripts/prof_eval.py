@@ -29,6 +29,9 @@ if __name__ == "__main__":
     wl, st = config_c_state()
     print(st.info())
     x, y = ffs.random_population(st, n, 10741)
+    KP = (st.K + 15) // 16 * 16   # the GA's padded rows (TMA row staging), as bench.py's eval_only
+    x = torch.nn.functional.pad(x, (0, KP - st.K)).contiguous()
+    y = torch.nn.functional.pad(y, (0, KP - st.K)).contiguous()
     for _ in range(reps):
         obj, T, M, _ = ffs.evaluate(st, x, y)
     torch.cuda.synchronize()

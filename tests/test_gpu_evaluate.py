@@ -253,3 +253,22 @@ def test_evaluate_host_chunked_pipeline(count):
     idx = np.random.default_rng(1).choice(count, 64, replace=False)
     oo, oT, oM, _ = octx.evaluate_batch(x[idx], y[idx])
     assert (obj[idx] == oo).all() and (T[idx] == oT).all() and (M[idx] == oM).all()
+
+
+@pytest.mark.parametrize("pad", [16, 5])
+def test_strided_rows_match_compact(pad, path):
+    """ffs_evaluate_strided: rows padded to a multiple of 16 genes (TMA row
+    staging) or by an odd amount (element loads) give the compact results."""
+    wl = wlmod.config_B()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(700, st.K, wl.o, seed=29)
+    R = (st.K + 15) // 16 * 16 if pad == 16 else st.K + pad
+    xp = np.zeros((len(x), R), np.int8)
+    yp = np.zeros((len(y), R), np.int16)
+    xp[:, :st.K] = x
+    yp[:, :st.K] = y
+    ref = gpu_eval(st, x, y, sched=True)
+    got = gpu_eval(st, xp, yp, sched=True)
+    for u, v in zip(ref, got):
+        assert (u == v).all()
+    compare(octx, st, x[:60], y[:60], n_sched=10)
