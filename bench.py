@@ -287,11 +287,9 @@ def run_ours(args):
 
     # ---- dominant kernel alone (decode + evaluate of the same 65,536 population,
     # same launch configuration), CUDA events on its stream
-    x, y = ffs.random_population(st, pop_local, SEED, first_id=b << 20, stream=stream)
     # the GA's own population layout: rows padded to 16 genes (TMA row staging)
     KP = (K + 15) // 16 * 16
-    x = torch.nn.functional.pad(x, (0, KP - K)).contiguous()
-    y = torch.nn.functional.pad(y, (0, KP - K)).contiguous()
+    x, y = ffs.random_population(st, pop_local, SEED, first_id=b << 20, stream=stream, row=KP)
     obj = torch.empty(pop_local, dtype=torch.int64, device=dev)
     T = torch.empty(pop_local, dtype=torch.int64, device=dev)
     M = torch.empty(pop_local, dtype=torch.int32, device=dev)
@@ -336,7 +334,7 @@ def run_ours(args):
         share = (total + world - 1) // world
         first = rank * share
         n_loc = max(0, min(share, total - first))
-        xs, ys = ffs.random_population(st, n_loc, SEED, first_id=first, stream=stream)
+        xs, ys = ffs.random_population(st, n_loc, SEED, first_id=first, stream=stream, row=KP)
         ob = torch.empty(max(n_loc, 1), dtype=torch.int64, device=dev)
         ffs.evaluate(st, xs, ys, ob[:n_loc], stream=stream)
         e0 = torch.cuda.Event(enable_timing=True)

@@ -203,6 +203,11 @@ FFS_API ffs_status ffs_brute_force(const ffs_state *st, int64_t limit, int64_t *
  * x [count*K], y [count*K]. */
 FFS_API ffs_status ffs_random_population(const ffs_state *st, int64_t count, uint64_t seed, int64_t first_id,
                                  int8_t *x, int16_t *y, void *cuda_stream);
+/* Same into rows of `row` genes (row >= K; genes K..row-1 untouched): the
+ * padded layout of ffs_evaluate_strided.  row = 0 means K. */
+FFS_API ffs_status ffs_random_population_strided(const ffs_state *st, int64_t count, uint64_t seed,
+                                                 int64_t first_id, int64_t row, int8_t *x, int16_t *y,
+                                                 void *cuda_stream);
 
 /* ------------------------------------------------------------------------
  * Island GA of one rescheduling point.

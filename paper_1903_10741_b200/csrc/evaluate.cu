@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
 // key (ties by gene index).  Warp per chromosome; ranks by a bitonic sort of
 // the keys in shared memory (rank_keys_warp).
 __global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32_t NP, int32_t O, int64_t count,
-                                                                uint64_t seed, int64_t first_id,
+                                                                uint64_t seed, int64_t first_id, int64_t row,
                                                                 int8_t *x, int16_t *y) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -206,10 +206,10 @@ __global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32
     for (int g = lane; g < K; g += 32) {
       u32x4 rx = philox((RNG_INIT_X << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
       u32x4 ry = philox((RNG_INIT_Y << 24) | (uint32_t)(g >> 2), indiv, 0u, island, k0, k1);
-      x[c * K + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
+      x[c * row + g] = (int8_t)bounded(word_of(rx, g & 3), (uint32_t)O);
       buf[g] = ((unsigned long long)word_of(ry, g & 3) << 32) | (uint32_t)g;
     }
-    rank_keys_warp(buf, K, NP, lane, y + c * K);
+    rank_keys_warp(buf, K, NP, lane, y + c * row);
   }
 }
 
@@ -275,7 +275,7 @@ ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, 
                : launch_typed<uint16_t, false>(st, a, scr, s, launches);
 }
 
-ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id,
+ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id, int64_t row,
                                     int8_t *x, int16_t *y, cudaStream_t s) {
   if (count <= 0 || st.K == 0) return FFS_OK;
   int NP = 64;
@@ -293,7 +293,7 @@ ffs_status launch_random_population(const State &st, int64_t count, uint64_t see
   int64_t cap = (int64_t)st.num_sms * 8;
   if (grid > cap) grid = cap;
   random_population_kernel<<<(unsigned)grid, warps * 32, smem, s>>>(st.K, NP, st.inst->o, count, seed, first_id,
-                                                                    x, y);
+                                                                    row, x, y);
   FFS_CUDA(cudaGetLastError());
   return FFS_OK;
 }

@@ -204,7 +204,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a, OvfScratch &scr, cuda
 
 ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
                            int *launches);
-ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id,
+ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id, int64_t row,
                                     int8_t *x, int16_t *y, cudaStream_t s);
 
 // ---------------------------------------------------------------------------

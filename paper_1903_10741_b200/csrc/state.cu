@@ -672,10 +672,16 @@ ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x,
 
 ffs_status ffs_random_population(const ffs_state *h, int64_t count, uint64_t seed, int64_t first_id, int8_t *x,
                                  int16_t *y, void *stream) {
+  return ffs_random_population_strided(h, count, seed, first_id, 0, x, y, stream);
+}
+
+ffs_status ffs_random_population_strided(const ffs_state *h, int64_t count, uint64_t seed, int64_t first_id,
+                                         int64_t row, int8_t *x, int16_t *y, void *stream) {
   if (!h || count < 0 || first_id < 0) return fail(FFS_ERR_INVALID_ARG, "bad arguments");
+  if (row != 0 && row < h->v.K) return fail(FFS_ERR_INVALID_ARG, "row stride must be 0 or >= K");
   if (count > 0 && h->v.K > 0 && (!x || !y)) return fail(FFS_ERR_INVALID_ARG, "null output arrays");
   cudaSetDevice(h->v.inst->dev);
-  return launch_random_population(h->v, count, seed, first_id, x, y, (cudaStream_t)stream);
+  return launch_random_population(h->v, count, seed, first_id, row > 0 ? row : h->v.K, x, y, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -26,7 +26,7 @@ EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
     "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
-    "ffs_evaluate_host", "ffs_evaluate_strided", "ffs_brute_force", "ffs_random_population", "ffs_evolve_begin", "ffs_evolve_step",
+    "ffs_evaluate_host", "ffs_evaluate_strided", "ffs_brute_force", "ffs_random_population", "ffs_random_population_strided", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
     "ffs_run_destroy",
 ]
@@ -86,6 +86,7 @@ def lib():
             "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_strided": ([P, C.c_int64, P, P, C.c_int64, P, P, P, P, P], C.c_int),
             "ffs_random_population": ([P, C.c_int64, C.c_uint64, C.c_int64, P, P, P], C.c_int),
+            "ffs_random_population_strided": ([P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, P, P, P], C.c_int),
             "ffs_evolve_begin": ([P, C.POINTER(GAConfig), P, P], C.c_int),
             "ffs_evolve_step": ([P, C.c_int32], C.c_int),
             "ffs_evolve": ([P, C.POINTER(GAConfig), P, P], C.c_int),
@@ -126,6 +127,14 @@ def _stream(stream):
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
+
+
+def _on(stream):
+    """Context placing torch allocations (and their fills) on the stream the
+    library call is issued on, so they are ordered with it."""
+    import contextlib
+    import torch
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
 class Instance:
@@ -217,14 +226,15 @@ def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=
     count = x.shape[0] if x.dim() == 2 else (x.numel() // max(state.K, 1))
     row = x.shape[1] if (x.dim() == 2 and x.shape[1] != state.K) else 0
     dev = x.device
-    if objective is None:
-        objective = torch.empty(count, dtype=torch.int64, device=dev)
-    if total_tardiness is None:
-        total_tardiness = torch.empty(count, dtype=torch.int64, device=dev)
-    if makespan is None:
-        makespan = torch.empty(count, dtype=torch.int32, device=dev)
-    if with_schedule and start_out is None:
-        start_out = torch.empty((count, state.cells), dtype=torch.int32, device=dev)
+    with _on(stream):
+        if objective is None:
+            objective = torch.empty(count, dtype=torch.int64, device=dev)
+        if total_tardiness is None:
+            total_tardiness = torch.empty(count, dtype=torch.int64, device=dev)
+        if makespan is None:
+            makespan = torch.empty(count, dtype=torch.int32, device=dev)
+        if with_schedule and start_out is None:
+            start_out = torch.empty((count, state.cells), dtype=torch.int32, device=dev)
     n = count * (row or state.K)
     _check(lib().ffs_evaluate_strided(state.h, count, _dev_ptr(x, torch.int8, n, "x"),
                                       _dev_ptr(y, torch.int16, n, "y"), row,
@@ -278,15 +288,20 @@ def brute_force(state: State, limit: int = 1 << 34, stream=None):
     return b, ev.value, bx[:K], by[:K]
 
 
-def random_population(state: State, count: int, seed: int, first_id: int = 0, device=None, stream=None):
-    """Counter-based random chromosomes on the device."""
+def random_population(state: State, count: int, seed: int, first_id: int = 0, device=None, stream=None,
+                      row: int = 0):
+    """Counter-based random chromosomes on the device: [count, K], or
+    rows of `row` genes (zero padding; ffs_random_population_strided)."""
     import torch
     dev = torch.device("cuda", state.inst.device) if device is None else device
-    x = torch.empty((count, state.K), dtype=torch.int8, device=dev)
-    y = torch.empty((count, state.K), dtype=torch.int16, device=dev)
-    _check(lib().ffs_random_population(state.h, count, int(seed), int(first_id),
-                                       C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), _stream(stream)),
-           "ffs_random_population")
+    R = row if row else state.K
+    alloc = torch.zeros if R != state.K else torch.empty
+    with _on(stream):   # the zero fill must precede the kernel on its stream
+        x = alloc((count, R), dtype=torch.int8, device=dev)
+        y = alloc((count, R), dtype=torch.int16, device=dev)
+    _check(lib().ffs_random_population_strided(state.h, count, int(seed), int(first_id), int(row),
+                                               C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), _stream(stream)),
+           "ffs_random_population_strided")
     return x, y
 
 

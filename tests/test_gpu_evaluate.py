@@ -272,3 +272,13 @@ def test_strided_rows_match_compact(pad, path):
     for u, v in zip(ref, got):
         assert (u == v).all()
     compare(octx, st, x[:60], y[:60], n_sched=10)
+
+
+def test_random_population_strided_equals_compact():
+    wl = wlmod.config_B()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = ffs.random_population(st, 100, seed=77, first_id=5)
+    R = st.K + 13
+    xp, yp = ffs.random_population(st, 100, seed=77, first_id=5, row=R)
+    assert (xp[:, :st.K] == x).all() and (yp[:, :st.K] == y).all()
+    assert (xp[:, st.K:] == 0).all() and (yp[:, st.K:] == 0).all()
