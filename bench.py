@@ -65,17 +65,54 @@ def workload_desc(n_gpus):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """SM clocks and throttle reasons sampled DURING the timed region, through
+    NVML in-process (nvidia_ml_py; NVML is initialised once, before any timed
+    work: starting it, or an nvidia-smi process, next to running kernels was
+    measured to perturb them).  Falls back to an `nvidia-smi -lms` process."""
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    _nvml = None
+
+    @classmethod
+    def init(cls, index):
+        if cls._nvml is None:
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                cls._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+            except Exception:
+                cls._nvml = False
+        return cls._nvml
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.samples = []
+        self.lines = []
+
+    def _nvml_loop(self):
+        nv, hdl = self._nvml
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+                self.samples.append((sm, mx, [n for n, b in zip(self.NAMES, bits) if r & b]))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
 
     def __enter__(self):
-        # nvidia-smi's start-up (NVML init) can stall the GPU for milliseconds:
-        # start it and wait for its first sample BEFORE the timed region
-        self.lines = []
+        if os.environ.get("FFS_NO_CLOCKS"):   # diagnostics only
+            return self
+        if self.init(self.index):
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._t.start()
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -96,10 +133,14 @@ class ClockSampler:
         self._t.start()
         self._first.wait(timeout=10)
         time.sleep(0.2)
-        self._skip = len(self.lines)   # samples taken before the timed region
+        self._skip = len(self.lines)
         return self
 
     def __exit__(self, *a):
+        if getattr(self, "_stop", None) is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
+            return
         if self.p is not None:
             time.sleep(0.25)
             self.p.terminate()
@@ -111,8 +152,13 @@ class ClockSampler:
             self.lines = self.lines[max(self._skip - 1, 0):]
 
     def summary(self):
+        if self.samples:
+            sm = [s[0] for s in self.samples]
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                    "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(sm),
+                    "source": "nvml"}
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = self.NAMES
         for l in getattr(self, "lines", []):
             f = [v.strip() for v in l.split(",")]
             try:
@@ -234,6 +280,7 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    ClockSampler.init(local)   # NVML up before any timed work
 
     # ---- workload: plan decoded on the GPU at RS = 0, freeze at RS
     wl = wlmod.config_C()

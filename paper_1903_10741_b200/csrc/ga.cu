@@ -772,6 +772,16 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail(FFS_ERR_INVALID_ARG, "bad rank/world");
   State &st = sh->v;
   cudaSetDevice(st.inst->dev);
+  {
+    // load every kernel a generation may launch now (CUDA's lazy loading
+    // would otherwise load the migration kernels inside the 10th generation)
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, generation_kernel);
+    cudaFuncGetAttributes(&fa, replace_kernel);
+    cudaFuncGetAttributes(&fa, donor_kernel);
+    cudaFuncGetAttributes(&fa, import_kernel);
+    cudaFuncGetAttributes(&fa, trace0_kernel);
+  }
   ffs_run *h = new ffs_run();
   Run &r = h->v;
   r.st = &st;
