@@ -253,7 +253,7 @@ def latest_traffic():
     if not files:
         return None
     d = json.load(open(files[-1]))
-    return float(d["dram_bytes_per_evaluate"]), "profiles/" + os.path.basename(files[-1])
+    return float(d["dram_bytes_per_evaluate"]), "profiles/" + os.path.basename(files[-1]), d
 
 
 def run_ours(args):
@@ -538,8 +538,10 @@ def run_ours(args):
         achieved = eval_only * alg_ops
         out["roofline"] = {"bound": "alu", "achieved": achieved / 1e9, "peak": ISSUE_PEAK / 1e9,
                            "unit": "Gop/s", "frac": achieved / ISSUE_PEAK,
-                           "traffic": (latest_traffic() or (None, None))[0],
-                           "traffic_source": (latest_traffic() or (None, None))[1],
+                           "traffic": (latest_traffic() or (None, None, None))[0],
+                           "traffic_source": (latest_traffic() or (None, None, None))[1],
+                           "ncu": {k: (latest_traffic() or (None, None, {}))[2].get(k)
+                                   for k in ("kernels", "issue_active_pct", "alu_pipe_pct", "duration_us")},
                            "algorithmic_bytes": float(pop_local * (3 * K + 20)),
                            "note": "algorithmic ops (oracle-counted dispatches + power checks + delay jumps + "
                                    "profile updates per evaluation) / evaluate-kernel time, against the issue "

@@ -97,7 +97,12 @@ for rep in ("prof_eval", "prof_gen"):
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = h.index(m)
             tot += sum(float(r[i].replace(",", "")) * scale.get(units[i], 1.0) for r in rows[2:])
+        def col(m):
+            return [r[h.index(m)] for r in rows[2:]] if m in h else None
         traffic = {"kernels": [r[h.index("Kernel Name")].split("(")[0] for r in rows[2:]],
+                   "issue_active_pct": col("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "alu_pipe_pct": col("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                   "duration_us": col("gpu__time_duration.sum"),
                    "dram_bytes_per_evaluate": tot, "population": 65536,
                    "source": f"ncu --set full, gpurun_out/{tag}/prof_eval.ncu-rep (scripts/prof_eval.py 65536)"}
     out.append(f"## ncu --set full: {rep}\n")

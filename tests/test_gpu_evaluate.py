@@ -282,3 +282,14 @@ def test_random_population_strided_equals_compact():
     xp, yp = ffs.random_population(st, 100, seed=77, first_id=5, row=R)
     assert (xp[:, :st.K] == x).all() and (yp[:, :st.K] == y).all()
     assert (xp[:, st.K:] == 0).all() and (yp[:, st.K:] == 0).all()
+
+
+def test_strided_row_shorter_than_K_is_rejected():
+    wl = wlmod.config_A2()
+    octx, st, arr = both_event_ctx(wl)
+    x = torch.zeros((4, st.K - 1), dtype=torch.int8, device=DEV)
+    y = torch.zeros((4, st.K - 1), dtype=torch.int16, device=DEV)
+    with pytest.raises(ffs.FFSError):
+        ffs.evaluate(st, x, y)
+    with pytest.raises(ffs.FFSError):
+        ffs.random_population(st, 4, seed=1, row=st.K - 1)
