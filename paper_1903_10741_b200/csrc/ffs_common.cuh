@@ -56,7 +56,8 @@ struct ImageHdr {
   int32_t uniform_q;             // all Q_jsm equal
   uint32_t image_bytes;          // multiple of 16
   uint32_t lane_image_bytes;     // prefix staged by the lane-decode kernel
-  int32_t lane_mode;             // 0 bytes/general q, 1 bytes/uniform q, 2 nibble headroom (Q == 1, Q_max <= 15)
+  int32_t lane_mode;             // 0 bytes/general q, 1 bytes/uniform q, 2 headroom planes (uniform Q = q, Q_max / q <= 15)
+  int32_t lane_units;            // mode 2: Q_max / q, the number of ops that may run at once
   uint32_t off_hn0;              // u32 [hn_words0] initial headroom nibbles (mode 2)
   int32_t hn_words0;
   uint32_t off_bn0;              // u32 [bn_words0] initial blocked bits (mode 2)

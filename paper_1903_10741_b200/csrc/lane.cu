@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     for (int w = 0; w < MW; ++w) sts(mbase + ((uint32_t)w << 7), clamp3(m10[w], (uint32_t)hcap));
     {
       // host image: per 32 ticks four plane words + blocked word, tick t at bit t%32
-      const uint32_t qm = (uint32_t)h.q_max;
+      const uint32_t qm = (uint32_t)h.lane_units;   // headroom of an empty tick, in ops
       for (int tw = 0; tw < BW; ++tw) {
         const bool init = 5 * tw < h.hn_words0;
         uint32_t pr[4];

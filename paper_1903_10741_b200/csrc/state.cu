@@ -166,9 +166,13 @@ ffs_status State::build_image() {
   }
   const bool uq = qmin == qmaxv;
   // lane decode profile: nibble headroom when every Q_jsm == 1 and Q_max <= 15
-  const int lmode = (uq && qmin == 1 && in.q_max <= 15 && NJ <= 6144 && G * O <= 768) ? 2 : (uq ? 1 : 0);
+  // mode 2 when every op draws the same power q and at most 15 of them fit
+  // under Q_max: the limit is then "at most Q_max / q ops at once" and the
+  // headroom counts ops (q = 1 is the paper's Table 5 setting)
+  const int lmode = (uq && qmin >= 1 && in.q_max / qmin <= 15 && NJ <= 6144 && G * O <= 768) ? 2 : (uq ? 1 : 0);
   // lane-decode prefix (staged by the lane kernels), then warp-path tables
   H.lane_mode = lmode;
+  H.lane_units = lmode == 2 ? in.q_max / qmin : 0;
   // mode 2: 5 words (4 headroom bit planes + blocked bits) per 32 ticks;
   // modes 0/1 take the byte profile lvl0 instead
   H.hn_words0 = lmode == 2 ? (int32_t)(5 * ((Lr + 31) / 32)) : 0;
@@ -218,7 +222,7 @@ ffs_status State::build_image() {
       int64_t L = 0;
       for (auto &rq : running)
         if (rq.a <= t && t < rq.c) L += rq.q;
-      const int64_t hr = std::max<int64_t>(0, in.q_max - L);
+      const int64_t hr = std::max<int64_t>(0, (in.q_max - L) / std::max(qmin, 1));   // in ops of power q
       uint32_t *w = pl + 5 * (t >> 5);
       for (int b = 0; b < 4; ++b)
         if ((hr >> b) & 1) w[b] |= 1u << (t & 31);

@@ -227,10 +227,11 @@ def test_tile_boundary_K(n, g, path):
     compare(octx, st, x, y, n_sched=20)
 
 
-@pytest.mark.parametrize("q,q_max", [(1, 20), (2, 9), (3, 40)])
-def test_uniform_power_mode1(q, q_max, path):
-    """Uniform Q other than the mode-2 case (Q = 1, Q_max <= 15): the lane
-    kernel's byte-level mode 1."""
+@pytest.mark.parametrize("q,q_max", [(1, 20), (2, 40), (3, 50), (2, 9), (3, 40), (4, 7)])
+def test_uniform_power(q, q_max, path):
+    """Uniform Q = q: Q_max / q <= 15 takes mode 2 (headroom counted in ops of
+    power q; (2, 9), (3, 40), (4, 7): fractional remainders of Q_max / q),
+    larger ratios the byte-level mode 1."""
     wl = wlmod.gen_v1(f"U{q}", 20, 5, 3, q_max, arrivals_per_event=[5], ratios=[0.3], seed=40 + q)
     arr = wl.original_instance()
     arr = dict(arr, Q=np.full_like(arr["Q"], q))
