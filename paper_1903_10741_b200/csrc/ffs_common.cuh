@@ -148,11 +148,14 @@ struct State {
   // lane-decode path geometry (valid when lane_ok)
   bool lane_ok = false;
   bool lane_disabled = false;        // FFS_DISABLE_LANE set: force the warp path
+  bool ord_xs_disabled = false;      // FFS_ORDER_NO_XS set: order kernel without x staging
   int32_t lane_hcap = 0;             // profile slots per chromosome (multiple of 32)
   int32_t lane_wpt = 0;              // 32-bit state words per thread
   int lane_warps_per_cta = 0, lane_ctas_per_sm = 1;
   size_t lane_smem = 0;
-  size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0;   // order kernel (32 warps per CTA)
+  size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0, ord_xs_bytes = 0;
+  bool ord_xs = false;   // order kernel stages x rows (ord_smem + ord_xs_bytes fits)
+  // ^ order kernel (32 warps per CTA)
   int32_t max_pending = 0;                                   // most pending genes of one job
   int ord_ctas_per_sm = 1;
   OvfScratch scratch;

@@ -184,11 +184,14 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 }
 
 // BULK (row % 16 == 0, 16-B aligned bases -- the GA's padded population):
-// each warp stages its chromosome's whole y row into pmv and x row into xs
-// with two TMA bulk copies (one elected lane, per-warp mbarrier) instead of
+// each warp stages its chromosome's whole y row into pmv
+// with one TMA bulk copy (one elected lane, per-warp mbarrier) instead of
 // per-lane global loads; pass A then reads y from shared memory and writes
 // the prefix minima over it in place.
-template <bool BULK, int SCAN>
+// XS: the warp also stages the chromosome's machines (x row) in shared memory
+// during pass A (TMA under BULK); without it (long rows whose staging would
+// not fit in 227 KB) pass D reads them from global memory one tile ahead.
+template <bool BULK, int SCAN, bool XS>
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
@@ -201,13 +204,13 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
   const uint32_t h16s = smem_u32(h16), ords = smem_u32(ord);   // shared-window addresses
   // CTA-shared copies of the per-gene table base and the segment-head bits,
-  // and per-warp staging of the chromosome's machines (read once, in pass A)
+  // and (XS) per-warp staging of the chromosome's machines
   unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
   // gene table TRANSPOSED inside each 128-gene tile: gene 128t + 4l + k at
   // 128t + 32k + l, so pass D's reads (lane l, gene k) hit 32 distinct banks
   uint32_t *gtab = (uint32_t *)tail;
   uint32_t *headS = gtab + 128 * NT;
-  uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;
+  uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;   // XS only
   for (int i = threadIdx.x; i < K; i += blockDim.x)
     gtab[(i & ~127) | ((i & 3) << 5) | ((i >> 2) & 31)] = __ldg(a.gbase + i);
   for (int i = threadIdx.x; i < 4 * NT; i += blockDim.x) headS[i] = i < ((K + 31) >> 5) ? __ldg(a.head + i) : 0u;
@@ -226,17 +229,18 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       const int16_t *yr = a.y + (a.first + c) * a.row;
       const int8_t *xr = a.x + (a.first + c) * a.row;
       if (BULK && lane == 0) {
-        const uint32_t yb = (uint32_t)a.row * 2u, xb = (uint32_t)a.row;
+        const uint32_t yb = (uint32_t)a.row * 2u, xb = XS ? (uint32_t)a.row : 0u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the previous row's generic writes
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(yb + xb) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          smem_u32(pmv)),
                      "l"(yr), "r"(yb), "r"(bar)
                      : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(xs)),
-                     "l"(xr), "r"(xb), "r"(bar)
-                     : "memory");
+        if (XS)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(xs)),
+                       "l"(xr), "r"(xb), "r"(bar)
+                       : "memory");
       }
       // hist/start are indexed by u = K - pm (descending prefix minimum)
       for (int i = lane; i < ((K + 511) >> 9) << 8; i += 32) hist[i] = 0u;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       uint32_t hq = 0, xq = 0;
       if (!BULK) {
         load_quad<false>(yr, headS, K, 4 * lane, yq, hq);
-        load_xquad(xr, K, 4 * lane, xq);
+        if (XS) load_xquad(xr, K, 4 * lane, xq);
       }
       auto tileA = [&](const int t, auto fullc) {
         constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
@@ -268,10 +272,10 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           h = hq;
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = yq[k];
-          *(uint32_t *)(xs + g0) = xq;
+          if (XS) *(uint32_t *)(xs + g0) = xq;
           if (t + 1 < NT) {
             load_quad<false>(yr, headS, K, g0 + 128, yq, hq);
-            load_xquad(xr, K, g0 + 128, xq);
+            if (XS) load_xquad(xr, K, g0 + 128, xq);
           }
         }
         pm_quad<SCAN>(y, h, carry, lane, pm);
@@ -355,6 +359,20 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       // ---- pass D: a leader at g ranks start[u(g)]; the genes after it in its
       // run follow consecutively: rank(g) = base + g with base = start - g_leader
       int carry_b = 0;
+      // the lane's four machines of tile t (!XS): one aligned word of a padded
+      // row (BULK), else bytes; loaded one tile ahead to hide the latency
+      auto loadx = [&](const int t) {
+        const int g0 = (t << 7) + 4 * lane;
+        uint32_t v = 0u;
+        if (XS) {
+        } else if (BULK) {
+          if (g0 < K) v = __ldg((const uint32_t *)(xr + g0));
+        } else {
+          load_xquad(xr, K, g0, v);
+        }
+        return v;
+      };
+      uint32_t xnext = loadx(0);
       auto tileD = [&](const int t, auto fullc) {
         constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
         const int g0 = (t << 7) + 4 * lane;
@@ -374,14 +392,19 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         const int inb = __shfl_sync(FULL, lastb, lb ? 31 - __clz(lb) : 0);
         int base = lb ? inb : carry_b;
         const int tb = (int)(t << 7) + lane;   // transposed gene-table column of gene k: tb + 32k
+        uint32_t xw = xnext;
+        if (XS)
+          xw = *(const uint32_t *)(xs + g0);
+        else if (t + 1 < NT)
+          xnext = loadx(t + 1);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int g = g0 + k;
           base = ((lm >> k) & 1u) ? bk[k] : base;
           if (FT)
-            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + (uint32_t)xs[g]);
+            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + ((xw >> (8 * k)) & 0xFFu));
           else
-            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + (uint32_t)xs[g]);
+            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + ((xw >> (8 * k)) & 0xFFu));
         }
         if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
       };
@@ -982,22 +1005,20 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   // genes can span - 1 (pm_quad)
   const int span = (st.max_pending + 2) / 4 + 1;
   const int scan = span <= 4 ? 2 : span <= 8 ? 3 : 5;
-  void (*okern)(OrdArgs) = nullptr, (*okern_v)(OrdArgs) = nullptr;
-  static size_t attr_o[6] = {0, 0, 0, 0, 0, 0};
-  ffs_status e = FFS_OK;
-  if (scan == 2) {
-    okern = order_warp_kernel<false, 2>; okern_v = order_warp_kernel<true, 2>;
-    e = smem_attr(okern, st.ord_smem, attr_o[0]);
-    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[1]);
-  } else if (scan == 3) {
-    okern = order_warp_kernel<false, 3>; okern_v = order_warp_kernel<true, 3>;
-    e = smem_attr(okern, st.ord_smem, attr_o[2]);
-    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[3]);
-  } else {
-    okern = order_warp_kernel<false, 5>; okern_v = order_warp_kernel<true, 5>;
-    e = smem_attr(okern, st.ord_smem, attr_o[4]);
-    if (e == FFS_OK) e = smem_attr(okern_v, st.ord_smem, attr_o[5]);
-  }
+  // [scan 2/3/5][XS][BULK]
+  static void (*const okerns[3][2][2])(OrdArgs) = {
+      {{order_warp_kernel<false, 2, false>, order_warp_kernel<true, 2, false>},
+       {order_warp_kernel<false, 2, true>, order_warp_kernel<true, 2, true>}},
+      {{order_warp_kernel<false, 3, false>, order_warp_kernel<true, 3, false>},
+       {order_warp_kernel<false, 3, true>, order_warp_kernel<true, 3, true>}},
+      {{order_warp_kernel<false, 5, false>, order_warp_kernel<true, 5, false>},
+       {order_warp_kernel<false, 5, true>, order_warp_kernel<true, 5, true>}}};
+  static size_t attr_o[3][2][2] = {};
+  const int si = scan == 2 ? 0 : scan == 3 ? 1 : 2, xi = st.ord_xs ? 1 : 0;
+  void (*okern)(OrdArgs) = okerns[si][xi][0], (*okern_v)(OrdArgs) = okerns[si][xi][1];
+  const size_t osm = st.ord_smem + (st.ord_xs ? st.ord_xs_bytes : 0);
+  ffs_status e = smem_attr(okern, osm, attr_o[si][xi][0]);
+  if (e == FFS_OK) e = smem_attr(okern_v, osm, attr_o[si][xi][1]);
   if (e != FFS_OK) return e;
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
@@ -1032,7 +1053,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
-    (oa.vec ? okern_v : okern)<<<(unsigned)og, 1024, st.ord_smem, s>>>(oa);
+    (oa.vec ? okern_v : okern)<<<(unsigned)og, 1024, osm, s>>>(oa);
     FFS_CUDA(cudaGetLastError());
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);

@@ -322,8 +322,9 @@ ffs_status State::build_image() {
     {
       const size_t ntl = (size_t)(K + 127) / 128;
       ord_smem = 32 * (ord_hist_bytes + ord_stride + ((ntl * 128 * 2 + 15) & ~(size_t)15)) +   // per warp
-                 ntl * 128 * 4 + ntl * 16 +                                                      // gtab (transposed), head
-                 32 * ntl * 128;                                                                  // x staging
+                 ntl * 128 * 4 + ntl * 16;                                                       // gtab (transposed), head
+      ord_xs_bytes = 32 * ntl * 128;   // per-warp x staging, when it fits
+      ord_xs = !ord_xs_disabled && ord_smem + ord_xs_bytes + 2048 <= (size_t)kSmemLimit;
     }
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
     if (warps < 2 || hc < 32 || ord_smem + 2048 > (size_t)kSmemLimit || K > 65535) {   // + static smem
@@ -496,6 +497,7 @@ static ffs_status make_state(const ffs_instance *ih, int32_t rs, const int32_t *
   }
   st.lvl_bytes = in.q_max <= 255 ? 1 : 2;
   st.lane_disabled = getenv("FFS_DISABLE_LANE") != nullptr;
+  st.ord_xs_disabled = getenv("FFS_ORDER_NO_XS") != nullptr;   // test hook: unstaged order kernel
   cudaSetDevice(in.dev);
   ffs_status e = st.build_image();
   if (e != FFS_OK) {

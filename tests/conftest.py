@@ -27,12 +27,17 @@ def pytest_collection_modifyitems(config, items):
             it.add_marker(skip)
 
 
-@pytest.fixture(params=["lane", "warp"])
+@pytest.fixture(params=["lane", "warp", "lane_noxs"])
 def path(request, monkeypatch):
-    """Both evaluate paths: lane-per-chromosome (default when eligible) and the
-    general warp-per-chromosome kernel (FFS_DISABLE_LANE, read at state creation)."""
+    """The evaluate paths: lane-per-chromosome (default when eligible), the
+    general warp-per-chromosome kernel (FFS_DISABLE_LANE), and the lane path
+    with the order kernel's unstaged variant (FFS_ORDER_NO_XS: machines read
+    from global memory in pass D, the variant long rows take); both variables
+    are read at state creation."""
+    monkeypatch.delenv("FFS_DISABLE_LANE", raising=False)
+    monkeypatch.delenv("FFS_ORDER_NO_XS", raising=False)
     if request.param == "warp":
         monkeypatch.setenv("FFS_DISABLE_LANE", "1")
-    else:
-        monkeypatch.delenv("FFS_DISABLE_LANE", raising=False)
+    elif request.param == "lane_noxs":
+        monkeypatch.setenv("FFS_ORDER_NO_XS", "1")
     return request.param

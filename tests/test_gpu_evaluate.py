@@ -227,6 +227,30 @@ def test_tile_boundary_K(n, g, path):
     compare(octx, st, x, y, n_sched=20)
 
 
+@pytest.mark.parametrize("pad", [0, 16])
+def test_long_rows_K1000(pad, path):
+    """K = 1000 (100 jobs x 10 stages, RS = 0): the order kernel's x staging
+    does not fit beside its histograms, so the lane path takes the unstaged
+    variant; compact and 16-padded (TMA) rows."""
+    wl = wlmod.gen_v1("Cs", 100, 10, 4, 10, seed=1903)
+    a = wl.original_instance()
+    octx = orc.Ctx(fx.workload_instance(a), 0)
+    st = gpu_state(a, 0)
+    assert st.K == 1000
+    x, y = wlmod.random_chromosomes(160, st.K, 4, seed=31)
+    if pad:
+        R = (st.K + pad - 1) // pad * pad
+        xp = np.zeros((len(x), R), np.int8)
+        yp = np.zeros((len(y), R), np.int16)
+        xp[:, :st.K] = x
+        yp[:, :st.K] = y
+        got = gpu_eval(st, xp, yp)
+        oo, oT, oM, _ = octx.evaluate_batch(x, y, nthreads=8)
+        assert (got[0] == oo).all() and (got[1] == oT).all() and (got[2] == oM).all()
+    else:
+        compare(octx, st, x, y, n_sched=8)
+
+
 @pytest.mark.parametrize("q,q_max", [(1, 20), (2, 40), (3, 50), (2, 9), (3, 40), (4, 7)])
 def test_uniform_power(q, q_max, path):
     """Uniform Q = q: Q_max / q <= 15 takes mode 2 (headroom counted in ops of
