@@ -117,6 +117,7 @@ __device__ __forceinline__ bool decode(const ImageHdr &h, const unsigned char *i
     }
     int C = S + p;
     if (C > hcap) return false;
+    __syncwarp();   // every lane's reads of level / ready / mfree above precede the commit
     for (int k = lane; k < p; k += 32) w.level[S + k] = (LVL)(w.level[S + k] + q);
     w.ready[j] = C;  // every lane stores the same value: no cross-lane hazard
     w.mfree[mi] = C;

@@ -481,6 +481,15 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
     const uint4 *YA = (const uint4 *)(a.yp + (base + wa) * row), *YB = (const uint4 *)(a.yp + (base + wb) * row);
     uint4 *xa = (uint4 *)(a.xn + (base + ca) * row), *xb = (uint4 *)(a.xn + (base + cb) * row);
     uint4 *ya = (uint4 *)(a.yn + (base + ca) * row), *yb = (uint4 *)(a.yn + (base + cb) * row);
+    // the parents' rows into L2 now (HBM latency under the RNG and repair maps)
+    {
+      const int nxl = (int)((row + 127) >> 7), nyl = (int)((2 * row + 127) >> 7);
+      for (int l = lane; l < 2 * (nxl + nyl); l += 32) {
+        const int p = l >= nxl + nyl, q = l - p * (nxl + nyl);
+        const char *src = q < nxl ? (const char *)(p ? XB : XA) + 128 * q : (const char *)(p ? YB : YA) + 128 * (q - nxl);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+      }
+    }
     // the pair's three Philox blocks, one per lane 0..2, then broadcast:
     // lane 0 = crossover (a7), lanes 1, 2 = mutation of children a, b (a8)
     const u32x4 rl = philox(lane == 0 ? (RNG_XO << 24) : (RNG_MUT << 24), (uint32_t)(lane == 2 ? cb : ca), kg, I,
