@@ -112,42 +112,47 @@ struct OrdArgs {
 // prefix minima of the lane's four genes given the running min before the tile.
 // A job's pending genes (<= G of them, consecutive) span at most
 // floor((G+2)/4) + 1 lanes, so the segmented scan needs only SCAN doubling
-// steps with 2^SCAN > that span - 1 (SCAN = 2 for G <= 13).
+// steps with 2^SCAN > that span - 1 (SCAN = 2 for G <= 13).  The segment
+// structure is the same for every chromosome, so it comes from two CTA-wide
+// tables built once per launch: M = the quad's per-gene reset masks (all ones
+// iff the gene starts a segment: a job's first pending gene, or padding), and
+// dsc = the lane's scan-step enables (bit i: combine with lane - 2^i) and, in
+// bit 31, "a segment starts in an earlier lane of this tile".  A reset is an
+// OR with all ones before an unsigned min (y and the running minima are in
+// [1, INT_MAX]), so no compare / select per gene.
 template <int SCAN>
-__device__ __forceinline__ void pm_quad(const int y[4], uint32_t h, int carry, int lane, int pm[4]) {
-  // v = min over the lane's genes from its last segment head (or all four)
-  int v = y[0];
-#pragma unroll
-  for (int k = 1; k < 4; ++k) v = ((h >> k) & 1u) ? y[k] : min(v, y[k]);
-  // lanes whose quad holds a segment head; the scan of lane l only combines
-  // lanes >= the last head lane <= l (one shuffle per step)
-  const uint32_t hb = __ballot_sync(FULL, h != 0u);
-  const uint32_t below = hb & (0xFFFFFFFFu >> (31 - lane));      // head lanes <= lane
-  const int s0 = below ? 31 - __clz(below) : -1;                    // -1: no head in this tile yet
+__device__ __forceinline__ void pm_quad(const int y[4], const uint4 M, uint32_t dsc, uint32_t carry, uint32_t Z,
+                                        int pm[4]) {
+  // v = min over the lane's genes from its last segment start (or all four)
+  uint32_t v = (uint32_t)y[0];
+  v = umin(v | M.y, (uint32_t)y[1]);
+  v = umin(v | M.z, (uint32_t)y[2]);
+  v = umin(v | M.w, (uint32_t)y[3]);
 #pragma unroll
   for (int i = 0; i < SCAN; ++i) {
-    const int d = 1 << i;
-    const int vn = __shfl_up_sync(FULL, v, d);
-    if (lane - d >= s0 && lane >= d) v = min(v, vn);
+    const uint32_t vn = __shfl_up_sync(FULL, v, 1 << i);
+    if ((dsc >> i) & 1u) v = umin(v, vn);
   }
-  // exclusive value for the lane: min over lanes [s_prev, lane-1] (+ carry if
-  // no head since the tile start)
-  const int vex = __shfl_up_sync(FULL, v, 1);
-  const uint32_t bex = hb & ((1u << lane) - 1u);                    // head lanes < lane
-  int run = lane == 0 ? carry : (bex ? vex : min(vex, carry));
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    run = ((h >> k) & 1u) ? y[k] : min(run, y[k]);
-    pm[k] = run;
-  }
+  // exclusive value for the lane: min over lanes [s_prev, lane-1], plus the
+  // carry when no segment starts before the lane in this tile (Z: lane 0)
+  const uint32_t vex = __shfl_up_sync(FULL, v, 1);
+  uint32_t run = umin(vex | Z, carry | (uint32_t)((int32_t)dsc >> 31));
+  run = umin(run | M.x, (uint32_t)y[0]);
+  pm[0] = (int)run;
+  run = umin(run | M.y, (uint32_t)y[1]);
+  pm[1] = (int)run;
+  run = umin(run | M.z, (uint32_t)y[2]);
+  pm[2] = (int)run;
+  run = umin(run | M.w, (uint32_t)y[3]);
+  pm[3] = (int)run;
 }
 
 // BULK: the row was staged in shared memory (the genes g0..g0+3 are one 8-byte
 // word).  FULL: every gene of the tile is < K (no bounds tests).  y is in
-// [1, K] (a permutation), so the halves need no sign extension.
+// [1, K] (a permutation), so the halves need no sign extension; genes past
+// the end read as INT_MAX (their own segments, see the reset masks).
 template <bool BULK, bool FULL = false>
-__device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *head, int K, int g0, int y[4],
-                                          uint32_t &h) {
+__device__ __forceinline__ void load_quad(const int16_t *yr, int K, int g0, int y[4]) {
   if (BULK) {
     const uint2 w = *(const uint2 *)(yr + g0);
     const int v[4] = {(int)(w.x & 0xFFFFu), (int)(w.x >> 16), (int)(w.y & 0xFFFFu), (int)(w.y >> 16)};
@@ -156,13 +161,6 @@ __device__ __forceinline__ void load_quad(const int16_t *yr, const uint32_t *hea
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k) y[k] = (FULL || g0 + k < K) ? (int)__ldg(yr + g0 + k) : INT_MAX;
-  }
-  const uint32_t hw = (FULL || g0 < K) ? head[g0 >> 5] : 0u;
-  h = (hw >> (g0 & 31)) & 0xFu;
-  if (!FULL) {
-    // genes past the end are their own segments (never merge into valid ones)
-    const int valid = K - g0;
-    if (valid < 4) h |= (0xFu << (valid > 0 ? valid : 0)) & 0xFu;
   }
 }
 
@@ -203,17 +201,33 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
   const uint32_t h16s = smem_u32(h16), ords = smem_u32(ord);   // shared-window addresses
-  // CTA-shared copies of the per-gene table base and the segment-head bits,
-  // and (XS) per-warp staging of the chromosome's machines
+  // CTA-shared tables (the same for every chromosome): per-gene table base,
+  // segment reset masks and per-lane scan descriptors (pm_quad); and (XS)
+  // per-warp staging of the chromosome's machines
   unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
   // gene table TRANSPOSED inside each 128-gene tile: gene 128t + 4l + k at
   // 128t + 32k + l, so pass D's reads (lane l, gene k) hit 32 distinct banks
   uint32_t *gtab = (uint32_t *)tail;
-  uint32_t *headS = gtab + 128 * NT;
-  uint8_t *xs = (uint8_t *)(headS + 4 * NT) + (size_t)warp * 128 * NT;   // XS only
+  uint32_t *mtab = gtab + 128 * NT;
+  uint32_t *dtab = mtab + 128 * NT;
+  uint8_t *xs = (uint8_t *)(dtab + 32 * NT) + (size_t)warp * 128 * NT;   // XS only
   for (int i = threadIdx.x; i < K; i += blockDim.x)
     gtab[(i & ~127) | ((i & 3) << 5) | ((i >> 2) & 31)] = __ldg(a.gbase + i);
-  for (int i = threadIdx.x; i < 4 * NT; i += blockDim.x) headS[i] = i < ((K + 31) >> 5) ? __ldg(a.head + i) : 0u;
+  for (int i = threadIdx.x; i < 128 * NT; i += blockDim.x)
+    mtab[i] = (i >= K || ((__ldg(a.head + (i >> 5)) >> (i & 31)) & 1u)) ? 0xFFFFFFFFu : 0u;
+  __syncthreads();
+  for (int t = warp; t < NT; t += 32) {
+    const uint4 m = *(const uint4 *)(mtab + (t << 7) + 4 * lane);
+    const uint32_t hb = __ballot_sync(FULL, (m.x | m.y | m.z | m.w) != 0u);   // lanes holding a segment start
+    const uint32_t below = hb & (0xFFFFFFFFu >> (31 - lane));
+    const int s0 = below ? 31 - __clz(below) : -1;
+    uint32_t dsc = (hb & ((1u << lane) - 1u)) ? 0x80000000u : 0u;
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+      if (lane - (1 << i) >= s0 && lane >= (1 << i)) dsc |= 1u << i;
+    dtab[(t << 5) + lane] = dsc;
+  }
+  const uint32_t Z = lane == 0 ? 0xFFFFFFFFu : 0u;
   __shared__ __align__(8) uint64_t obar[32];
   const uint32_t bar = smem_u32(&obar[warp]);
   uint32_t phase = 0;
@@ -256,29 +270,27 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       // software pipeline (global loads): tile t+1's genes are loaded while
       // tile t is scanned
       int yq[4];
-      uint32_t hq = 0, xq = 0;
+      uint32_t xq = 0;
       if (!BULK) {
-        load_quad<false>(yr, headS, K, 4 * lane, yq, hq);
+        load_quad<false>(yr, K, 4 * lane, yq);
         if (XS) load_xquad(xr, K, 4 * lane, xq);
       }
       auto tileA = [&](const int t, auto fullc) {
         constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
         const int g0 = (t << 7) + 4 * lane;
         int y[4], pm[4];
-        uint32_t h;
         if (BULK) {
-          load_quad<true, FT>((const int16_t *)pmv, headS, K, g0, y, h);
+          load_quad<true, FT>((const int16_t *)pmv, K, g0, y);
         } else {
-          h = hq;
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = yq[k];
           if (XS) *(uint32_t *)(xs + g0) = xq;
           if (t + 1 < NT) {
-            load_quad<false>(yr, headS, K, g0 + 128, yq, hq);
+            load_quad<false>(yr, K, g0 + 128, yq);
             if (XS) load_xquad(xr, K, g0 + 128, xq);
           }
         }
-        pm_quad<SCAN>(y, h, carry, lane, pm);
+        pm_quad<SCAN>(y, *(const uint4 *)(mtab + g0), dtab[(t << 5) + lane], (uint32_t)carry, Z, pm);
         // leaders = new prefix minima (pm == y); each distinct pm is one run
         // (a leader and the non-leaders after it in its job), and a run's
         // length is stored once, by its leader, at u = K - pm: hist[u] = len

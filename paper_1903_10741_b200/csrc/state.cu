@@ -322,7 +322,7 @@ ffs_status State::build_image() {
     {
       const size_t ntl = (size_t)(K + 127) / 128;
       ord_smem = 32 * (ord_hist_bytes + ord_stride + ((ntl * 128 * 2 + 15) & ~(size_t)15)) +   // per warp
-                 ntl * 128 * 4 + ntl * 16;                                                       // gtab (transposed), head
+                 ntl * 128 * 4 * 2 + ntl * 32 * 4;                                               // gtab, mtab, dtab
       ord_xs_bytes = 32 * ntl * 128;   // per-warp x staging, when it fits
       ord_xs = !ord_xs_disabled && ord_smem + ord_xs_bytes + 2048 <= (size_t)kSmemLimit;
     }
