@@ -65,6 +65,16 @@ __device__ __forceinline__ uint32_t lds16_if(bool p, uint32_t a) {
                : "memory");
   return v;
 }
+// predicated load at a - 65536: the caller's address carries a leader flag
+// (bit 15 of a u16 key, doubled) that the offset removes
+__device__ __forceinline__ uint32_t lds16_if_flag(bool p, uint32_t a) {
+  unsigned short v = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1+-65536];\n}\n"
+               : "+h"(v)
+               : "r"(a), "r"((uint32_t)p)
+               : "memory");
+  return v;
+}
 // lane-interleaved u16 element v: word v/2, half v%2
 [[maybe_unused]] __device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
   return base + ((v >> 1) << 7) + ((v & 1u) << 1);
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
     dtab[(t << 5) + lane] = dsc;
   }
   const uint32_t Z = lane == 0 ? 0xFFFFFFFFu : 0u;
+  for (int r = K + lane; r < 4 * KQ; r += 32) ord[r] = 0;   // padding ranks (never ranked)
   __shared__ __align__(8) uint64_t obar[32];
   const uint32_t bar = smem_u32(&obar[warp]);
   uint32_t phase = 0;
@@ -314,13 +325,15 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         const int fpos = g0 + __ffs(lm) - 1;
         const uint32_t hiB = B & (0xFFFFFFFEu << lane);
         const int nxl = __shfl_sync(FULL, fpos, hiB ? __ffs(hiB) - 1 : 0);
-        if (B) {
+        {   // branch-free (B == 0: fl = ll = -1, nothing changes)
           const int fl = __ffs(B) - 1;
-          const int first = __shfl_sync(FULL, fpos, fl);
+          const int first = __shfl_sync(FULL, fpos, fl & 31);
           sts16_if(open_u >= 0 && lane == fl, h16s + 2u * (uint32_t)open_u, (uint32_t)(first - open_pos));
-          const int ll = 31 - __clz(B);
-          open_pos = __shfl_sync(FULL, g0 + 31 - __clz(lm | 1u), ll);
-          open_u = __shfl_sync(FULL, (int)lu, ll);
+          const int ll = (31 - __clz(B)) & 31;
+          const int np = __shfl_sync(FULL, g0 + 31 - __clz(lm | 1u), ll);
+          const int nu = __shfl_sync(FULL, (int)lu, ll);
+          open_pos = B ? np : open_pos;
+          open_u = B ? nu : open_u;
         }
         int nx = hiB ? nxl : -1;
 #pragma unroll
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {   // leaders only: padding genes carry u = K, no flag
           const bool ldk = (pk[k] & 0x8000u) != 0u;
-          bk[k] = (int)lds16_if(ldk, h16s + 2u * (pk[k] & 0x7FFFu)) - (g0 + k);
+          bk[k] = (int)lds16_if_flag(ldk, h16s + 2u * pk[k]) - (g0 + k);
           lastb = ldk ? bk[k] : lastb;
           lm |= (ldk ? 1u : 0u) << k;
         }
@@ -418,27 +431,26 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           else
             sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + ((xw >> (8 * k)) & 0xFFu));
         }
-        if (B) carry_b = __shfl_sync(FULL, lastb, 31 - __clz(B));
+        const int cb = __shfl_sync(FULL, lastb, (31 - __clz(B)) & 31);
+        carry_b = B ? cb : carry_b;
       };
       for (int t = 0; t + 1 < NT; ++t) tileD(t, std::true_type{});
       tileD(NT - 1, std::false_type{});
     }
     __syncthreads();
-    // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome cc
-    uint2 *dst = (uint2 *)(a.ordg + tile * (int64_t)KQ * 128);
-    const int nrows = (int)min((int64_t)32, a.count - tile * 32);
-    for (int idx = threadIdx.x; idx < KQ * 32; idx += blockDim.x) {
-      const int qd = idx >> 5, cc = idx & 31;
-      if (cc < nrows) {
-        uint2 v = *(const uint2 *)(ordb + (size_t)cc * a.ord_stride + (size_t)qd * 8);
-        const int r0 = 4 * qd;   // ranks >= K are padding: write 0 (a valid table index)
-        if (r0 + 3 >= K) {
-          if (r0 + 0 >= K) v.x &= 0xFFFF0000u;
-          if (r0 + 1 >= K) v.x &= 0x0000FFFFu;
-          if (r0 + 2 >= K) v.y &= 0xFFFF0000u;
-          if (r0 + 3 >= K) v.y &= 0x0000FFFFu;
-        }
-        dst[idx] = v;
+    // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome
+    // cc, at dst[32 q + cc]; with 32 x 32 threads, thread (warp w, lane l) moves
+    // chromosome l's elements q = w, w + 32, ... (conflict-free: the staged
+    // arrays are an odd number of 8-byte words apart).  Ranks >= K hold the
+    // zeros written at kernel start (a valid table index).
+    if (lane < a.count - tile * 32) {
+      const unsigned char *src = ordb + (size_t)lane * a.ord_stride + (size_t)warp * 8;
+      uint2 *dst = (uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + warp * 32 + lane;
+#pragma unroll 2
+      for (int qd = warp; qd < KQ; qd += 32) {
+        *dst = *(const uint2 *)src;
+        src += 256;
+        dst += 1024;
       }
     }
     __syncthreads();
