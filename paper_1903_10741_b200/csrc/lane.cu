@@ -58,9 +58,9 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {   // 
                : "memory");
 }
 __device__ __forceinline__ uint32_t lds16_if(bool p, uint32_t a) {
-  unsigned short v = 0;
+  uint32_t v = 0;   // zero-extended by the load (a 32-bit destination)
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}\n"
-               : "+h"(v)
+               : "+r"(v)
                : "r"(a), "r"((uint32_t)p)
                : "memory");
   return v;
@@ -68,9 +68,9 @@ __device__ __forceinline__ uint32_t lds16_if(bool p, uint32_t a) {
 // predicated load at a - 65536: the caller's address carries a leader flag
 // (bit 15 of a u16 key, doubled) that the offset removes
 __device__ __forceinline__ uint32_t lds16_if_flag(bool p, uint32_t a) {
-  unsigned short v = 0;
+  uint32_t v = 0;   // zero-extended by the load (a 32-bit destination)
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1+-65536];\n}\n"
-               : "+h"(v)
+               : "+r"(v)
                : "r"(a), "r"((uint32_t)p)
                : "memory");
   return v;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
                        : "memory");
       }
       // hist/start are indexed by u = K - pm (descending prefix minimum)
-      for (int i = lane; i < ((K + 511) >> 9) << 8; i += 32) hist[i] = 0u;
+      for (int i = lane; i < ((K + 511) >> 9) << 6; i += 32) ((uint4 *)hist)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncwarp();
       if (BULK) {
         while (!mbar_try(bar, phase)) {
@@ -427,9 +427,9 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const int g = g0 + k;
           base = ((lm >> k) & 1u) ? bk[k] : base;
           if (FT)
-            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + ((xw >> (8 * k)) & 0xFFu));
+            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + __byte_perm(xw, 0u, 0x4440u + k));
           else
-            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + ((xw >> (8 * k)) & 0xFFu));
+            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + __byte_perm(xw, 0u, 0x4440u + k));
         }
         const int cb = __shfl_sync(FULL, lastb, (31 - __clz(B)) & 31);
         carry_b = B ? cb : carry_b;
