@@ -140,8 +140,9 @@ __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  WarpMem<LVL> w = carve<LVL>(smem + img_bytes + (size_t)warp * a.per_warp_bytes, h, !FALLBACK, a.h_cap);
-  if (FALLBACK) w.level = (LVL *)a.lvl_global + (size_t)gw * (size_t)a.h_cap;
+  WarpMem<LVL> w = carve<LVL>(smem + img_bytes + (size_t)warp * a.per_warp_bytes, h, !FALLBACK || a.lvl_smem,
+                              a.h_cap);
+  if (FALLBACK && !a.lvl_smem) w.level = (LVL *)a.lvl_global + (size_t)gw * (size_t)a.h_cap;
   const int64_t count = FALLBACK ? (int64_t)a.ovf[0] : a.count;
   const int K = h.K;
   for (int64_t i = gw; i < count; i += nw) {
@@ -231,6 +232,16 @@ ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cu
   EvalArgs a = a0;
   a.ovf = scr.list;
   FFS_CUDA(cudaMemsetAsync(scr.list, 0, sizeof(int32_t), s));
+  FFS_CUDA(cudaMemsetAsync(scr.list2, 0, sizeof(int32_t), s));
+  // mode 2's lane path re-decodes its overflow list itself (lane_hcap2) once
+  // this state has been seen to overflow (the sticky mapped flag, read
+  // without synchronising: an overflow not yet visible here is still caught
+  // by the general fallback); the fallback then takes what is left (list2).
+  // Decided once per call: both launches below follow the same decision.
+  const bool relist = st.lane_ok && st.lane_hcap2 > st.lane_hcap && st.ovf_seen_host &&
+                      *(volatile const int32_t *)st.ovf_seen_host != 0;
+  a.relist = relist ? 1 : 0;
+  a.ovf_seen = st.ovf_seen_dev;
   if (a.count > 0 && st.lane_ok) {
     ffs_status e = launch_lane(st, a, scr, s, launches);
     if (e != FFS_OK) return e;
@@ -246,11 +257,13 @@ ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cu
     FFS_CUDA(cudaGetLastError());
     if (launches) ++*launches;
   }
-  if ((st.lane_ok ? st.lane_hcap : st.h_cap) < st.h_bound && a.count > 0) {
-    // overflow path: global-memory profile of full horizon
+  if ((st.lane_ok ? (relist ? st.lane_hcap2 : st.lane_hcap) : st.h_cap) < st.h_bound && a.count > 0) {
+    // overflow path: profile of the full proven horizon
+    if (relist) a.ovf = scr.list2;
     a.h_cap = st.h_bound;
     a.per_warp_bytes = (int32_t)st.fb_per_warp_bytes;
     a.lvl_global = scr.level;
+    a.lvl_smem = st.fb_level_smem ? 1 : 0;
     ffs_status e = set_smem_attr<LVL, SCHED, true>(st.fb_smem_bytes);
     if (e != FFS_OK) return e;
     evaluate_kernel<LVL, SCHED, true><<<(unsigned)st.num_sms, st.fb_warps_per_cta * 32, st.fb_smem_bytes, s>>>(a);
@@ -266,7 +279,7 @@ ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, 
                            int *launches) {
   int64_t fb_warps = (int64_t)st.num_sms * st.fb_warps_per_cta;
   const int32_t cap = st.lane_ok ? st.lane_hcap : st.h_cap;
-  ffs_status e = scr.ensure(a.count, cap < st.h_bound ? fb_warps * st.h_bound * st.lvl_bytes : 0);
+  ffs_status e = scr.ensure(a.count, cap < st.h_bound && !st.fb_level_smem ? fb_warps * st.h_bound * st.lvl_bytes : 0);
   if (e != FFS_OK) return e;
   const bool sched = a.start_out != nullptr;
   if (st.lvl_bytes == 1)

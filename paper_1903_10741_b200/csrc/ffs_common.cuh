@@ -79,6 +79,7 @@ struct Instance {
 // in-SMEM profile are re-decoded with a global-memory profile).
 struct OvfScratch {
   int32_t *list = nullptr;       // [1 + cap]: count, then chromosome ids
+  int32_t *list2 = nullptr;      // [1 + cap]: what the LIST re-decode still overflows
   int64_t cap = 0;
   uint16_t *ordg = nullptr;      // lane path: rank-ordered ops, [tile][K][32]
   int64_t ordg_elems = 0;
@@ -145,6 +146,11 @@ struct State {
   size_t smem_bytes = 0, per_warp_bytes = 0;
   size_t fb_smem_bytes = 0, fb_per_warp_bytes = 0;
   int fb_warps_per_cta = 4;
+  bool fb_level_smem = false;        // fallback profile in shared memory (h_bound fits)
+  bool fb_global_forced = false;     // FFS_FALLBACK_GLOBAL set: keep it in global memory
+  int32_t relist_cap = -1;           // FFS_RELIST_CAP: cap of lane_hcap2 (0: no re-decode, <0: none)
+  int32_t *ovf_seen_host = nullptr;  // mapped: nonzero once any lane decode of this state overflowed
+  int32_t *ovf_seen_dev = nullptr;
   // lane-decode path geometry (valid when lane_ok)
   bool lane_ok = false;
   bool lane_disabled = false;        // FFS_DISABLE_LANE set: force the warp path
@@ -153,6 +159,11 @@ struct State {
   int32_t lane_wpt = 0;              // 32-bit state words per thread
   int lane_warps_per_cta = 0, lane_ctas_per_sm = 1;
   size_t lane_smem = 0;
+  // mode 2's overflow re-decode (LIST launch): the same lane kernel over the
+  // overflow list with a longer horizon and fewer warps per CTA (0: none)
+  int32_t lane_hcap2 = 0, lane_wpt2 = 0;
+  int lane_warps2 = 0;
+  size_t lane_smem2 = 0;
   size_t ord_smem = 0, ord_hist_bytes = 0, ord_stride = 0, ord_xs_bytes = 0;
   bool ord_xs = false;   // order kernel stages x rows (ord_smem + ord_xs_bytes fits)
   // ^ order kernel (32 warps per CTA)
@@ -196,7 +207,11 @@ struct EvalArgs {
   const int64_t *emax;           // optional: fitness = max(*emax - obj, 0)
   int64_t *fit;
   int32_t *ovf;                  // overflow list (count at [0])
+  int32_t *ovf2;                 // LIST launch: its own overflows (count at [0])
+  int32_t *ovf_seen;             // mapped host flag, set on any overflow (may be null)
+  int32_t relist;                // lane path: launch the LIST re-decode (decided once per call)
   void *lvl_global;              // fallback: global profiles
+  int32_t lvl_smem;              // fallback: profile in shared memory instead (h_cap fits)
   int32_t h_cap;                 // slots in the profile used by this launch
   int32_t per_warp_bytes;
   const uint16_t *ordg;          // lane path

@@ -57,14 +57,6 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {   // 
                "h"((unsigned short)v), "r"((uint32_t)p)
                : "memory");
 }
-__device__ __forceinline__ uint32_t lds16_if(bool p, uint32_t a) {
-  uint32_t v = 0;   // zero-extended by the load (a 32-bit destination)
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}\n"
-               : "+r"(v)
-               : "r"(a), "r"((uint32_t)p)
-               : "memory");
-  return v;
-}
 // predicated load at a - 65536: the caller's address carries a leader flag
 // (bit 15 of a u16 key, doubled) that the offset removes
 __device__ __forceinline__ uint32_t lds16_if_flag(bool p, uint32_t a) {
@@ -838,10 +830,14 @@ __device__ __forceinline__ uint32_t clamp3(uint32_t w, uint32_t cap) {
   return o;
 }
 
-template <bool SCHED>
+// LIST: the re-decode of the chunk's overflow list a.ovf (chromosome ids;
+// entries of other chunks are skipped) with a longer horizon a.h_cap; what
+// still overflows goes to a.ovf2 for the general fallback.
+template <bool SCHED, bool LIST>
 __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_t lane_wpt) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
+  if (LIST && *(volatile const int32_t *)a.ovf == 0) return;   // nothing listed: before staging
   __shared__ uint4 ptab[8];      // by p-1: run-test multipliers (-2^a, 2^b, 2^c), p ticks at bits 15..16-p
   if (threadIdx.x < 8) {
     const int p = threadIdx.x + 1;
@@ -870,12 +866,20 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
   const uint32_t *r10 = (const uint32_t *)(smem + h.off_ready16);
   const uint32_t *m10 = (const uint32_t *)(smem + h.off_mfree16);
   const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
-  const int64_t ntile = (a.count + 31) / 32;
+  const int64_t nunits = LIST ? (int64_t)*(volatile const int32_t *)a.ovf : a.count;
+  const int64_t ntile = (nunits + 31) / 32;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; tile < ntile; tile += nw) {
-    const int64_t c = tile * 32 + lane;
-    const bool active = c < a.count;
-    const int64_t gc = a.first + c;
+  // LIST: a short list, one warp per SM first (its chain runs alone)
+  const int64_t tile0 = LIST ? (int64_t)warp * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  for (int64_t tile = tile0; tile < ntile; tile += nw) {
+    int64_t c = tile * 32 + lane, gc = a.first + c;
+    bool active = c < a.count;
+    if (LIST) {
+      gc = c < nunits ? (int64_t)a.ovf[1 + c] : -1;
+      c = gc - a.first;
+      active = gc >= 0 && c >= 0 && c < a.count;
+      if (!active) c = 0;
+    }
     // --- initial state: times clamped to the horizon (an op that cannot start
     // before it overflows either way), RUNNING ops' headroom, sentinels
     for (int w = 0; w < RW; ++w) sts(lbase + ((uint32_t)w << 7), clamp3(r10[w], (uint32_t)hcap));
@@ -907,7 +911,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       srow = a.start_out + gc * h.cells;
       for (int k = 0; k < h.cells; ++k) srow[k] = a.fstart[k];
     }
-    const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
+    // the chromosome's ranks: lane c % 32 of ordg tile c / 32
+    const uint2 *op = (const uint2 *)(a.ordg + (c >> 5) * (int64_t)KQ * 128) + (c & 31);
     const int kq_pref = active ? KQ : 0;
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
@@ -976,8 +981,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     }
     if (!active) continue;
     if (sgn < 0) {
-      int pos = atomicAdd(&a.ovf[0], 1);
-      a.ovf[1 + pos] = (int32_t)gc;
+      int32_t *ol = LIST ? a.ovf2 : a.ovf;
+      int pos = atomicAdd(&ol[0], 1);
+      ol[1 + pos] = (int32_t)gc;
+      if (!LIST && a.ovf_seen) *(volatile int32_t *)a.ovf_seen = 1;
       continue;
     }
     // Eqs. (1)-(3) over every job (R9); frozen jobs are constants of the state
@@ -1047,12 +1054,20 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
   void (*kern)(EvalArgs, int32_t) =
-      mode == 2 ? (sched ? lane_decode2_kernel<true> : lane_decode2_kernel<false>)
+      mode == 2 ? (sched ? lane_decode2_kernel<true, false> : lane_decode2_kernel<false, false>)
       : mode == 1 ? (sched ? lane_decode_kernel<1, true> : lane_decode_kernel<1, false>)
                   : (sched ? lane_decode_kernel<0, true> : lane_decode_kernel<0, false>);
   static size_t attr[6] = {0, 0, 0, 0, 0, 0};
   e = smem_attr(kern, st.lane_smem, attr[mode * 2 + (sched ? 1 : 0)]);
   if (e != FFS_OK) return e;
+  // mode 2: the overflow list's re-decode with the longer horizon lane_hcap2
+  const bool relist = mode == 2 && a0.relist;
+  void (*kern2)(EvalArgs, int32_t) = sched ? lane_decode2_kernel<true, true> : lane_decode2_kernel<false, true>;
+  if (relist) {
+    static size_t attr2[2] = {0, 0};
+    e = smem_attr(kern2, st.lane_smem2, attr2[sched ? 1 : 0]);
+    if (e != FFS_OK) return e;
+  }
   for (int64_t first = 0; first < a0.count; first += chunk) {
     EvalArgs a = a0;
     a.first = first;
@@ -1085,6 +1100,14 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     kern<<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
     FFS_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
+    if (relist) {   // launched unconditionally (no host round trip); empty list: every CTA leaves at once
+      EvalArgs b = a;
+      b.h_cap = st.lane_hcap2;
+      b.ovf2 = scr.list2;
+      kern2<<<(unsigned)st.num_sms, (unsigned)(st.lane_warps2 * 32), st.lane_smem2, s>>>(b, st.lane_wpt2);
+      FFS_CUDA(cudaGetLastError());
+      if (launches) *launches += 1;
+    }
   }
   return FFS_OK;
 }

@@ -41,8 +41,9 @@ ffs_status OvfScratch::ensure(int64_t count, int64_t level_bytes_needed) {
     free_(list);
     list = nullptr;
     int64_t c = std::max<int64_t>(count + 1, 1024);
-    ffs_status e = alloc((void **)&list, (size_t)c * sizeof(int32_t));
+    ffs_status e = alloc((void **)&list, (size_t)2 * c * sizeof(int32_t));
     if (e != FFS_OK) return e;
+    list2 = list + c;
     cap = c;
   }
   if (level_bytes_needed > level_bytes) {
@@ -60,6 +61,7 @@ void OvfScratch::release() {
   free_(level);
   free_(ordg);
   list = nullptr;
+  list2 = nullptr;
   level = nullptr;
   ordg = nullptr;
   cap = 0;
@@ -288,8 +290,12 @@ ffs_status State::build_image() {
   per_warp_bytes = per_warp(hcap, true);
   warps_per_cta = (int)std::min<int64_t>(kMaxWarpsPerCta, budget / (int64_t)per_warp_bytes);
   smem_bytes = H.image_bytes + (size_t)warps_per_cta * per_warp_bytes;
-  fb_per_warp_bytes = per_warp(0, false);
-  fb_warps_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(4, budget / (int64_t)fb_per_warp_bytes));
+  // overflow fallback over the proven horizon h_bound: its profile in shared
+  // memory when a warp's copy fits (the usual case: ~4.5 KB at config C's
+  // K = 1,000), else in global memory
+  fb_level_smem = !fb_global_forced && (int64_t)per_warp(h_bound, true) <= budget;
+  fb_per_warp_bytes = per_warp(fb_level_smem ? h_bound : 0, fb_level_smem);
+  fb_warps_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(8, budget / (int64_t)fb_per_warp_bytes));
   fb_smem_bytes = H.image_bytes + (size_t)fb_warps_per_cta * fb_per_warp_bytes;
 
   // --- lane-decode path (one lane per chromosome): eligibility and geometry
@@ -335,6 +341,21 @@ ffs_status State::build_image() {
       lane_warps_per_cta = warps;
       lane_smem = H.lane_image_bytes + (size_t)warps * lane_wpt * 128;
       lane_ctas_per_sm = 1;
+      // mode 2: chromosomes that overflow this horizon are re-decoded by the
+      // same lane kernel over the overflow list, with the longest horizon
+      // that keeps 4 warps (<= h_bound, <= 992: 10-bit times)
+      lane_hcap2 = 0;
+      if (lmode == 2 && hc < h_bound && hc < 992 && relist_cap != 0) {
+        int64_t h2 = std::min<int64_t>({(h_bound + 31) / 32 * 32, 992,
+                                        (lbudget / (128 * 4) - fixed_words - 3) / 5 * 32});
+        if (relist_cap > 0) h2 = std::min<int64_t>(h2, ((int64_t)relist_cap + 31) / 32 * 32);
+        if (h2 > hc) {
+          lane_hcap2 = (int32_t)h2;
+          lane_wpt2 = (int32_t)words(h2);
+          lane_warps2 = (int)std::min<int64_t>(8, lbudget / (words(h2) * 128));
+          lane_smem2 = H.lane_image_bytes + (size_t)lane_warps2 * lane_wpt2 * 128;
+        }
+      }
     }
   }
 
@@ -498,6 +519,8 @@ static ffs_status make_state(const ffs_instance *ih, int32_t rs, const int32_t *
   st.lvl_bytes = in.q_max <= 255 ? 1 : 2;
   st.lane_disabled = getenv("FFS_DISABLE_LANE") != nullptr;
   st.ord_xs_disabled = getenv("FFS_ORDER_NO_XS") != nullptr;   // test hook: unstaged order kernel
+  st.fb_global_forced = getenv("FFS_FALLBACK_GLOBAL") != nullptr;   // test hook: global-memory fallback profile
+  if (const char *rc = getenv("FFS_RELIST_CAP")) st.relist_cap = atoi(rc);   // test hook: 0 = no re-decode
   cudaSetDevice(in.dev);
   ffs_status e = st.build_image();
   if (e != FFS_OK) {
@@ -513,6 +536,13 @@ static ffs_status make_state(const ffs_instance *ih, int32_t rs, const int32_t *
   if (ce == cudaSuccess) ce = cudaMalloc(&st.cut_dev, (size_t)(st.cells + 1) * 4);
   if (ce == cudaSuccess)
     ce = cudaMemcpy(st.cut_dev, st.pend_before.data(), (size_t)(st.cells + 1) * 4, cudaMemcpyHostToDevice);
+  // sticky "a lane decode overflowed" flag in mapped host memory: set by the
+  // device (rare path), read by the host without synchronising (launch_typed)
+  if (ce == cudaSuccess) ce = cudaHostAlloc((void **)&st.ovf_seen_host, 4, cudaHostAllocMapped);
+  if (ce == cudaSuccess) {
+    *(volatile int32_t *)st.ovf_seen_host = 0;
+    ce = cudaHostGetDevicePointer((void **)&st.ovf_seen_dev, st.ovf_seen_host, 0);
+  }
   if (ce != cudaSuccess) {
     ffs_state_destroy(h);
     return cuda_fail(ce, "state upload");
@@ -585,6 +615,7 @@ void ffs_state_destroy(ffs_state *h) {
   if (st.fstart_dev) cudaFree(st.fstart_dev);
   if (st.cut_dev) cudaFree(st.cut_dev);
   if (st.gbase_dev) cudaFree(st.gbase_dev);
+  if (st.ovf_seen_host) cudaFreeHost(st.ovf_seen_host);
   st.scratch.release();
   st.stage.release();
   st.stage.release_streams();

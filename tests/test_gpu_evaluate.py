@@ -72,17 +72,34 @@ def test_general_power_path(path):
     compare(octx, st, x, y, n_sched=20)
 
 
-def test_overflow_path_is_exact(path):
-    """A tiny in-SMEM horizon forces the global-memory overflow path."""
+@pytest.mark.parametrize("fb", ["relist", "relist_chain", "smem", "global"])
+def test_overflow_path_is_exact(path, fb, monkeypatch):
+    """A tiny in-SMEM horizon forces the overflow paths: mode 2's lane
+    re-decode of the overflow list with a longer horizon (relist; capped at
+    96 ticks so that some chromosomes go on to the general fallback:
+    relist_chain), and the general fallback over the full proven horizon with
+    its profile in shared memory, or in global memory (FFS_FALLBACK_GLOBAL)."""
+    monkeypatch.delenv("FFS_RELIST_CAP", raising=False)
+    monkeypatch.delenv("FFS_FALLBACK_GLOBAL", raising=False)
+    if fb == "relist_chain":
+        monkeypatch.setenv("FFS_RELIST_CAP", "96")
+    elif fb in ("smem", "global"):
+        monkeypatch.setenv("FFS_RELIST_CAP", "0")
+    if fb == "global":
+        monkeypatch.setenv("FFS_FALLBACK_GLOBAL", "1")
     wl = wlmod.config_B()
     octx, st, arr = both_event_ctx(wl)
     x, y = wlmod.random_chromosomes(400, st.K, wl.o, seed=9)
     ref = gpu_eval(st, x, y, sched=True)
     st.set_horizon_cap(64)
     assert st.info()["horizon_bound"] > 64
-    got = gpu_eval(st, x, y, sched=True)
-    for u, v in zip(ref, got):
-        assert (u == v).all()
+    # the first overflowing call goes to the general fallback; it sets the
+    # state's sticky overflow flag, so the second one (relist*) re-decodes the
+    # overflow list on the lane path first
+    for _ in range(2):
+        got = gpu_eval(st, x, y, sched=True)
+        for u, v in zip(ref, got):
+            assert (u == v).all()
     compare(octx, st, x[:100], y[:100], n_sched=20)
     st.set_horizon_cap(0)
 
