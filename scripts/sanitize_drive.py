@@ -4,8 +4,8 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
     compute-sanitizer --tool racecheck python scripts/sanitize_drive.py
 
 Covers: state staging, the lane path (order kernel with and without x
-staging, both row layouts; decode modes 0/1/2), the warp path and its
-overflow fallback, random_population, the island GA (generation, replace,
+staging, both row layouts; decode modes 0/1/2; the LIST re-decode), the warp
+path and the overflow fallback, random_population, the island GA (generation, replace,
 migration, trace), the brute force.  Checks nothing itself -- the tool does."""
 import os
 import sys
@@ -56,6 +56,12 @@ def main():
         del os.environ["FFS_DISABLE_LANE"]
         st3.set_horizon_cap(64)
         evals(st3, 100, False)
+        # lane path with a tiny horizon: first call -> general fallback (smem
+        # profile), second -> LIST re-decode (the state has seen an overflow)
+        st4 = state_of(arr)
+        st4.set_horizon_cap(64)
+        evals(st4, 100, False)
+        evals(st4, 100, False)
         xh, yh = wlmod.random_chromosomes(300, st.K, wl.o, seed=5)
         ffs.evaluate_host(st, xh, yh)
     if which in ("all", "ga"):
