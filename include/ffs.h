@@ -126,9 +126,11 @@ FFS_API ffs_status ffs_state_cells(const ffs_state *st, int32_t *cell_state);
  * the compact cut of a row-major crossover point (R13).  Host [cells+1]. */
 FFS_API ffs_status ffs_state_cut_table(const ffs_state *st, int32_t *pending_before);
 /* Horizon capacity (time slots) of the in-SMEM power profile.  A chromosome
- * whose schedule outgrows it is re-decoded by the global-memory overflow
- * path with identical results.  cap <= 0 restores the automatic choice.
- * (Testing/tuning knob.) */
+ * whose schedule outgrows it is re-decoded exactly, with identical results:
+ * (uniform power, once the state has seen an overflow) first by the lane
+ * decoder over a longer horizon, then by the warp-per-chromosome fallback over
+ * the proven bound (its profile in shared memory when it fits, else global
+ * memory).  cap <= 0 restores the automatic choice.  (Testing/tuning knob.) */
 FFS_API ffs_status ffs_state_set_horizon_cap(ffs_state *st, int32_t cap);
 FFS_API ffs_status ffs_state_info(const ffs_state *st, int32_t *K, int32_t *cells, int32_t *horizon_cap,
                           int32_t *horizon_bound, int32_t *smem_bytes_per_cta);
