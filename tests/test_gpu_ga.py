@@ -142,3 +142,28 @@ def test_trajectory_parity_long_jobs():
         ga.step()
     for u, v in zip(run.population(), ga.population()):
         assert (u == v).all()
+
+
+@pytest.mark.parametrize("relist", ["on", "off"])
+def test_trajectory_parity_through_overflows(relist, monkeypatch):
+    """A tiny horizon makes many children overflow every generation: the GA's
+    evaluations go through the overflow routes (the lane re-decode once the
+    state has seen an overflow, then the general fallback; or the fallback
+    alone) and the trajectory still equals the oracle's."""
+    monkeypatch.delenv("FFS_RELIST_CAP", raising=False)
+    if relist == "off":
+        monkeypatch.setenv("FFS_RELIST_CAP", "0")
+    wl = wlmod.config_B()
+    octx, st, _ = both_event_ctx(wl)
+    st.set_horizon_cap(64)
+    G = 10
+    run = ffs.Run(st, 16, 8, 4, G, 777)
+    run.step(G)
+    ga = orc.GA(octx, 16, 8, 4, G, 777, nthreads=8)
+    for _ in range(G + 1):
+        ga.step()
+    for u, v in zip(run.population(), ga.population()):
+        assert (u == v).all()
+    tmin, tsum = ga.trace()
+    b = run.best()
+    assert (b["trace_min"] == tmin).all() and (b["trace_sum"] == tsum).all()
