@@ -131,6 +131,8 @@ template <typename LVL, bool SCHED, bool FALLBACK>
 __global__ void __launch_bounds__(1024, 1) evaluate_kernel(EvalArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
+  pdl_trigger();
+  pdl_wait();
   // the overflow fallback is launched unconditionally (no host round trip);
   // with an empty list every block leaves before staging the image
   if (FALLBACK && *(volatile const int32_t *)a.ovf == 0) return;
@@ -231,8 +233,10 @@ ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cu
                         int *launches) {
   EvalArgs a = a0;
   a.ovf = scr.list;
-  FFS_CUDA(cudaMemsetAsync(scr.list, 0, sizeof(int32_t), s));
-  FFS_CUDA(cudaMemsetAsync(scr.list2, 0, sizeof(int32_t), s));
+  if (!(a.count > 0 && st.lane_ok)) {   // the lane path's first order launch resets them
+    FFS_CUDA(cudaMemsetAsync(scr.list, 0, sizeof(int32_t), s));
+    FFS_CUDA(cudaMemsetAsync(scr.list2, 0, sizeof(int32_t), s));
+  }
   // mode 2's lane path re-decodes its overflow list itself (lane_hcap2) once
   // this state has been seen to overflow (the sticky mapped flag, read
   // without synchronising: an overflow not yet visible here is still caught
@@ -253,8 +257,8 @@ ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cu
     a.per_warp_bytes = (int32_t)st.per_warp_bytes;
     ffs_status e = set_smem_attr<LVL, SCHED, false>(st.smem_bytes);
     if (e != FFS_OK) return e;
-    evaluate_kernel<LVL, SCHED, false><<<(unsigned)grid, st.warps_per_cta * 32, st.smem_bytes, s>>>(a);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(evaluate_kernel<LVL, SCHED, false>, dim3((unsigned)grid), dim3(st.warps_per_cta * 32),
+                        st.smem_bytes, s, a));
     if (launches) ++*launches;
   }
   if ((st.lane_ok ? (relist ? st.lane_hcap2 : st.lane_hcap) : st.h_cap) < st.h_bound && a.count > 0) {
@@ -266,8 +270,8 @@ ffs_status launch_typed(const State &st, const EvalArgs &a0, OvfScratch &scr, cu
     a.lvl_smem = st.fb_level_smem ? 1 : 0;
     ffs_status e = set_smem_attr<LVL, SCHED, true>(st.fb_smem_bytes);
     if (e != FFS_OK) return e;
-    evaluate_kernel<LVL, SCHED, true><<<(unsigned)st.num_sms, st.fb_warps_per_cta * 32, st.fb_smem_bytes, s>>>(a);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(evaluate_kernel<LVL, SCHED, true>, dim3((unsigned)st.num_sms), dim3(st.fb_warps_per_cta * 32),
+                        st.fb_smem_bytes, s, a));
     if (launches) ++*launches;
   }
   return FFS_OK;

@@ -11,6 +11,29 @@
 
 namespace edffs {
 
+// Programmatic dependent launch (sm_90+): kernels of the evaluate / GA chain
+// are launched with launch_pdl, so a kernel's CTAs may start (launch, image
+// staging, table building) while the previous kernel in the stream drains.
+// Every kernel launched this way calls pdl_wait() -- in every CTA, before it
+// touches anything an earlier kernel wrote -- and pdl_trigger() early, so its
+// own successor can be scheduled.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------------------
 // Error plumbing (thread-local last error, status returns only)
 // ---------------------------------------------------------------------------

@@ -210,6 +210,8 @@ __device__ void island_trace(const int64_t *obj_isl, int tile, int real, int li,
 
 __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
                                int16_t *hy, int64_t *hobj, int64_t *hfit, TraceArgs tr) {
+  pdl_trigger();
+  pdl_wait();
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
@@ -236,6 +238,8 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
 // and remember its worst cell (R22)
 __global__ void donor_kernel(int K, int64_t row, int tile, size_t rec, const int8_t *x, const int16_t *y,
                              const int64_t *obj, const int64_t *fit, unsigned char *donor, int32_t *worst_idx) {
+  pdl_trigger();
+  pdl_wait();
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
   int b, w;
@@ -257,6 +261,8 @@ __global__ void donor_kernel(int K, int64_t row, int tile, size_t rec, const int
 __global__ void import_kernel(int K, int64_t row, int tile, size_t rec, const unsigned char *donor,
                               const unsigned char *incoming, const int32_t *worst_idx, int8_t *x, int16_t *y,
                               int64_t *obj, int64_t *fit, TraceArgs tr) {
+  pdl_trigger();
+  pdl_wait();
   const int li = blockIdx.x;
   const unsigned char *src = li == 0 ? incoming : donor + (size_t)(li - 1) * rec;
   const int64_t cw = worst_idx[li];
@@ -450,6 +456,8 @@ __device__ __forceinline__ uint4 mutate16(uint4 v, int g0, uint32_t cell, uint32
 
 __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, nwd = (K + 31) >> 5;
   const int fmb = (K + 1 + 15) & ~15;   // byte maps indexed by value 0..K (slot 0: padding genes)
@@ -728,21 +736,18 @@ static ffs_status ga_generation(Run &r) {
     attr = smem;
   }
   int64_t grid = std::min<int64_t>((g.npairs + warps - 1) / warps, (int64_t)st.num_sms * 8);
-  generation_kernel<<<(unsigned)grid, warps * 32, smem, r.s>>>(g);
-  FFS_CUDA(cudaGetLastError());
+  FFS_CUDA(launch_pdl(generation_kernel, dim3((unsigned)grid), dim3(warps * 32), smem, r.s, g));
   r.launches++;
   ffs_status e = evaluate_population(r, nb, true);
   if (e != FFS_OK) return e;
   const bool migrate = k % r.cfg.migration_interval == 0 && r.cfg.islands_total >= 2;
   TraceArgs tr{r.parts, r.tcounter, r.tmin, r.tsum, k, st.real_wt, r.nisl, migrate ? 0 : 1};
-  replace_kernel<<<r.nisl, 256, 0, r.s>>>(r.row, r.tile, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb], r.hx, r.hy,
-                                          r.hobj, r.hfit, tr);
-  FFS_CUDA(cudaGetLastError());
+  FFS_CUDA(launch_pdl(replace_kernel, dim3(r.nisl), dim3(256), 0, r.s, r.row, r.tile, r.x[nb], r.y[nb], r.obj[nb],
+                      r.fit[nb], r.hx, r.hy, r.hobj, r.hfit, tr));
   r.launches++;
   if (migrate) {
-    donor_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.x[nb], r.y[nb], r.obj[nb], r.fit[nb],
-                                          r.donor, r.worst_idx);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(donor_kernel, dim3(r.nisl), dim3(256), 0, r.s, r.K, r.row, r.tile, r.rec, r.x[nb], r.y[nb],
+                        r.obj[nb], r.fit[nb], r.donor, r.worst_idx));
     r.launches++;
     const unsigned char *incoming = r.donor + (size_t)(r.nisl - 1) * r.rec;
     if (r.cfg.world > 1) {
@@ -751,9 +756,9 @@ static ffs_status ga_generation(Run &r) {
         return fail(FFS_ERR_COMM, "allgather hook failed");
       incoming = r.recv + (size_t)((r.cfg.rank + r.cfg.world - 1) % r.cfg.world) * r.rec;
     }
-    import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.donor, incoming, r.worst_idx, r.x[nb],
-                                           r.y[nb], r.obj[nb], r.fit[nb], tr);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(import_kernel, dim3(r.nisl), dim3(256), 0, r.s, r.K, r.row, r.tile, r.rec,
+                        (const unsigned char *)r.donor, incoming, (const int32_t *)r.worst_idx, r.x[nb], r.y[nb],
+                        r.obj[nb], r.fit[nb], tr));
     r.launches++;
   }
   r.cur = nb;

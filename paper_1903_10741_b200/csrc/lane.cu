@@ -109,6 +109,7 @@ struct OrdArgs {
   uint32_t hist_bytes;     // per warp
   uint32_t ord_stride;     // bytes between staged ord arrays (8 * odd)
   uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
+  int32_t *zero0, *zero1;  // first chunk: the overflow lists' counts to reset (else null)
 };
 
 // prefix minima of the lane's four genes given the running min before the tile.
@@ -231,6 +232,14 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   }
   const uint32_t Z = lane == 0 ? 0xFFFFFFFFu : 0u;
   for (int r = K + lane; r < 4 * KQ; r += 32) ord[r] = 0;   // padding ranks (never ranked)
+  pdl_trigger();
+  pdl_wait();   // the tables above are state constants; x, y and ordg are not
+  // the call's overflow counts start at 0 (here rather than by a memset node,
+  // so the launch chain stays kernel-to-kernel; earlier readers are done)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.zero0) {
+    *a.zero0 = 0;
+    *a.zero1 = 0;
+  }
   __shared__ __align__(8) uint64_t obar[32];
   const uint32_t bar = smem_u32(&obar[warp]);
   uint32_t phase = 0;
@@ -548,6 +557,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);
+  pdl_trigger();
+  pdl_wait();
   uint32_t cm_base = smem_u32(cmask);
   pin(cm_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
@@ -837,7 +848,11 @@ template <bool SCHED, bool LIST>
 __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_t lane_wpt) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
-  if (LIST && *(volatile const int32_t *)a.ovf == 0) return;   // nothing listed: before staging
+  pdl_trigger();
+  if (LIST) {
+    pdl_wait();
+    if (*(volatile const int32_t *)a.ovf == 0) return;   // nothing listed: before staging
+  }
   __shared__ uint4 ptab[8];      // by p-1: run-test multipliers (-2^a, 2^b, 2^c), p ticks at bits 15..16-p
   if (threadIdx.x < 8) {
     const int p = threadIdx.x + 1;
@@ -847,7 +862,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     ptab[threadIdx.x] = make_uint4(0u - (1u << sa), 1u << sb, 1u << sc, ((1u << p) - 1u) << (16 - p));
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
-  stage_image(smem, a.image, img_bytes, &bar);
+  stage_image(smem, a.image, img_bytes, &bar);   // the state image: a constant of the state
+  if (!LIST) pdl_wait();
   uint32_t pt_base = smem_u32(ptab);
   pin(pt_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
@@ -1091,21 +1107,21 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.hist_bytes = (uint32_t)st.ord_hist_bytes;
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
+    oa.zero0 = first == 0 ? scr.list : nullptr;
+    oa.zero1 = first == 0 ? scr.list2 : nullptr;
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);
-    (oa.vec ? okern_v : okern)<<<(unsigned)og, 1024, osm, s>>>(oa);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(oa.vec ? okern_v : okern, dim3((unsigned)og), dim3(1024), osm, s, oa));
     const int64_t wpc = st.lane_warps_per_cta;
     int64_t lg = std::min<int64_t>((ntile + wpc - 1) / wpc, (int64_t)st.num_sms * st.lane_ctas_per_sm);
     const unsigned thr = (unsigned)(wpc * 32);
-    kern<<<(unsigned)lg, thr, st.lane_smem, s>>>(a, st.lane_wpt);
-    FFS_CUDA(cudaGetLastError());
+    FFS_CUDA(launch_pdl(kern, dim3((unsigned)lg), dim3(thr), st.lane_smem, s, a, st.lane_wpt));
     if (launches) *launches += 2;
     if (relist) {   // launched unconditionally (no host round trip); empty list: every CTA leaves at once
       EvalArgs b = a;
       b.h_cap = st.lane_hcap2;
       b.ovf2 = scr.list2;
-      kern2<<<(unsigned)st.num_sms, (unsigned)(st.lane_warps2 * 32), st.lane_smem2, s>>>(b, st.lane_wpt2);
-      FFS_CUDA(cudaGetLastError());
+      FFS_CUDA(launch_pdl(kern2, dim3((unsigned)st.num_sms), dim3((unsigned)(st.lane_warps2 * 32)), st.lane_smem2, s,
+                          b, st.lane_wpt2));
       if (launches) *launches += 1;
     }
   }
