@@ -863,7 +863,6 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
   }
   const uint32_t img_bytes = ((const ImageHdr *)a.image)->lane_image_bytes;
   stage_image(smem, a.image, img_bytes, &bar);   // the state image: a constant of the state
-  if (!LIST) pdl_wait();
   uint32_t pt_base = smem_u32(ptab);
   pin(pt_base);
   const ImageHdr &h = *(const ImageHdr *)smem;
@@ -887,6 +886,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   // LIST: a short list, one warp per SM first (its chain runs alone)
   const int64_t tile0 = LIST ? (int64_t)warp * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  bool waited = LIST;
   for (int64_t tile = tile0; tile < ntile; tile += nw) {
     int64_t c = tile * 32 + lane, gc = a.first + c;
     bool active = c < a.count;
@@ -921,6 +921,13 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       sts(pl_base + ((uint32_t)(4 * BW) << 7), 0u);   // dummy group past the horizon: blocked
       sts(bb_base + ((uint32_t)BW << 7), 0xFFFFFFFFu);
       sts(bb_base + ((uint32_t)(BW + 1) << 7), 0xFFFFFFFFu);
+    }
+    // the lane state above comes from the image; ordg, x and the outputs
+    // belong to earlier kernels (first tile: its initialisation overlapped
+    // the predecessor's drain)
+    if (!LIST && !waited) {
+      pdl_wait();
+      waited = true;
     }
     int32_t *srow = nullptr;
     if (SCHED && active) {
@@ -1023,6 +1030,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     if (a.cmax) a.cmax[gc] = cm;
     if (a.fit) a.fit[gc] = fitness_word(h.real_wt, *a.emax, obj);   // Eq. (13)
   }
+  if (!waited) pdl_wait();   // warps without a tile: the grid still completes after its predecessor
 }
 
 template <typename KERN>
