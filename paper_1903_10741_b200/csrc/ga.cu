@@ -214,20 +214,47 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
   pdl_wait();
   const int li = blockIdx.x;
   const int64_t base = (int64_t)li * tile;
+  __shared__ long long s_hist[2];   // the island's elite record: fitness, objective (before this generation)
+  if (threadIdx.x == 0) {
+    s_hist[0] = hfit[li];
+    s_hist[1] = hobj[li];
+  }
   int b, w;
-  island_best_worst(fit + base, tile, b, w);
+  island_best_worst(fit + base, tile, b, w);   // (its barriers publish s_hist)
   const int64_t cb = base + b, cw = base + w;
   int8_t *hxr = hx + (int64_t)li * row;
   int16_t *hyr = hy + (int64_t)li * row;
-  const bool upd = fit[cb] > hfit[li];
-  __syncthreads();
-  if (upd) {
-    copy_row(hxr, hyr, x + cb * row, y + cb * row, row);
-    if (threadIdx.x == 0) { hobj[li] = obj[cb]; hfit[li] = fit[cb]; }
+  const int64_t fb = fit[cb];
+  const bool upd = fb > s_hist[0];   // strict improvement (R21)
+  // one pass: worst <- (upd ? best : elite), elite <- best when upd (the old
+  // two-pass order, elite first then worst <- elite, gives the same rows)
+  {
+    const int8_t *sx = upd ? x + cb * row : hxr;
+    const int16_t *sy = upd ? y + cb * row : hyr;
+    int8_t *dx = x + cw * row;
+    int16_t *dy = y + cw * row;
+    const int nx = (int)(row >> 4), ny = (int)(row >> 3);
+    for (int i = threadIdx.x; i < nx + ny; i += blockDim.x) {
+      if (i < nx) {
+        const uint4 v = ((const uint4 *)sx)[i];
+        ((uint4 *)dx)[i] = v;
+        if (upd) ((uint4 *)hxr)[i] = v;
+      } else {
+        const uint4 v = ((const uint4 *)sy)[i - nx];
+        ((uint4 *)dy)[i - nx] = v;
+        if (upd) ((uint4 *)hyr)[i - nx] = v;
+      }
+    }
   }
-  __syncthreads();
-  copy_row(x + cw * row, y + cw * row, hxr, hyr, row);
-  if (threadIdx.x == 0) { obj[cw] = hobj[li]; fit[cw] = hfit[li]; }
+  if (threadIdx.x == 0) {
+    const int64_t ob = upd ? obj[cb] : (int64_t)s_hist[1], fv = upd ? fb : (int64_t)s_hist[0];
+    if (upd) {
+      hobj[li] = ob;
+      hfit[li] = fv;
+    }
+    obj[cw] = ob;
+    fit[cw] = fv;
+  }
   if (tr.on) {   // no migration this generation: the trace is final now
     __syncthreads();
     island_trace(obj + base, tile, tr.real, li, tr.nisl, tr.parts, tr.counter, tr.tmin, tr.tsum, tr.k);
