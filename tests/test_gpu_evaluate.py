@@ -335,3 +335,26 @@ def test_strided_row_shorter_than_K_is_rejected():
         ffs.evaluate(st, x, y)
     with pytest.raises(ffs.FFSError):
         ffs.random_population(st, 4, seed=1, row=st.K - 1)
+
+
+def test_evaluate_host_long_rows_through_overflows():
+    """K = 1,000 through ffs_evaluate_host (4 chunks on two streams): ~1% of
+    the chromosomes overflow the lane horizon (416 ticks) and are re-decoded
+    (the general fallback on the first call, the LIST re-decode after); the
+    host results equal the device call and, on the overflowed chromosomes
+    and a random sample, the oracle."""
+    wl = wlmod.gen_v1("Cs", 100, 10, 4, 10, seed=1903)
+    a = wl.original_instance()
+    octx = orc.Ctx(fx.workload_instance(a), 0)
+    st = gpu_state(a, 0)
+    cap = st.info()["horizon_cap"]
+    x, y = wlmod.random_chromosomes(33001, st.K, 4, seed=41)
+    for _ in range(2):   # first call: fallback only; second: the state has seen an overflow
+        obj, T, M = ffs.evaluate_host(st, x, y)
+        ref = gpu_eval(st, x, y)
+        assert (obj == ref[0]).all() and (T == ref[1]).all() and (M == ref[2]).all()
+    over = np.flatnonzero(M > cap)
+    assert len(over) > 0
+    idx = np.concatenate([over[:48], np.random.default_rng(2).choice(len(x), 16, replace=False)])
+    oo, oT, oM, _ = octx.evaluate_batch(x[idx], y[idx], nthreads=8)
+    assert (obj[idx] == oo).all() and (T[idx] == oT).all() and (M[idx] == oM).all()
