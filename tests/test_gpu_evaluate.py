@@ -218,6 +218,31 @@ def test_full_size_sampled_parity(path):
     assert bool((ysort == torch.arange(1, st.K + 1, device=y.device, dtype=torch.int32)).all())
 
 
+def test_multi_chunk_equals_per_chunk():
+    """Above 2^17 chromosomes the lane path runs in chunks (order + decode
+    per chunk, the overflow counts reset by the first chunk's order kernel,
+    kernels chained by programmatic dependent launch): a 140,000-chromosome
+    call (padded rows, as the GA) equals the same rows evaluated in two
+    separate calls, and the oracle on a sample across the chunk boundary."""
+    wl = wlmod.config_C()
+    octx, st, arr = both_event_ctx(wl)
+    KP = (st.K + 15) // 16 * 16
+    n = 140_000
+    x, y = ffs.random_population(st, n, seed=77, row=KP)
+    obj, T, M, _ = ffs.evaluate(st, x, y)
+    cut = 131_072
+    o1, T1, M1, _ = ffs.evaluate(st, x[:cut], y[:cut])
+    o2, T2, M2, _ = ffs.evaluate(st, x[cut:], y[cut:])
+    torch.cuda.synchronize()
+    assert bool((obj == torch.cat([o1, o2])).all()) and bool((T == torch.cat([T1, T2])).all())
+    assert bool((M == torch.cat([M1, M2])).all())
+    idx = np.concatenate([np.arange(cut - 8, cut + 8), np.random.default_rng(3).choice(n, 16, replace=False)])
+    xs, ys = x[:, :st.K].cpu().numpy()[idx], y[:, :st.K].cpu().numpy()[idx]
+    oo, oT, oM, _ = octx.evaluate_batch(xs, ys, nthreads=8)
+    assert (obj.cpu().numpy()[idx] == oo).all()
+    assert (T.cpu().numpy()[idx] == oT).all() and (M.cpu().numpy()[idx] == oM).all()
+
+
 @pytest.mark.parametrize("g,n,o,q_max", [(16, 12, 3, 5), (40, 5, 2, 4), (70, 3, 2, 3)])
 def test_long_jobs(g, n, o, q_max, path):
     """Jobs with up to G pending genes span more lanes of the order kernel's
