@@ -219,13 +219,7 @@ __global__ void __launch_bounds__(256) random_population_kernel(int32_t K, int32
 
 template <typename LVL, bool SCHED, bool FB>
 ffs_status set_smem_attr(size_t bytes) {
-  static size_t done = 0;
-  if (bytes > done) {
-    FFS_CUDA(cudaFuncSetAttribute(evaluate_kernel<LVL, SCHED, FB>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    done = bytes;
-  }
-  return FFS_OK;
+  return ensure_smem_attr((const void *)evaluate_kernel<LVL, SCHED, FB>, bytes);
 }
 
 template <typename LVL, bool SCHED>
@@ -301,11 +295,9 @@ ffs_status launch_random_population(const State &st, int64_t count, uint64_t see
   const int warps = (int)std::min<size_t>(8, (size_t)kSmemLimit / ((size_t)NP * 8));
   if (warps < 1) return fail(FFS_ERR_INVALID_ARG, "K too large for random_population");
   size_t smem = (size_t)warps * NP * 8;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    FFS_CUDA(cudaFuncSetAttribute(random_population_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr = smem;
+  if (smem > 48 * 1024) {
+    ffs_status e = ensure_smem_attr((const void *)random_population_kernel, smem);
+    if (e != FFS_OK) return e;
   }
   int64_t grid = (count + warps - 1) / warps;
   int64_t cap = (int64_t)st.num_sms * 8;

@@ -244,6 +244,11 @@ struct EvalArgs {
 
 ffs_status launch_lane(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s, int *launches);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) when `bytes` exceeds what
+// was set before for this kernel on the current device (the attribute lives
+// in the device context; the cache is keyed by kernel and device, thread-safe)
+ffs_status ensure_smem_attr(const void *kernel, size_t bytes);
+
 ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
                            int *launches);
 ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id, int64_t row,

@@ -757,10 +757,9 @@ static ffs_status ga_generation(Run &r) {
   g.xn = r.x[nb]; g.yn = r.y[nb];
   const int warps = 8;
   size_t smem = (size_t)warps * gen_smem_per_warp(r.K);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    FFS_CUDA(cudaFuncSetAttribute(generation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+  if (smem > 48 * 1024) {
+    ffs_status ea = ensure_smem_attr((const void *)generation_kernel, smem);
+    if (ea != FFS_OK) return ea;
   }
   // 4 waves of 4 CTAs per SM: finer balancing of the pairs' uneven costs
   // than 2 waves (0.509 -> 0.505 ms per GA step), less launch work than 7

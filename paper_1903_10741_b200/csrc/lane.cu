@@ -1034,12 +1034,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
 }
 
 template <typename KERN>
-ffs_status smem_attr(KERN k, size_t bytes, size_t &done) {
-  if (bytes > done) {
-    FFS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    done = bytes;
-  }
-  return FFS_OK;
+ffs_status smem_attr(KERN k, size_t bytes) {
+  return ensure_smem_attr((const void *)k, bytes);
 }
 
 }  // namespace
@@ -1068,12 +1064,11 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
        {order_warp_kernel<false, 3, true>, order_warp_kernel<true, 3, true>}},
       {{order_warp_kernel<false, 5, false>, order_warp_kernel<true, 5, false>},
        {order_warp_kernel<false, 5, true>, order_warp_kernel<true, 5, true>}}};
-  static size_t attr_o[3][2][2] = {};
   const int si = scan == 2 ? 0 : scan == 3 ? 1 : 2, xi = st.ord_xs ? 1 : 0;
   void (*okern)(OrdArgs) = okerns[si][xi][0], (*okern_v)(OrdArgs) = okerns[si][xi][1];
   const size_t osm = st.ord_smem + (st.ord_xs ? st.ord_xs_bytes : 0);
-  ffs_status e = smem_attr(okern, osm, attr_o[si][xi][0]);
-  if (e == FFS_OK) e = smem_attr(okern_v, osm, attr_o[si][xi][1]);
+  ffs_status e = smem_attr(okern, osm);
+  if (e == FFS_OK) e = smem_attr(okern_v, osm);
   if (e != FFS_OK) return e;
   const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
@@ -1081,15 +1076,13 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
       mode == 2 ? (sched ? lane_decode2_kernel<true, false> : lane_decode2_kernel<false, false>)
       : mode == 1 ? (sched ? lane_decode_kernel<1, true> : lane_decode_kernel<1, false>)
                   : (sched ? lane_decode_kernel<0, true> : lane_decode_kernel<0, false>);
-  static size_t attr[6] = {0, 0, 0, 0, 0, 0};
-  e = smem_attr(kern, st.lane_smem, attr[mode * 2 + (sched ? 1 : 0)]);
+  e = smem_attr(kern, st.lane_smem);
   if (e != FFS_OK) return e;
   // mode 2: the overflow list's re-decode with the longer horizon lane_hcap2
   const bool relist = mode == 2 && a0.relist;
   void (*kern2)(EvalArgs, int32_t) = sched ? lane_decode2_kernel<true, true> : lane_decode2_kernel<false, true>;
   if (relist) {
-    static size_t attr2[2] = {0, 0};
-    e = smem_attr(kern2, st.lane_smem2, attr2[sched ? 1 : 0]);
+    e = smem_attr(kern2, st.lane_smem2);
     if (e != FFS_OK) return e;
   }
   for (int64_t first = 0; first < a0.count; first += chunk) {

@@ -5,6 +5,8 @@
 // else PENDING (reading R7); every op of a new job is PENDING.  RUNNING ops
 // keep their machine busy and draw power until C (R3).
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -67,6 +69,20 @@ void OvfScratch::release() {
   cap = 0;
   level_bytes = 0;
   ordg_elems = 0;
+}
+
+ffs_status ensure_smem_attr(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  FFS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &d = done[{kernel, dev}];
+  if (bytes > d) {
+    FFS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    d = bytes;
+  }
+  return FFS_OK;
 }
 
 void pool_keep(int dev) {
