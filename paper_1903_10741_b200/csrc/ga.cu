@@ -784,9 +784,17 @@ static ffs_status ga_generation(Run &r) {
         return fail(FFS_ERR_COMM, "allgather hook failed");
       incoming = r.recv + (size_t)((r.cfg.rank + r.cfg.world - 1) % r.cfg.world) * r.rec;
     }
-    FFS_CUDA(launch_pdl(import_kernel, dim3(r.nisl), dim3(256), 0, r.s, r.K, r.row, r.tile, r.rec,
-                        (const unsigned char *)r.donor, incoming, (const int32_t *)r.worst_idx, r.x[nb], r.y[nb],
-                        r.obj[nb], r.fit[nb], tr));
+    if (r.cfg.world > 1) {
+      // after the allgather hook (another library's stream work): plain
+      // stream order, no programmatic overlap with anything before it
+      import_kernel<<<r.nisl, 256, 0, r.s>>>(r.K, r.row, r.tile, r.rec, r.donor, incoming, r.worst_idx, r.x[nb],
+                                             r.y[nb], r.obj[nb], r.fit[nb], tr);
+      FFS_CUDA(cudaGetLastError());
+    } else {
+      FFS_CUDA(launch_pdl(import_kernel, dim3(r.nisl), dim3(256), 0, r.s, r.K, r.row, r.tile, r.rec,
+                          (const unsigned char *)r.donor, incoming, (const int32_t *)r.worst_idx, r.x[nb], r.y[nb],
+                          r.obj[nb], r.fit[nb], tr));
+    }
     r.launches++;
   }
   r.cur = nb;
