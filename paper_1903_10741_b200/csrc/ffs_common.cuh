@@ -19,6 +19,10 @@ namespace edffs {
 // own successor can be scheduled.  Both are no-ops without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// launches on this thread that must NOT overlap what precedes them in their
+// stream (e.g. the first kernel after a cross-stream event wait): launch_pdl
+// uses plain stream order for that many launches
+inline thread_local int t_plain_launches = 0;
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -31,6 +35,10 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (t_plain_launches > 0) {
+    --t_plain_launches;
+    cfg.numAttrs = 0;
+  }
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 

@@ -708,7 +708,9 @@ ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x,
     }
     FFS_CUDA(cudaEventRecord(hs.ev[c], hs.copy));
     FFS_CUDA(cudaStreamWaitEvent(hs.comp, hs.ev[c], 0));
+    t_plain_launches = 1;   // the chunk's first kernel follows the copy-stream event: plain order
     ffs_status rc = ffs_evaluate(h, n, hs.x + g0, hs.y + g0, hs.obj + a0, hs.T + a0, hs.M + a0, nullptr, hs.comp);
+    t_plain_launches = 0;
     if (rc != FFS_OK) return rc;
     if (objective)
       FFS_CUDA(cudaMemcpyAsync(objective + a0, hs.obj + a0, (size_t)n * 8, cudaMemcpyDeviceToHost, hs.comp));
