@@ -644,6 +644,171 @@ void or_mutate(const or_ctx *c, int32_t *X, int32_t *Y, const uint32_t *rx,
   }
 }
 
+/* Generation-0 priorities: "y_js(k) is also generated randomly from
+ * the range starting from 1 to the amount of unassigned operations ... and
+ * the value of each element is unique".  Each gene draws a random key; y of
+ * gene gi = 1 + the number of genes h whose key is smaller, or equal with
+ * h < gi (ties by gene index), i.e. the rank of the key. */
+void or_init_ranks(int32_t K, const uint32_t *keys, int32_t *y) {
+  for (int gi = 0; gi < K; ++gi) {
+    int rank = 0;
+    for (int h = 0; h < K; ++h)
+      if (keys[h] < keys[gi] || (keys[h] == keys[gi] && h < gi)) ++rank;
+    y[gi] = rank + 1;
+  }
+}
+
+/* largest fitness, ties -> lowest index (R21, R28) */
+int32_t or_argmax_fitness(const double *fit, int32_t n) {
+  int32_t b = 0;
+  for (int32_t i = 1; i < n; ++i) if (fit[i] > fit[b]) b = i;
+  return b;
+}
+/* smallest fitness, ties -> lowest index (R21) */
+int32_t or_argmin_fitness(const double *fit, int32_t n) {
+  int32_t w = 0;
+  for (int32_t i = 1; i < n; ++i) if (fit[i] < fit[w]) w = i;
+  return w;
+}
+
+/* Local asteroid selection: "every individual compares its fitness
+ * with its four neighbours ... the individual with the largest fitness
+ * replaces it".  Tournament over self, N, S, E, W, torus inside the island
+ * tile (R17), strictly larger wins so ties go to the earlier of that order
+ * (R18).  fit: one island tile [h*w] row-major; winner[cell] = tile index. */
+void or_select(const double *fit, int32_t w, int32_t h, int32_t *winner) {
+  for (int row = 0; row < h; ++row)
+    for (int col = 0; col < w; ++col) {
+      int nb[5] = {row * w + col,                      /* self */
+                   ((row + h - 1) % h) * w + col,      /* N: row above */
+                   ((row + 1) % h) * w + col,          /* S: row below */
+                   row * w + (col + 1) % w,            /* E: next column */
+                   row * w + (col + w - 1) % w};       /* W: previous column */
+      int best = nb[0];
+      for (int t = 1; t < 5; ++t) if (fit[nb[t]] > fit[best]) best = nb[t];
+      winner[row * w + col] = best;
+    }
+}
+
+/* One island's breeding from the selected winners (R19, R20):
+ * cells (r,2c) and (r,2c+1) of the winner grid pair up; the pair's crossover
+ * fires iff xo_fire < xo_threshold (R16) at row-major cut
+ * p = 1 + floor(xo_cut * (cells-1) / 2^32) (R13), else both winners are copied;
+ * then every cell i mutates iff mut_fire[i] < mut_threshold, with gene draws
+ * mut_x[i*K ..] and the Y swap of genes a = floor(mut_a*K/2^32),
+ * b = floor(mut_b*(K-1)/2^32) (+1 if b >= a).
+ * PX/PY: the island's snapshot [tile*cells]; X/Y: its new cells. */
+void or_breed(const or_ctx *c, int32_t w, int32_t h, const int32_t *PX, const int32_t *PY,
+              const int32_t *winner, const or_breed_draws *d, int32_t *X, int32_t *Y) {
+  int K = c->K, o = c->in.o, cells = c->cells, tile = w * h;
+  for (int row = 0; row < h; ++row)
+    for (int cp = 0; cp < w / 2; ++cp) {
+      int a = row * w + 2 * cp, b = a + 1, pair = row * (w / 2) + cp;
+      const int32_t *XA = PX + (size_t)winner[a] * cells, *YA = PY + (size_t)winner[a] * cells;
+      const int32_t *XB = PX + (size_t)winner[b] * cells, *YB = PY + (size_t)winner[b] * cells;
+      if (d->xo_fire[pair] < d->xo_threshold) {
+        int32_t p = 1 + (int32_t)bounded(d->xo_cut[pair], (uint32_t)(cells - 1));
+        or_crossover(c, XA, YA, XB, YB, p, X + (size_t)a * cells, Y + (size_t)a * cells,
+                     X + (size_t)b * cells, Y + (size_t)b * cells);
+      } else {
+        memcpy(X + (size_t)a * cells, XA, cells * sizeof(int32_t));
+        memcpy(Y + (size_t)a * cells, YA, cells * sizeof(int32_t));
+        memcpy(X + (size_t)b * cells, XB, cells * sizeof(int32_t));
+        memcpy(Y + (size_t)b * cells, YB, cells * sizeof(int32_t));
+      }
+    }
+  for (int i = 0; i < tile; ++i) {
+    if (d->mut_fire[i] >= d->mut_threshold) continue;
+    int32_t ga = -1, gb = -1;
+    if (K >= 2) {
+      ga = (int32_t)bounded(d->mut_a[i], (uint32_t)K);
+      gb = (int32_t)bounded(d->mut_b[i], (uint32_t)(K - 1));
+      if (gb >= ga) ++gb;
+    }
+    or_mutate(c, X + (size_t)i * cells, Y + (size_t)i * cells,
+              o >= 2 ? d->mut_x + (size_t)i * K : NULL, ga, gb);
+  }
+}
+
+/* Elitist replacement: "the best individual in history of each
+ * island replaces the worst individual of the current generation".  Per
+ * island: the history is updated from the evaluated cells only when their
+ * best fitness is strictly larger (lowest index among equals); then the
+ * worst cell (smallest fitness, lowest index) takes the history elite (R21).
+ * X/Y [nisl*tile*cells], obj/fit [nisl*tile]; HX/HY [nisl*cells], hobj/hfit [nisl]. */
+void or_replace(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y,
+                double *obj, double *fit, int32_t *HX, int32_t *HY, double *hobj, double *hfit) {
+  for (int li = 0; li < nisl; ++li) {
+    size_t base = (size_t)li * tile;
+    size_t b = base + or_argmax_fitness(fit + base, tile);
+    if (fit[b] > hfit[li]) {
+      memcpy(HX + (size_t)li * cells, X + b * cells, cells * sizeof(int32_t));
+      memcpy(HY + (size_t)li * cells, Y + b * cells, cells * sizeof(int32_t));
+      hobj[li] = obj[b]; hfit[li] = fit[b];
+    }
+    size_t wst = base + or_argmin_fitness(fit + base, tile);
+    memcpy(X + wst * cells, HX + (size_t)li * cells, cells * sizeof(int32_t));
+    memcpy(Y + wst * cells, HY + (size_t)li * cells, cells * sizeof(int32_t));
+    obj[wst] = hobj[li]; fit[wst] = hfit[li];
+  }
+}
+
+/* Single-ring migration: "the best individual of each island
+ * replaces the worst individual of its neighbouring island" on a single
+ * ring.  Synchronous (R22): every island's best and worst are found first,
+ * then island I's worst takes the best of island I-1 (mod islands_total).
+ * This shard holds nisl consecutive islands; its first island receives the
+ * last island of the previous shard (rank-1 mod world) through `allgather`
+ * (one record per rank: X[cells] int32, Y[cells] int32, obj, fit binary64);
+ * world == 1 (or no allgather) closes the ring inside the shard. */
+int or_migrate(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y,
+               double *obj, double *fit, int32_t rank, int32_t world,
+               int (*allgather)(void *user, const void *send, void *recv, size_t bytes_per_rank),
+               void *user) {
+  size_t rec = (size_t)cells * 2 * sizeof(int32_t) + 2 * sizeof(double);
+  char *donors = (char *)malloc(rec * nisl);
+  int *worst = (int *)malloc(nisl * sizeof(int));
+  for (int li = 0; li < nisl; ++li) {       /* snapshot first: synchronous */
+    size_t base = (size_t)li * tile;
+    size_t b = base + or_argmax_fitness(fit + base, tile);
+    char *d = donors + rec * li;
+    memcpy(d, X + b * cells, cells * sizeof(int32_t));
+    memcpy(d + cells * sizeof(int32_t), Y + b * cells, cells * sizeof(int32_t));
+    memcpy(d + cells * 2 * sizeof(int32_t), &obj[b], sizeof(double));
+    memcpy(d + cells * 2 * sizeof(int32_t) + sizeof(double), &fit[b], sizeof(double));
+    worst[li] = (int)(base + or_argmin_fitness(fit + base, tile));
+  }
+  char *incoming = (char *)malloc(rec);
+  int st = OR_OK;
+  if (allgather && world > 1) {
+    char *all = (char *)malloc(rec * world);
+    if (allgather(user, donors + rec * (nisl - 1), all, rec) != 0) st = OR_ERR_ARG;
+    memcpy(incoming, all + rec * ((rank + world - 1) % world), rec);
+    free(all);
+  } else {
+    memcpy(incoming, donors + rec * (nisl - 1), rec);
+  }
+  if (st == OR_OK)
+    for (int li = 0; li < nisl; ++li) {
+      const char *src = li == 0 ? incoming : donors + rec * (li - 1);
+      size_t wst = (size_t)worst[li];
+      memcpy(X + wst * cells, src, cells * sizeof(int32_t));
+      memcpy(Y + wst * cells, src + cells * sizeof(int32_t), cells * sizeof(int32_t));
+      memcpy(&obj[wst], src + cells * 2 * sizeof(int32_t), sizeof(double));
+      memcpy(&fit[wst], src + cells * 2 * sizeof(int32_t) + sizeof(double), sizeof(double));
+    }
+  free(donors); free(worst); free(incoming);
+  return st;
+}
+
+/* Per-generation trace: smallest objective and the sum of all
+ * objectives, summed in cell-index order. */
+void or_trace_stats(const double *obj, int64_t n, double *mn, double *sum) {
+  double m = obj[0], s = 0.0;
+  for (int64_t i = 0; i < n; ++i) { if (obj[i] < m) m = obj[i]; s += obj[i]; }
+  *mn = m; *sum = s;
+}
+
 /* ------------------------------------------------------------------ */
 /* threaded evaluation (for baseline timing; results are per-cell)     */
 /* ------------------------------------------------------------------ */
@@ -785,22 +950,7 @@ static void evaluate_population(or_run *r) {
 }
 
 static void record_trace(or_run *r, int k) {
-  double mn = r->obj[0], sum = 0.0;      /* sum in index order */
-  for (int i = 0; i < r->nloc; ++i) { if (r->obj[i] < mn) mn = r->obj[i]; sum += r->obj[i]; }
-  r->tmin[k] = mn; r->tsum[k] = sum;
-}
-
-/* argmax fitness inside island li (ties -> lowest cell index) */
-static int island_best(const or_run *r, int li) {
-  int base = li * r->tile, b = base;
-  for (int i = base + 1; i < base + r->tile; ++i) if (r->fit[i] > r->fit[b]) b = i;
-  return b;
-}
-/* argmin fitness inside island li (ties -> lowest cell index) */
-static int island_worst(const or_run *r, int li) {
-  int base = li * r->tile, w = base;
-  for (int i = base + 1; i < base + r->tile; ++i) if (r->fit[i] < r->fit[w]) w = i;
-  return w;
+  or_trace_stats(r->obj, r->nloc, &r->tmin[k], &r->tsum[k]);
 }
 
 static void set_history(or_run *r, int li, int idx) {
@@ -815,28 +965,23 @@ static int ga_init(or_run *r) {
   int K = c->K, o = c->in.o;
   uint64_t seed = r->cfg.seed;
   uint32_t *keys = (uint32_t *)malloc((K + 1) * sizeof(uint32_t));
+  int32_t *y = (int32_t *)malloc((K + 1) * sizeof(int32_t));
   for (int li = 0; li < r->nisl; ++li) {
     uint32_t I = (uint32_t)(r->cfg.island_begin + li);
     for (int i = 0; i < r->tile; ++i) {
       int32_t *X = cellX(r, li * r->tile + i), *Y = cellY(r, li * r->tile + i);
       for (int cell = 0; cell < c->cells; ++cell) { X[cell] = -1; Y[cell] = -1; }
       /* "x_js(k) is equal to a random integer representing the target
-       * machine"; "y_js(k) is also generated randomly from the range
-       * starting from 1 to the amount of unassigned operations ... unique"
-       * (P:227): y = 1 + rank of the gene's random key. */
+       * machine"; y from the rank of a random key (or_init_ranks) */
       for (int gi = 0; gi < K; ++gi) {
         X[c->gene_cell[gi]] = (int32_t)bounded(draw(seed, 1, gi / 4, gi % 4, i, 0, I), (uint32_t)o);
         keys[gi] = draw(seed, 2, gi / 4, gi % 4, i, 0, I);
       }
-      for (int gi = 0; gi < K; ++gi) {
-        int rank = 0;
-        for (int h = 0; h < K; ++h)
-          if (keys[h] < keys[gi] || (keys[h] == keys[gi] && h < gi)) ++rank;
-        Y[c->gene_cell[gi]] = rank + 1;
-      }
+      or_init_ranks(K, keys, y);
+      for (int gi = 0; gi < K; ++gi) Y[c->gene_cell[gi]] = y[gi];
     }
   }
-  free(keys);
+  free(keys); free(y);
   /* E_max from every individual's initial objective (R23: global) */
   r->emax = 10.0;   /* placeholder so evaluate_population computes fitness */
   evaluate_population(r);
@@ -845,7 +990,9 @@ static int ga_init(or_run *r) {
   if (r->cfg.allreduce_max && r->cfg.allreduce_max(r->cfg.user, &mx) != 0) return OR_ERR_ARG;
   r->emax = or_emax_real(&mx, 1);
   for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness_real(r->obj[i], r->emax);
-  for (int li = 0; li < r->nisl; ++li) set_history(r, li, island_best(r, li));
+  /* generation 0: each island's history elite = its best cell (R27) */
+  for (int li = 0; li < r->nisl; ++li)
+    set_history(r, li, li * r->tile + or_argmax_fitness(r->fit + (size_t)li * r->tile, r->tile));
   record_trace(r, 0);
   r->gen = 0;
   return OR_OK;
@@ -853,7 +1000,7 @@ static int ga_init(or_run *r) {
 
 static int ga_generation(or_run *r, int k) {
   const or_ctx *c = r->c;
-  int K = c->K, o = c->in.o, cells = c->cells;
+  int K = c->K, cells = c->cells;
   int w = r->cfg.island_w, h = r->cfg.island_h, tile = r->tile;
   uint64_t seed = r->cfg.seed;
   size_t bytes = (size_t)r->nloc * cells * sizeof(int32_t);
@@ -863,106 +1010,53 @@ static int ga_generation(or_run *r, int k) {
   memcpy(PX, r->X, bytes); memcpy(PY, r->Y, bytes);
   memcpy(Pfit, r->fit, r->nloc * sizeof(double));
   int32_t *winner = (int32_t *)malloc(tile * sizeof(int32_t));
-  uint32_t *rx = (uint32_t *)malloc((K + 1) * sizeof(uint32_t));
+  uint32_t *xo_fire = (uint32_t *)malloc((tile / 2) * sizeof(uint32_t));
+  uint32_t *xo_cut = (uint32_t *)malloc((tile / 2) * sizeof(uint32_t));
+  uint32_t *mut_fire = (uint32_t *)malloc(tile * sizeof(uint32_t));
+  uint32_t *mut_a = (uint32_t *)malloc(tile * sizeof(uint32_t));
+  uint32_t *mut_b = (uint32_t *)malloc(tile * sizeof(uint32_t));
+  uint32_t *mut_x = (uint32_t *)calloc((size_t)tile * (K + 1), sizeof(uint32_t));
+  or_breed_draws d = {r->cfg.xo_threshold, r->cfg.mut_threshold, xo_fire, xo_cut,
+                      mut_fire, mut_a, mut_b, mut_x};
 
   for (int li = 0; li < r->nisl; ++li) {
     uint32_t I = (uint32_t)(r->cfg.island_begin + li);
-    int base = li * tile;
-    /* local asteroid selection: tournament over self, N, S, E, W
-     * (torus inside the island tile, R17); largest fitness wins, ties in
-     * that order (R18) */
-    for (int row = 0; row < h; ++row)
-      for (int col = 0; col < w; ++col) {
-        int nb[5] = {row * w + col,
-                     ((row + h - 1) % h) * w + col,
-                     ((row + 1) % h) * w + col,
-                     row * w + (col + 1) % w,
-                     row * w + (col + w - 1) % w};
-        int best = nb[0];
-        for (int t = 1; t < 5; ++t) if (Pfit[base + nb[t]] > Pfit[base + best]) best = nb[t];
-        winner[row * w + col] = best;
-      }
-    /* neighbouring paired crossover: pairs (r,2c),(r,2c+1) (R19) */
+    size_t base = (size_t)li * tile;
+    /* a6: selection on the snapshot */
+    or_select(Pfit + base, w, h, winner);
+    /* the pair's draws are keyed by its left cell, the mutation's by the
+     * cell */
     for (int row = 0; row < h; ++row)
       for (int cp = 0; cp < w / 2; ++cp) {
-        int a = row * w + 2 * cp, b = a + 1;
-        const int32_t *XA = PX + (size_t)(base + winner[a]) * cells, *YA = PY + (size_t)(base + winner[a]) * cells;
-        const int32_t *XB = PX + (size_t)(base + winner[b]) * cells, *YB = PY + (size_t)(base + winner[b]) * cells;
-        uint32_t fire = draw(seed, 3, 0, 0, (uint32_t)a, (uint32_t)k, I);
-        if (fire < r->cfg.xo_threshold) {
-          uint32_t ucut = draw(seed, 3, 0, 1, (uint32_t)a, (uint32_t)k, I);
-          int32_t p = 1 + (int32_t)bounded(ucut, (uint32_t)(cells - 1));
-          or_crossover(c, XA, YA, XB, YB, p, cellX(r, base + a), cellY(r, base + a),
-                       cellX(r, base + b), cellY(r, base + b));
-        } else {
-          memcpy(cellX(r, base + a), XA, cells * sizeof(int32_t));
-          memcpy(cellY(r, base + a), YA, cells * sizeof(int32_t));
-          memcpy(cellX(r, base + b), XB, cells * sizeof(int32_t));
-          memcpy(cellY(r, base + b), YB, cells * sizeof(int32_t));
-        }
+        uint32_t a = (uint32_t)(row * w + 2 * cp);
+        xo_fire[row * (w / 2) + cp] = draw(seed, 3, 0, 0, a, (uint32_t)k, I);
+        xo_cut[row * (w / 2) + cp] = draw(seed, 3, 0, 1, a, (uint32_t)k, I);
       }
-    /* mutation: per individual with probability p_m (R16) */
     for (int i = 0; i < tile; ++i) {
-      uint32_t fire = draw(seed, 4, 0, 0, (uint32_t)i, (uint32_t)k, I);
-      if (fire >= r->cfg.mut_threshold) continue;
-      for (int gi = 0; gi < K; ++gi) rx[gi] = draw(seed, 5, gi / 4, gi % 4, (uint32_t)i, (uint32_t)k, I);
-      int32_t ga = -1, gb = -1;
-      if (K >= 2) {
-        ga = (int32_t)bounded(draw(seed, 4, 0, 1, (uint32_t)i, (uint32_t)k, I), (uint32_t)K);
-        gb = (int32_t)bounded(draw(seed, 4, 0, 2, (uint32_t)i, (uint32_t)k, I), (uint32_t)(K - 1));
-        if (gb >= ga) ++gb;
-      }
-      or_mutate(c, cellX(r, base + i), cellY(r, base + i), o >= 2 ? rx : NULL, ga, gb);
+      mut_fire[i] = draw(seed, 4, 0, 0, (uint32_t)i, (uint32_t)k, I);
+      mut_a[i] = draw(seed, 4, 0, 1, (uint32_t)i, (uint32_t)k, I);
+      mut_b[i] = draw(seed, 4, 0, 2, (uint32_t)i, (uint32_t)k, I);
+      if (mut_fire[i] < r->cfg.mut_threshold)   /* gene draws only where read */
+        for (int gi = 0; gi < K; ++gi)
+          mut_x[(size_t)i * K + gi] = draw(seed, 5, gi / 4, gi % 4, (uint32_t)i, (uint32_t)k, I);
     }
+    /* a7 + a8: crossover + correction, then mutation */
+    or_breed(c, w, h, PX + base * cells, PY + base * cells, winner, &d,
+             cellX(r, (int)base), cellY(r, (int)base));
   }
-  free(PX); free(PY); free(Pfit); free(winner); free(rx);
+  free(PX); free(PY); free(Pfit); free(winner);
+  free(xo_fire); free(xo_cut); free(mut_fire); free(mut_a); free(mut_b); free(mut_x);
 
   evaluate_population(r);
 
-  /* elitist replacement (R21) */
-  for (int li = 0; li < r->nisl; ++li) {
-    int b = island_best(r, li);
-    if (r->fit[b] > r->hfit[li]) set_history(r, li, b);
-    int wst = island_worst(r, li);
-    memcpy(cellX(r, wst), r->HX + (size_t)li * cells, cells * sizeof(int32_t));
-    memcpy(cellY(r, wst), r->HY + (size_t)li * cells, cells * sizeof(int32_t));
-    r->obj[wst] = r->hobj[li]; r->fit[wst] = r->hfit[li];
-  }
+  /* a9: elitist replacement */
+  or_replace(r->nisl, tile, cells, r->X, r->Y, r->obj, r->fit, r->HX, r->HY, r->hobj, r->hfit);
 
-  /* single-ring migration every migration_interval generations (R22) */
+  /* a10: single-ring migration every migration_interval generations */
   if (k % r->cfg.migration_interval == 0 && r->cfg.islands_total >= 2) {
-    size_t rec = (size_t)cells * 2 * sizeof(int32_t) + 2 * sizeof(double);
-    char *donors = (char *)malloc(rec * r->nisl);
-    int *worst = (int *)malloc(r->nisl * sizeof(int));
-    for (int li = 0; li < r->nisl; ++li) {    /* snapshot first: synchronous */
-      int b = island_best(r, li);
-      char *d = donors + rec * li;
-      memcpy(d, cellX(r, b), cells * sizeof(int32_t));
-      memcpy(d + cells * sizeof(int32_t), cellY(r, b), cells * sizeof(int32_t));
-      memcpy(d + cells * 2 * sizeof(int32_t), &r->obj[b], sizeof(double));
-      memcpy(d + cells * 2 * sizeof(int32_t) + sizeof(double), &r->fit[b], sizeof(double));
-      worst[li] = island_worst(r, li);
-    }
-    /* island begin receives from global island begin-1: the last island of
-     * the previous shard (rank-1 mod world) */
-    char *incoming = (char *)malloc(rec);
-    if (r->cfg.allgather && r->cfg.world > 1) {
-      char *all = (char *)malloc(rec * r->cfg.world);
-      r->cfg.allgather(r->cfg.user, donors + rec * (r->nisl - 1), all, rec);
-      memcpy(incoming, all + rec * ((r->cfg.rank + r->cfg.world - 1) % r->cfg.world), rec);
-      free(all);
-    } else {
-      memcpy(incoming, donors + rec * (r->nisl - 1), rec);
-    }
-    for (int li = 0; li < r->nisl; ++li) {
-      const char *src = li == 0 ? incoming : donors + rec * (li - 1);
-      int wst = worst[li];
-      memcpy(cellX(r, wst), src, cells * sizeof(int32_t));
-      memcpy(cellY(r, wst), src + cells * sizeof(int32_t), cells * sizeof(int32_t));
-      memcpy(&r->obj[wst], src + cells * 2 * sizeof(int32_t), sizeof(double));
-      memcpy(&r->fit[wst], src + cells * 2 * sizeof(int32_t) + sizeof(double), sizeof(double));
-    }
-    free(donors); free(worst); free(incoming);
+    int st = or_migrate(r->nisl, tile, cells, r->X, r->Y, r->obj, r->fit, r->cfg.rank,
+                        r->cfg.world, r->cfg.allgather, r->cfg.user);
+    if (st != OR_OK) return st;
   }
   record_trace(r, k);
   r->gen = k;

@@ -17,8 +17,11 @@
  * (P:355-359), Eq. (13) + E_max rule examples, Philox Random123 KATs,
  * brute force over all (X, order) on tiny instances, exhaustive integer scan
  * for the delay rule, schedule invariants Eqs. (4)-(10).
- * "parity unpinned": the GA trajectory as a whole (the paper prints only run
- * statistics) -- pinned only by its operators and invariants.
+ * GA steps (init ranks, selection, breeding order, replacement, ring
+ * migration across a shard boundary, trace): hand-derived goldens
+ * (tests/golden/ga_ops.json).  The GA trajectory as a
+ * whole has no printed value in the paper; it is the composition of those
+ * pinned steps.
  */
 #ifndef FFS_ORACLE_H
 #define FFS_ORACLE_H
@@ -155,6 +158,39 @@ void or_crossover(const or_ctx *c, const int32_t *XA, const int32_t *YA,
  * (x <- (x + 1 + floor(rx*(o-1)/2^32)) mod o), then swap Y at genes a, b. */
 void or_mutate(const or_ctx *c, int32_t *X, int32_t *Y, const uint32_t *rx,
                int32_t gene_a, int32_t gene_b);
+
+/* ---- GA steps on one generation; the GA below runs
+ * exactly these functions, so their goldens (tests/golden/ga_ops.json) pin
+ * the trajectory's operators.  Fitness/objective values are binary64. ---- */
+/* y of gene gi = 1 + rank of keys[gi] ascending, ties by gene index */
+void or_init_ranks(int32_t K, const uint32_t *keys, int32_t *y);
+/* largest / smallest fitness, ties -> lowest index */
+int32_t or_argmax_fitness(const double *fit, int32_t n);
+int32_t or_argmin_fitness(const double *fit, int32_t n);
+/* asteroid selection on one island tile fit[h*w] (R17, R18) */
+void or_select(const double *fit, int32_t w, int32_t h, int32_t *winner);
+/* the draws one island's breeding consumes */
+typedef struct {
+  uint32_t xo_threshold, mut_threshold;
+  const uint32_t *xo_fire, *xo_cut;             /* [tile/2], pair = row*(w/2)+c   */
+  const uint32_t *mut_fire, *mut_a, *mut_b;     /* [tile]                         */
+  const uint32_t *mut_x;                        /* [tile*K], row i read iff cell i mutates */
+} or_breed_draws;
+/* crossover + correction of the winner pairs, then mutation (
+ * R13-R16, R19, R20).  PX/PY: island snapshot [tile*cells]; X/Y: new cells. */
+void or_breed(const or_ctx *c, int32_t w, int32_t h, const int32_t *PX, const int32_t *PY,
+              const int32_t *winner, const or_breed_draws *d, int32_t *X, int32_t *Y);
+/* elitist replacement over nisl islands of `tile` cells of `cells` ints (R21) */
+void or_replace(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y,
+                double *obj, double *fit, int32_t *HX, int32_t *HY, double *hobj, double *hfit);
+/* synchronous single-ring migration of this shard's nisl islands (
+ * R22); cross-shard record = X[cells] int32, Y[cells] int32, obj, fit */
+int or_migrate(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y,
+               double *obj, double *fit, int32_t rank, int32_t world,
+               int (*allgather)(void *user, const void *send, void *recv, size_t bytes_per_rank),
+               void *user);
+/* trace: min objective and sum in index order */
+void or_trace_stats(const double *obj, int64_t n, double *mn, double *sum);
 
 /* ---- the island GA of one rescheduling point ---- */
 typedef struct {

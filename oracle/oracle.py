@@ -52,6 +52,12 @@ _ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double))
 _ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 
 
+class _Draws(C.Structure):
+    _fields_ = [("xo_threshold", C.c_uint32), ("mut_threshold", C.c_uint32),
+                ("xo_fire", C.c_void_p), ("xo_cut", C.c_void_p), ("mut_fire", C.c_void_p),
+                ("mut_a", C.c_void_p), ("mut_b", C.c_void_p), ("mut_x", C.c_void_p)]
+
+
 class _GaCfg(C.Structure):
     _fields_ = [("island_w", C.c_int32), ("island_h", C.c_int32), ("islands_total", C.c_int32),
                 ("island_begin", C.c_int32), ("island_end", C.c_int32),
@@ -109,6 +115,15 @@ def lib():
         _lib.or_ga_history.argtypes = [P, P, P, P, P]
         _lib.or_ga_destroy.argtypes = [P]
         _lib.or_evaluate_batch.argtypes = [P, C.c_int64, P, P, P, P, P, P, C.c_int32, C.POINTER(_Cnt)]
+        _lib.or_init_ranks.argtypes = [C.c_int32, P, P]
+        _lib.or_argmax_fitness.argtypes = [P, C.c_int32]
+        _lib.or_argmin_fitness.argtypes = [P, C.c_int32]
+        _lib.or_select.argtypes = [P, C.c_int32, C.c_int32, P]
+        _lib.or_breed.argtypes = [P, C.c_int32, C.c_int32, P, P, P, C.POINTER(_Draws), P, P]
+        _lib.or_replace.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P, P, P, P]
+        _lib.or_migrate.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, P, P, C.c_int32, C.c_int32,
+                                    _ALLGATHER, P]
+        _lib.or_trace_stats.argtypes = [P, C.c_int64, P, P]
     return _lib
 
 
@@ -326,6 +341,89 @@ class Ctx:
             obj = val
         return obj, T, M, dict(dispatches=cnt.dispatches, checks=cnt.checks, jumps=cnt.jumps,
                                updates=cnt.updates)
+
+
+# ---- single GA steps (the functions the oracle GA itself runs) ----
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _u32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def init_ranks(keys):
+    """Generation-0 priorities: y = 1 + rank of the key (ties by index)."""
+    k = _u32(keys)
+    y = np.zeros(len(k), dtype=np.int32)
+    lib().or_init_ranks(len(k), _p(k), _p(y))
+    return y
+
+
+def select(fit_tile, w, h):
+    """Asteroid selection on one island tile: winner index per cell."""
+    f = _f64(fit_tile).ravel()
+    assert f.size == w * h
+    win = np.zeros(w * h, dtype=np.int32)
+    lib().or_select(_p(f), int(w), int(h), _p(win))
+    return win
+
+
+def breed(ctx: "Ctx", w, h, PX, PY, winner, xo_fire, xo_cut, mut_fire, mut_a, mut_b, mut_x,
+          xo_threshold=None, mut_threshold=None):
+    """One island's crossover + correction and mutation with explicit draws."""
+    tile = w * h
+    px, py = _i32(PX).reshape(tile, ctx.cells), _i32(PY).reshape(tile, ctx.cells)
+    arrs = [_i32(winner), _u32(xo_fire), _u32(xo_cut), _u32(mut_fire), _u32(mut_a), _u32(mut_b),
+            _u32(mut_x).reshape(tile * max(ctx.K, 1))]
+    d = _Draws(XO_090 if xo_threshold is None else xo_threshold,
+               MUT_010 if mut_threshold is None else mut_threshold,
+               *[a.ctypes.data for a in arrs[1:]])
+    X = np.zeros((tile, ctx.cells), dtype=np.int32)
+    Y = np.zeros((tile, ctx.cells), dtype=np.int32)
+    lib().or_breed(ctx.h, int(w), int(h), _p(px), _p(py), _p(arrs[0]), C.byref(d), _p(X), _p(Y))
+    return X, Y
+
+
+def replace(tile, X, Y, obj, fit, HX, HY, hobj, hfit):
+    """Elitist replacement over len(hfit) islands; arrays updated in place."""
+    nisl = len(hfit)
+    cells = X.shape[-1]
+    for a, dt in ((X, np.int32), (Y, np.int32), (HX, np.int32), (HY, np.int32),
+                  (obj, np.float64), (fit, np.float64), (hobj, np.float64), (hfit, np.float64)):
+        assert a.dtype == dt and a.flags.c_contiguous
+    lib().or_replace(nisl, int(tile), int(cells), _p(X), _p(Y), _p(obj), _p(fit), _p(HX), _p(HY),
+                     _p(hobj), _p(hfit))
+
+
+def migrate(nisl, tile, X, Y, obj, fit, rank=0, world=1, allgather=None):
+    """Synchronous ring migration of one shard's islands, in place.
+    allgather(bytes) -> list of per-rank bytes (rank-major)."""
+    cells = X.shape[-1]
+    for a, dt in ((X, np.int32), (Y, np.int32), (obj, np.float64), (fit, np.float64)):
+        assert a.dtype == dt and a.flags.c_contiguous
+    ag = _ALLGATHER()
+    if allgather is not None:
+        def _ag(user, send, recv, nbytes):
+            joined = b"".join(allgather(C.string_at(send, nbytes)))
+            C.memmove(recv, joined, len(joined))
+            return 0
+        ag = _ALLGATHER(_ag)
+    _chk(lib().or_migrate(int(nisl), int(tile), int(cells), _p(X), _p(Y), _p(obj), _p(fit),
+                          int(rank), int(world), ag, None), "migrate")
+
+
+def migration_record(x, y, obj, fit):
+    """The cross-shard record of or_migrate: X[cells] int32, Y[cells] int32, obj, fit."""
+    return (_i32(x).tobytes() + _i32(y).tobytes() + np.float64(obj).tobytes()
+            + np.float64(fit).tobytes())
+
+
+def trace_stats(obj):
+    o = _f64(obj)
+    mn, sm = C.c_double(), C.c_double()
+    lib().or_trace_stats(_p(o), len(o), C.byref(mn), C.byref(sm))
+    return mn.value, sm.value
 
 
 XO_090 = 3865470566   # floor(0.9 * 2^32)
