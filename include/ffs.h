@@ -98,7 +98,9 @@ FFS_API void ffs_instance_destroy(ffs_instance *inst);
  *   K_out: number of pending ops = genes per chromosome (g(n+n') - r, R11).
  * The canonical gene order is the pending cells in row-major order
  * (job-major, stage-minor); ffs_state_genes reports it.
- * Errors: FFS_ERR_INVALID_SCHEDULE if the plan violates Eqs. (4)-(7).
+ * Errors: FFS_ERR_INVALID_SCHEDULE if the plan violates Eqs. (4)-(7);
+ * FFS_ERR_INVALID_ARG if WT * sum T + C_max could reach 1e17 (the 64-bit
+ * objective word and its E_max = 10^a, must stay below 2^63).
  * ---------------------------------------------------------------------- */
 FFS_API ffs_status ffs_reschedule_state(const ffs_instance *inst, int32_t rs, const int32_t *orig_assign,
                                 const int32_t *orig_start, ffs_state **out, int32_t *K_out);
@@ -147,13 +149,23 @@ FFS_API void ffs_state_destroy(ffs_state *st);
  * the trace sum is a fixed-order binary64 sum.  Decoding does not depend on
  * WT.  wt: finite, >= 0.  Call before ffs_evolve_begin; a run keeps the mode
  * it started with only if the state is not switched again while it runs.
- * Errors: FFS_ERR_INVALID_ARG for a negative or non-finite wt.
+ * Errors: FFS_ERR_INVALID_ARG for a negative or non-finite wt, or one for
+ * which WT * sum T + C_max could reach 1e300 (the state is then unchanged).
  * ---------------------------------------------------------------------- */
 FFS_API ffs_status ffs_state_set_objective_weight(ffs_state *st, double wt);
 
 /* ------------------------------------------------------------------------
  * Decode + evaluate (Algorithm 1; Algorithm 2, P:273-289;
- * Eqs. (1)-(3)).  One warp per chromosome.
+ * Eqs. (1)-(3)).  Algorithm 1 runs one WARP per chromosome (a
+ * counting sort, order_warp_kernel); Algorithm 2 runs one LANE per chromosome
+ * (lane_decode*_kernel: its per-dispatch work is scalar and sequential) when
+ * the instance fits the lane decoder (P <= 8, Q_max <= 127, ...), else one
+ * warp per chromosome with a 32-tick ballot window (evaluate_kernel); the
+ * results are identical.
+ * Streams: every device-pointer call on a state shares the state's scratch
+ * (overflow lists, the order->decode buffer); a call issued on another stream
+ * than the previous call is ordered after it (event), so calls on several
+ * streams are correct but do not overlap each other.
  *   x: device int8  [count*K], machine of each gene, in [0, o-1] (X(k))
  *   y: device int16 [count*K], priorities: a permutation of 1..K per
  *      chromosome, larger = earlier (Y(k)).  Not validated.
@@ -241,7 +253,9 @@ typedef struct {
 } ffs_ga_config;
 
 /* Generation 0: initialise, evaluate, E_max (global via the
- * allreduce hook, R23), fitness (Eq. (13)), per-island history elite. */
+ * allreduce hook, R23), fitness (Eq. (13)), per-island history elite.
+ * Errors: FFS_ERR_INVALID_ARG for a bad tile/shard/rank, or world > 1
+ * without BOTH hooks. */
 FFS_API ffs_status ffs_evolve_begin(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
 /* Run `generations` more generations (selection, crossover + correction,
  * mutation, evaluation, elitist replacement, ring migration every
@@ -250,10 +264,14 @@ FFS_API ffs_status ffs_evolve_step(ffs_run *run, int32_t generations);
 /* begin + step(cfg->generations) + synchronise.  K == 0: returns a run whose
  * best is the frozen plan and whose trace is empty. */
 FFS_API ffs_status ffs_evolve(ffs_state *st, const ffs_ga_config *cfg, void *cuda_stream, ffs_run **out);
-/* Best-in-history of this shard (ties -> lowest island) and its decoded,
+/* Best-in-history of THIS SHARD (ties -> lowest island) and its decoded,
  * merged schedule.  Host outputs, any may be NULL:
  *   x [K], y [K], assign/start [(n+n')*g], trace_min/trace_sum [G+1] (local
- *   shard: min objective and sum of objectives per generation). */
+ *   shard: min objective and sum of objectives per generation).
+ * Sharded runs: the global best of the ring and the global trace
+ * are the reduction of every shard's ffs_best over the process group --
+ * min objective, ties -> lowest rank (= lowest global island), trace min of
+ * mins and sum of sums (paper_1903_10741_b200.dist.global_best). */
 FFS_API ffs_status ffs_best(ffs_run *run, int8_t *x, int16_t *y, int32_t *assign, int32_t *start,
                     int64_t *objective, int64_t *total_tardiness, int32_t *makespan,
                     int64_t *trace_min, int64_t *trace_sum);

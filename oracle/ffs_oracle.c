@@ -802,10 +802,21 @@ int or_migrate(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y
 }
 
 /* Per-generation trace: smallest objective and the sum of all
- * objectives, summed in cell-index order. */
-void or_trace_stats(const double *obj, int64_t n, double *mn, double *sum) {
+ * objectives of nisl islands of `tile` cells.  The sum (R33) is taken island
+ * by island: each island's objectives in cell order, then the island sums in
+ * island order (exact for the integer objective; for the binary64 objective
+ * of f3 it fixes the rounding). */
+void or_trace_stats(const double *obj, int64_t nisl, int32_t tile, double *mn, double *sum) {
   double m = obj[0], s = 0.0;
-  for (int64_t i = 0; i < n; ++i) { if (obj[i] < m) m = obj[i]; s += obj[i]; }
+  for (int64_t li = 0; li < nisl; ++li) {
+    double p = 0.0;
+    for (int32_t i = 0; i < tile; ++i) {
+      double v = obj[li * tile + i];
+      if (v < m) m = v;
+      p += v;
+    }
+    s += p;
+  }
   *mn = m; *sum = s;
 }
 
@@ -819,6 +830,7 @@ typedef struct {
   const int8_t *xc; const int16_t *yc;   /* compact form [count*K]  */
   int64_t *obj, *sumT, *cmax;
   double *value;                 /* Eq. (1) in the context's weight mode */
+  int32_t *start;                /* optional merged schedule [count*cells] */
   or_counters cnt;
   int status;
 } eval_job;
@@ -843,7 +855,8 @@ static void *eval_worker(void *arg) {
       Xi = X; Yi = Y;
     }
     int64_t T, M, O;
-    int st = or_decode(c, Xi, Yi, NULL, NULL, NULL, &T, &M, &O, &w->cnt);
+    int32_t *Si = w->start ? w->start + i * c->cells : NULL;
+    int st = or_decode(c, Xi, Yi, NULL, NULL, Si, &T, &M, &O, &w->cnt);
     if (st != OR_OK) { w->status = st; break; }
     if (w->obj) w->obj[i] = O;
     if (w->sumT) w->sumT[i] = T;
@@ -856,7 +869,7 @@ static void *eval_worker(void *arg) {
 
 static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int32_t *Ys,
                     const int8_t *xc, const int16_t *yc, int64_t *obj, int64_t *sumT,
-                    int64_t *cmax, double *value, int nthreads, or_counters *cnt) {
+                    int64_t *cmax, double *value, int32_t *start, int nthreads, or_counters *cnt) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > count) nthreads = count > 0 ? (int)count : 1;
   eval_job *jobs = (eval_job *)calloc(nthreads, sizeof(eval_job));
@@ -867,6 +880,7 @@ static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int
     jobs[t].end = count * (t + 1) / nthreads;
     jobs[t].Xs = Xs; jobs[t].Ys = Ys; jobs[t].xc = xc; jobs[t].yc = yc;
     jobs[t].obj = obj; jobs[t].sumT = sumT; jobs[t].cmax = cmax; jobs[t].value = value;
+    jobs[t].start = start;
   }
   if (nthreads == 1) eval_worker(&jobs[0]);
   else {
@@ -888,7 +902,13 @@ static int run_eval(const or_ctx *c, int64_t count, const int32_t *Xs, const int
 int or_evaluate_batch(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
                       int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
                       double *value, int32_t nthreads, or_counters *cnt) {
-  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, value, nthreads, cnt);
+  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, value, NULL, nthreads, cnt);
+}
+
+int or_evaluate_batch_schedule(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
+                               int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
+                               int32_t *start, int32_t nthreads) {
+  return run_eval(c, count, NULL, NULL, x, y, objective, sum_tardiness, makespan, NULL, start, nthreads, NULL);
 }
 
 /* ------------------------------------------------------------------ */
@@ -945,12 +965,12 @@ static int32_t *cellX(or_run *r, int idx) { return r->X + (size_t)idx * r->c->ce
 static int32_t *cellY(or_run *r, int idx) { return r->Y + (size_t)idx * r->c->cells; }
 
 static void evaluate_population(or_run *r) {
-  run_eval(r->c, r->nloc, r->X, r->Y, NULL, NULL, NULL, NULL, NULL, r->obj, r->cfg.nthreads, NULL);
+  run_eval(r->c, r->nloc, r->X, r->Y, NULL, NULL, NULL, NULL, NULL, r->obj, NULL, r->cfg.nthreads, NULL);
   for (int i = 0; i < r->nloc; ++i) r->fit[i] = or_fitness_real(r->obj[i], r->emax);
 }
 
 static void record_trace(or_run *r, int k) {
-  or_trace_stats(r->obj, r->nloc, &r->tmin[k], &r->tsum[k]);
+  or_trace_stats(r->obj, r->nisl, r->tile, &r->tmin[k], &r->tsum[k]);
 }
 
 static void set_history(or_run *r, int li, int idx) {

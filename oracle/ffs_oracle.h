@@ -189,8 +189,9 @@ int or_migrate(int32_t nisl, int32_t tile, int32_t cells, int32_t *X, int32_t *Y
                double *obj, double *fit, int32_t rank, int32_t world,
                int (*allgather)(void *user, const void *send, void *recv, size_t bytes_per_rank),
                void *user);
-/* trace: min objective and sum in index order */
-void or_trace_stats(const double *obj, int64_t n, double *mn, double *sum);
+/* trace: min objective and sum over nisl islands of `tile` cells, each
+ * island in cell order, then islands in order (R33) */
+void or_trace_stats(const double *obj, int64_t nisl, int32_t tile, double *mn, double *sum);
 
 /* ---- the island GA of one rescheduling point ---- */
 typedef struct {
@@ -223,8 +224,8 @@ int32_t or_ga_generation(const or_run *r);
 double or_ga_emax(const or_run *r);
 /* local shard population as compact genes (canonical order) [cells_local*K] */
 void or_ga_population(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit);
-/* local trace: per generation min objective and sum of objectives (summed in
- * cell-index order) [G+1] */
+/* local trace: per generation min objective and sum of objectives (summed
+ * per island in cell order, then islands in order, R33) [G+1] */
 void or_ga_trace(const or_run *r, double *tmin, double *tsum);
 /* per-island history elites of the shard: [islands_local*K] + obj/fit */
 void or_ga_history(const or_run *r, int8_t *x, int16_t *y, double *obj, double *fit);
@@ -235,6 +236,12 @@ void or_ga_destroy(or_run *r);
 int or_evaluate_batch(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
                       int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
                       double *value, int32_t nthreads, or_counters *cnt);
+
+/* the same with each chromosome's merged schedule start[count*cells]
+ * (Algorithm 2's start times, frozen cells copied) -- or_decode per row */
+int or_evaluate_batch_schedule(const or_ctx *c, int64_t count, const int8_t *x, const int16_t *y,
+                               int64_t *objective, int64_t *sum_tardiness, int64_t *makespan,
+                               int32_t *start, int32_t nthreads);
 
 #ifdef __cplusplus
 }

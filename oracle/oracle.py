@@ -115,6 +115,7 @@ def lib():
         _lib.or_ga_history.argtypes = [P, P, P, P, P]
         _lib.or_ga_destroy.argtypes = [P]
         _lib.or_evaluate_batch.argtypes = [P, C.c_int64, P, P, P, P, P, P, C.c_int32, C.POINTER(_Cnt)]
+        _lib.or_evaluate_batch_schedule.argtypes = [P, C.c_int64, P, P, P, P, P, P, C.c_int32]
         _lib.or_init_ranks.argtypes = [C.c_int32, P, P]
         _lib.or_argmax_fitness.argtypes = [P, C.c_int32]
         _lib.or_argmin_fitness.argtypes = [P, C.c_int32]
@@ -123,7 +124,7 @@ def lib():
         _lib.or_replace.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P, P, P, P]
         _lib.or_migrate.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, P, P, C.c_int32, C.c_int32,
                                     _ALLGATHER, P]
-        _lib.or_trace_stats.argtypes = [P, C.c_int64, P, P]
+        _lib.or_trace_stats.argtypes = [P, C.c_int64, C.c_int32, P, P]
     return _lib
 
 
@@ -342,6 +343,19 @@ class Ctx:
         return obj, T, M, dict(dispatches=cnt.dispatches, checks=cnt.checks, jumps=cnt.jumps,
                                updates=cnt.updates)
 
+    def evaluate_batch_schedule(self, x, y, nthreads=1):
+        """evaluate_batch plus every chromosome's merged start times [count, cells]."""
+        x = np.ascontiguousarray(x, dtype=np.int8)
+        y = np.ascontiguousarray(y, dtype=np.int16)
+        count = x.shape[0]
+        obj = np.zeros(count, dtype=np.int64)
+        T = np.zeros(count, dtype=np.int64)
+        M = np.zeros(count, dtype=np.int64)
+        S = np.zeros((count, self.cells), dtype=np.int32)
+        _chk(lib().or_evaluate_batch_schedule(self.h, count, _p(x), _p(y), _p(obj), _p(T), _p(M), _p(S),
+                                              int(nthreads)), "evaluate_batch_schedule")
+        return obj, T, M, S
+
 
 # ---- single GA steps (the functions the oracle GA itself runs) ----
 def _f64(a):
@@ -419,10 +433,13 @@ def migration_record(x, y, obj, fit):
             + np.float64(fit).tobytes())
 
 
-def trace_stats(obj):
+def trace_stats(obj, tile=None):
+    """(min, sum) over islands of `tile` cells (default: one island), R33."""
     o = _f64(obj)
+    tile = len(o) if tile is None else int(tile)
+    assert len(o) % tile == 0
     mn, sm = C.c_double(), C.c_double()
-    lib().or_trace_stats(_p(o), len(o), C.byref(mn), C.byref(sm))
+    lib().or_trace_stats(_p(o), len(o) // tile, tile, C.byref(mn), C.byref(sm))
     return mn.value, sm.value
 
 

@@ -180,7 +180,7 @@ ffs_status ffs_brute_force(const ffs_state *h, int64_t limit, int64_t *best_obje
     a.y = dy;
     a.obj = dobj;
     a.fstart = st.fstart_dev;
-    e = launch_evaluate(st, a, st.scratch, s, nullptr);
+    e = launch_evaluate_shared(st, a, s);
     if (e != FFS_OK) break;
     argmin_kernel<<<1, 1024, 0, s>>>(dobj, n, first, dbest);
     ce = cudaGetLastError();

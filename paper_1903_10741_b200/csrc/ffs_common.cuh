@@ -121,6 +121,11 @@ struct OvfScratch {
   // runs); unset: plain cudaMalloc
   cudaStream_t pool = nullptr;
   bool pooled = false;
+  // cross-stream ordering of a state's shared scratch: `done` is recorded on
+  // `last` after every call that used it; a call on another stream waits for it
+  cudaEvent_t done = nullptr;
+  cudaStream_t last = nullptr;
+  bool used = false;
   ffs_status ensure(int64_t count, int64_t level_bytes_needed);
   ffs_status alloc(void **p, size_t bytes);
   void free_(void *p);
@@ -259,6 +264,10 @@ ffs_status ensure_smem_attr(const void *kernel, size_t bytes);
 
 ffs_status launch_evaluate(const State &st, const EvalArgs &a, OvfScratch &scr, cudaStream_t s,
                            int *launches);
+// launch_evaluate on the state's own scratch (every device-pointer call on a
+// state: ffs_evaluate*, ffs_evaluate_host's chunks, ffs_brute_force): ordered
+// after the previous such call when that one ran on another stream.
+ffs_status launch_evaluate_shared(State &st, const EvalArgs &a, cudaStream_t s);
 ffs_status launch_random_population(const State &st, int64_t count, uint64_t seed, int64_t first_id, int64_t row,
                                     int8_t *x, int16_t *y, cudaStream_t s);
 

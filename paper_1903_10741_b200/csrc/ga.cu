@@ -50,6 +50,8 @@ struct Run {
   int64_t *scal = nullptr;          // [0] emax, [1] max objective
   int64_t *tmin = nullptr, *tsum = nullptr;
   int64_t *parts = nullptr;         // [islands][2] per-island trace partials
+  int64_t *best_v = nullptr;        // ffs_best: objective, sum T of the decoded elite
+  int32_t *best_s = nullptr;        // ffs_best: its schedule [cells] + C_max
   unsigned *tcounter = nullptr;     // islands finished in the current trace
   OvfScratch scr;
   int64_t evaluations = 0;
@@ -119,12 +121,12 @@ __global__ void emax_fitness_kernel(int64_t *scal, const int64_t *obj, int64_t *
   if (real) {   // binary64 words (f3); powers of ten are exact up to 1e22
     const double mx = __longlong_as_double(scal[1]);
     double e = 10.0;
-    while (e <= mx) e *= 10.0;
+    for (int a = 1; a < 308 && e <= mx; ++a) e *= 10.0;   // bounded: objectives < 1e300 (state check)
     E = __double_as_longlong(e);
   } else {
     const int64_t mx = scal[1];
     E = 10;
-    while (E <= mx) E *= 10;
+    for (int a = 1; a < 18 && E <= mx; ++a) E *= 10;     // bounded: objectives < 1e17 (state check)
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = E;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -307,10 +309,10 @@ __global__ void import_kernel(int K, int64_t row, int tile, size_t rec, const un
 }
 
 // trace[k] = (min objective, sum of objectives).  Real-WT words (f3): the min
-// works on the words (non-negative doubles), the sum is a binary64 sum in a
-// fixed order (strided per-thread partials, a fixed shuffle tree, islands in
-// index order), so it is deterministic but rounds differently from a
-// sequential sum.
+// works on the words (non-negative doubles); the sum is the binary64 sum of
+// reading R33 -- each island's objectives in cell order, then the island sums
+// in island order -- the oracle's order, so the trace is bit-identical (the
+// integer sum is exact in any order and stays a parallel tree).
 // Block reduction of (min, sum) over v[0..n) (all threads get the result).
 __device__ void block_min_sum(const int64_t *v, int64_t n, int real, long long &mn, long long &sm) {
   __shared__ long long smin[32], ssum[32];
@@ -343,7 +345,14 @@ __device__ void block_min_sum(const int64_t *v, int64_t n, int real, long long &
       if (real) d2 += __shfl_xor_sync(FULL, d2, d);
       else s2 += __shfl_xor_sync(FULL, s2, d);
     }
-    if (threadIdx.x == 0) { smin[0] = mn; ssum[0] = real ? __double_as_longlong(d2) : s2; }
+    if (threadIdx.x == 0) {
+      if (real) {   // R33: island sums in island order
+        d2 = 0.0;
+        for (int64_t i = 0; i < n; ++i) d2 += __longlong_as_double(__ldcg((const long long *)v + 2 * i + 1));
+      }
+      smin[0] = mn;
+      ssum[0] = real ? __double_as_longlong(d2) : s2;
+    }
   }
   __syncthreads();
   mn = smin[0];
@@ -386,9 +395,10 @@ __device__ void island_trace(const int64_t *obj_isl, int tile, int real, int li,
       double d0 = 0.0;
       for (int w = 0; w < nw; ++w) {
         m0 = min(m0, smin[w]);
-        if (real) d0 += __longlong_as_double(ssum[w]);
-        else s0 += ssum[w];
+        if (!real) s0 += ssum[w];
       }
+      if (real)   // R33: the island's objectives in cell order
+        for (int i = 0; i < tile; ++i) d0 += __longlong_as_double(obj_isl[i]);
       parts[2 * li] = m0;
       parts[2 * li + 1] = real ? __double_as_longlong(d0) : s0;
       __threadfence();
@@ -820,6 +830,8 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
     return fail(FFS_ERR_INVALID_ARG, "bad island shard");
   if (cfg->generations < 0 || cfg->migration_interval < 1) return fail(FFS_ERR_INVALID_ARG, "bad generations");
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail(FFS_ERR_INVALID_ARG, "bad rank/world");
+  if (cfg->world > 1 && (!cfg->allgather || !cfg->allreduce_max_i64))
+    return fail(FFS_ERR_INVALID_ARG, "world > 1 needs both collective hooks (allreduce_max_i64, allgather)");
   State &st = sh->v;
   cudaSetDevice(st.inst->dev);
   {
@@ -873,6 +885,8 @@ ffs_status ffs_evolve_begin(ffs_state *sh, const ffs_ga_config *cfg, void *strea
   if (e == FFS_OK) e = r.alloc(&r.tsum, (size_t)cfg->generations + 1);
   if (e == FFS_OK) e = r.alloc(&r.parts, (size_t)2 * r.nisl);
   if (e == FFS_OK) e = r.alloc(&r.tcounter, 1);
+  if (e == FFS_OK) e = r.alloc(&r.best_v, 2);
+  if (e == FFS_OK) e = r.alloc(&r.best_s, (size_t)st.cells + 1);
   if (e == FFS_OK) {
     cudaError_t ce = cudaMemsetAsync(r.tcounter, 0, sizeof(unsigned), r.s);
     if (ce != cudaSuccess) e = cuda_fail(ce, "trace counter");
@@ -927,50 +941,38 @@ ffs_status ffs_best(ffs_run *h, int8_t *x, int16_t *y, int32_t *assign, int32_t 
   const int K = r.K;
   std::vector<int8_t> bx(std::max(K, 1), 0);
   std::vector<int16_t> by(std::max(K, 1), 1);
+  int b = 0;
   if (K > 0) {
     std::vector<int64_t> hf(r.nisl);
-    FFS_CUDA(cudaMemcpy(hf.data(), r.hfit, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost));
-    int b = 0;
+    FFS_CUDA(cudaMemcpyAsync(hf.data(), r.hfit, (size_t)r.nisl * 8, cudaMemcpyDeviceToHost, r.s));
+    FFS_CUDA(cudaStreamSynchronize(r.s));
     for (int i = 1; i < r.nisl; ++i)
-      if (hf[i] > hf[b]) b = i;  // ties -> lowest island
-    FFS_CUDA(cudaMemcpy(bx.data(), r.hx + (size_t)b * r.row, (size_t)K, cudaMemcpyDeviceToHost));
-    FFS_CUDA(cudaMemcpy(by.data(), r.hy + (size_t)b * r.row, (size_t)K * 2, cudaMemcpyDeviceToHost));
+      if (hf[i] > hf[b]) b = i;  // ties -> lowest island (R28)
   }
-  // decode the elite once more to emit its schedule
-  int8_t *dx = nullptr;
-  int16_t *dy = nullptr;
-  int64_t *dv = nullptr;
-  int32_t *di = nullptr;
-  FFS_CUDA(cudaMalloc(&dx, bx.size()));
-  FFS_CUDA(cudaMalloc(&dy, by.size() * 2));
-  FFS_CUDA(cudaMalloc(&dv, 16));
-  FFS_CUDA(cudaMalloc(&di, (size_t)(st.cells + 1) * 4));
-  cudaMemcpy(dx, bx.data(), bx.size(), cudaMemcpyHostToDevice);
-  cudaMemcpy(dy, by.data(), by.size() * 2, cudaMemcpyHostToDevice);
+  // decode the elite once more, in place in the history row, to emit its
+  // schedule (run-owned output buffers, everything ordered on the run's stream)
   EvalArgs a{};
   a.image = st.image_dev;
   a.count = 1;
-  a.x = dx;
-  a.y = dy;
-  a.obj = dv;
-  a.tard = dv + 1;
-  a.cmax = di + st.cells;
-  a.start_out = di;
+  a.x = r.hx + (size_t)b * r.row;
+  a.y = r.hy + (size_t)b * r.row;
+  a.row = K > 0 ? r.row : 0;
+  a.obj = r.best_v;
+  a.tard = r.best_v + 1;
+  a.cmax = r.best_s + st.cells;
+  a.start_out = r.best_s;
   a.fstart = st.fstart_dev;
   ffs_status e = launch_evaluate(st, a, r.scr, r.s, nullptr);
+  if (e != FFS_OK) return e;
   std::vector<int32_t> hs(st.cells + 1);
   int64_t hv[2] = {0, 0};
-  if (e == FFS_OK) {
-    cudaError_t ce = cudaMemcpyAsync(hs.data(), di, (size_t)(st.cells + 1) * 4, cudaMemcpyDeviceToHost, r.s);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(hv, dv, 16, cudaMemcpyDeviceToHost, r.s);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(r.s);
-    if (ce != cudaSuccess) e = cuda_fail(ce, "ffs_best copy-out");
+  FFS_CUDA(cudaMemcpyAsync(hs.data(), r.best_s, (size_t)(st.cells + 1) * 4, cudaMemcpyDeviceToHost, r.s));
+  FFS_CUDA(cudaMemcpyAsync(hv, r.best_v, 16, cudaMemcpyDeviceToHost, r.s));
+  if (K > 0) {
+    FFS_CUDA(cudaMemcpyAsync(bx.data(), a.x, (size_t)K, cudaMemcpyDeviceToHost, r.s));
+    FFS_CUDA(cudaMemcpyAsync(by.data(), a.y, (size_t)K * 2, cudaMemcpyDeviceToHost, r.s));
   }
-  cudaFree(dx);
-  cudaFree(dy);
-  cudaFree(dv);
-  cudaFree(di);
-  if (e != FFS_OK) return e;
+  FFS_CUDA(cudaStreamSynchronize(r.s));
   if (x && K) std::memcpy(x, bx.data(), (size_t)K);
   if (y && K) std::memcpy(y, by.data(), (size_t)K * 2);
   if (start) std::memcpy(start, hs.data(), (size_t)st.cells * 4);
@@ -982,8 +984,11 @@ ffs_status ffs_best(ffs_run *h, int8_t *x, int16_t *y, int32_t *assign, int32_t 
   if (total_tardiness) *total_tardiness = hv[1];
   if (makespan) *makespan = hs[st.cells];
   if (K > 0 && r.gen >= 0) {
-    if (trace_min) FFS_CUDA(cudaMemcpy(trace_min, r.tmin, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost));
-    if (trace_sum) FFS_CUDA(cudaMemcpy(trace_sum, r.tsum, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost));
+    if (trace_min)
+      FFS_CUDA(cudaMemcpyAsync(trace_min, r.tmin, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost, r.s));
+    if (trace_sum)
+      FFS_CUDA(cudaMemcpyAsync(trace_sum, r.tsum, (size_t)(r.gen + 1) * 8, cudaMemcpyDeviceToHost, r.s));
+    FFS_CUDA(cudaStreamSynchronize(r.s));
   }
   return FFS_OK;
 }

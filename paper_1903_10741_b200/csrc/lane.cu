@@ -255,7 +255,10 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       const int16_t *yr = a.y + (a.first + c) * a.row;
       const int8_t *xr = a.x + (a.first + c) * a.row;
       if (BULK && lane == 0) {
-        const uint32_t yb = (uint32_t)a.row * 2u, xb = XS ? (uint32_t)a.row : 0u;
+        // ceil16(K) genes of the row (<= row: row % 16 == 0 and row >= K), never
+        // the whole row: the smem slots are sized from K (128 * ceil(K/128))
+        const uint32_t kc = ((uint32_t)K + 15u) & ~15u;
+        const uint32_t yb = kc * 2u, xb = XS ? kc : 0u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the previous row's generic writes
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(yb + xb) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -58,6 +58,18 @@ ffs_status OvfScratch::ensure(int64_t count, int64_t level_bytes_needed) {
   return FFS_OK;
 }
 
+ffs_status launch_evaluate_shared(State &st, const EvalArgs &a, cudaStream_t s) {
+  OvfScratch &scr = st.scratch;
+  if (!scr.done) FFS_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
+  else if (scr.used && scr.last != s) FFS_CUDA(cudaStreamWaitEvent(s, scr.done, 0));
+  ffs_status e = launch_evaluate(st, a, scr, s, nullptr);
+  if (e != FFS_OK) return e;
+  FFS_CUDA(cudaEventRecord(scr.done, s));
+  scr.last = s;
+  scr.used = true;
+  return FFS_OK;
+}
+
 void OvfScratch::release() {
   free_(list);
   free_(level);
@@ -167,6 +179,15 @@ ffs_status State::build_image() {
   hb = (hb + 31) / 32 * 32;
   if (hb >= (int64_t)1 << 30) return fail(FFS_ERR_INVALID_ARG, "time horizon exceeds 2^30 ticks");
   h_bound = (int32_t)hb;
+  {
+    // every objective stays inside its 64-bit word with room for E_max = 10^a
+    // (P:375): C_j <= Cb, sum T <= NJ * Cb, so WT * sum T + C_max < 1e17
+    // (integer: E_max <= 1e18 < 2^63) or < 1e300 (binary64, f3)
+    const double Cb = (double)std::max<int64_t>((int64_t)rs + hb, frozen_cmax);
+    const double objmax = (real_wt ? wt_f : (double)in.wt) * (double)NJ * Cb + Cb;
+    if (!(objmax < (real_wt ? 1e300 : 1e17)))
+      return fail(FFS_ERR_INVALID_ARG, "WT too large: WT * sum T + C_max could overflow the objective word");
+  }
 
   // --- image layout
   const int nt = (K + 31) / 32;
@@ -607,10 +628,20 @@ ffs_status ffs_state_set_horizon_cap(ffs_state *h, int32_t cap) {
 ffs_status ffs_state_set_objective_weight(ffs_state *h, double wt) {
   if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
   if (!(wt >= 0.0) || wt > 1e300) return fail(FFS_ERR_INVALID_ARG, "WT must be finite and >= 0");
+  const int32_t old_real = h->v.real_wt;
+  const double old_wt = h->v.wt_f;
   h->v.real_wt = 1;
   h->v.wt_f = wt;
   cudaSetDevice(h->v.inst->dev);
-  return h->v.build_image();
+  ffs_status e = h->v.build_image();
+  if (e != FFS_OK) {   // keep the state as it was
+    std::string msg = ffs_last_error();
+    h->v.real_wt = old_real;
+    h->v.wt_f = old_wt;
+    h->v.build_image();
+    return fail(e, msg.c_str());
+  }
+  return FFS_OK;
 }
 
 ffs_status ffs_state_info(const ffs_state *h, int32_t *K, int32_t *cells, int32_t *hcap, int32_t *hb,
@@ -633,6 +664,7 @@ void ffs_state_destroy(ffs_state *h) {
   if (st.gbase_dev) cudaFree(st.gbase_dev);
   if (st.ovf_seen_host) cudaFreeHost(st.ovf_seen_host);
   st.scratch.release();
+  if (st.scratch.done) cudaEventDestroy(st.scratch.done);
   st.stage.release();
   st.stage.release_streams();
   delete h;
@@ -663,7 +695,7 @@ ffs_status ffs_evaluate_strided(const ffs_state *h, int64_t count, const int8_t 
   a.start_out = start_out;
   a.fstart = st.fstart_dev;
   a.row = row;
-  return launch_evaluate(st, a, st.scratch, (cudaStream_t)stream, nullptr);
+  return launch_evaluate_shared(st, a, (cudaStream_t)stream);
 }
 
 ffs_status ffs_evaluate_host(const ffs_state *h, int64_t count, const int8_t *x, const int16_t *y,

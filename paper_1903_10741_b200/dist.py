@@ -114,3 +114,73 @@ def make_hooks(device_memory: bool = True):
             return 1
 
     return allreduce, allgather
+
+
+def global_best(best: dict) -> dict:
+    """The ring's result from every shard's ffs_best.
+
+    The answer of the island GA is the best individual in history over all
+    islands and the trace is over the whole population
+    (S:199-202); each rank's `Run.best()` covers its own shard only.  One
+    allgather (rank-major) of each shard's record -- objective word, sum T,
+    C_max, x, y, merged schedule, local trace -- then, identically on every
+    rank: the best is the smallest objective (fitness Eq. (13) is strictly
+    decreasing in it above 0), ties -> lowest rank, which holds the lowest
+    global islands (shards are contiguous, ties -> lowest island, R28);
+    trace_min = min over shards, trace_sum = sum over shards in rank order
+    (exact for the integer objective).  Returns Run.best()'s keys plus
+    "rank" (the shard that holds it).
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    real = isinstance(best["objective"], float)
+    K = best["x"].size
+    cells = best["start"].size
+    G1 = best["trace_min"].size
+
+    def word(v):
+        return int(np.array([v], np.float64).view(np.int64)[0]) if real else int(v)
+
+    head = np.array([word(best["objective"]), best["sum_tardiness"], best["makespan"]], np.int64)
+    tmin = np.asarray(best["trace_min"])
+    tsum = np.asarray(best["trace_sum"])
+    if real:
+        tmin, tsum = tmin.astype(np.float64).view(np.int64), tsum.astype(np.float64).view(np.int64)
+    parts = [head, tmin.astype(np.int64), tsum.astype(np.int64)]
+    rec = b"".join([p.tobytes() for p in parts] + [np.asarray(best["x"], np.int8).tobytes(),
+                                                   np.asarray(best["y"], np.int16).tobytes(),
+                                                   np.asarray(best["assign"], np.int32).tobytes(),
+                                                   np.asarray(best["start"], np.int32).tobytes()])
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    send = torch.frombuffer(bytearray(rec), dtype=torch.uint8).to(dev)
+    allb = allgather_bytes_tensor(send).cpu().numpy().reshape(world, len(rec))
+    n64 = 3 + 2 * G1
+
+    def unpack(r):
+        b = allb[r]
+        v = b[: 8 * n64].view(np.int64)
+        o = 8 * n64
+        x = b[o:o + K].view(np.int8); o += K
+        y = b[o:o + 2 * K].view(np.int16); o += 2 * K
+        a = b[o:o + 4 * cells].view(np.int32); o += 4 * cells
+        s = b[o:o + 4 * cells].view(np.int32)
+        return v[:3], v[3:3 + G1], v[3 + G1:], x, y, a, s
+
+    recs = [unpack(r) for r in range(world)]
+    r = min(range(world), key=lambda i: (int(recs[i][0][0]), i))
+    head, _, _, x, y, a, s = recs[r]
+    tmin_all = np.stack([q[1] for q in recs])
+    tsum_all = np.stack([q[2] for q in recs])
+    if real:
+        obj = float(head[:1].view(np.float64)[0])
+        gmin = tmin_all.min(axis=0).view(np.float64)
+        gsum = np.zeros(G1, np.float64)
+        for q in tsum_all.view(np.float64):       # rank order
+            gsum = gsum + q
+    else:
+        obj = int(head[0])
+        gmin = tmin_all.min(axis=0)
+        gsum = tsum_all.sum(axis=0)
+    return dict(x=x.copy(), y=y.copy(), assign=a.copy(), start=s.copy(), objective=obj,
+                sum_tardiness=int(head[1]), makespan=int(head[2]), trace_min=gmin, trace_sum=gsum, rank=r)

@@ -341,6 +341,13 @@ def make_state(inst: Instance, rs: int, orig_assign=None, orig_start=None, stati
     return st
 
 
+def evolve(state: State, island_w: int, island_h: int, islands_total: int, generations: int, seed: int,
+           **kw) -> "Run":
+    """The one-shot call ffs_evolve: every generation of the island GA of one
+    rescheduling point, returned as a finished Run (read it with best())."""
+    return Run(state, island_w, island_h, islands_total, generations, seed, one_shot=True, **kw)
+
+
 class Run:
     """Island GA of one rescheduling point (ffs_evolve_begin / _step / ffs_best).
 
@@ -351,7 +358,7 @@ class Run:
     def __init__(self, state: State, island_w: int, island_h: int, islands_total: int, generations: int,
                  seed: int, island_begin: int = 0, island_end: int | None = None, xo_threshold: int = XO_090,
                  mut_threshold: int = MUT_010, migration_interval: int = 10, rank: int = 0, world: int = 1,
-                 hooks=None, stream=None):
+                 hooks=None, stream=None, one_shot: bool = False):
         self.state = state
         island_end = islands_total if island_end is None else island_end
         ar, ag = (ALLRED(), ALLGATHER()) if hooks is None else (ALLRED(hooks[0]), ALLGATHER(hooks[1]))
@@ -364,7 +371,9 @@ class Run:
         self.nloc = self.nisl * self.tile
         self._stream = stream
         h = C.c_void_p()
-        _check(lib().ffs_evolve_begin(state.h, C.byref(self.cfg), _stream(stream), C.byref(h)), "ffs_evolve_begin")
+        # one_shot: ffs_evolve (all generations, synchronised) instead of ffs_evolve_begin
+        fn = "ffs_evolve" if one_shot else "ffs_evolve_begin"
+        _check(getattr(lib(), fn)(state.h, C.byref(self.cfg), _stream(stream), C.byref(h)), fn)
         self.h = h
 
     def __del__(self):

@@ -87,9 +87,11 @@ class Workload:
 
 
 def gen_v1(name: str, n: int, g: int, o: int, q_max: int, *, arrivals_per_event: Sequence[int] = (),
-           ratios: Sequence[float] = (), wt: int = 100, seed: int = 1903, power: str = "one") -> Workload:
+           ratios: Sequence[float] = (), wt: int = 100, seed: int = 1903, power: str = "one",
+           p_range: Sequence[int] = (1, 5)) -> Workload:
+    """p_range: P_sm ~ U{lo..hi}; the paper's (1, 5) by default (Table 5)."""
     rng = np.random.default_rng(seed)
-    Psm = rng.integers(1, 6, size=(g, o))                              # U{1..5}
+    Psm = rng.integers(int(p_range[0]), int(p_range[1]) + 1, size=(g, o))   # U{1..5} (P:382)
     n_arr = int(sum(arrivals_per_event))
     NT = n + n_arr
     P = np.broadcast_to(Psm, (NT, g, o)).astype(np.int32).copy()

@@ -69,8 +69,9 @@ PERTURBATIONS = {
     "mutation: swap gene b not shifted past a": (
         "if (gb >= ga) ++gb;", "if (gb > ga) ++gb;"),
     "trace: min skips the last cell": (
-        "for (int64_t i = 0; i < n; ++i) { if (obj[i] < m) m = obj[i]; s += obj[i]; }",
-        "for (int64_t i = 0; i < n; ++i) { if (i + 1 < n && obj[i] < m) m = obj[i]; s += obj[i]; }"),
+        "      if (v < m) m = v;", "      if (v < m && !(li == nisl - 1 && i == tile - 1)) m = v;"),
+    "trace: one sequential sum over all cells": (
+        "      p += v;\n    }\n    s += p;", "      s += v;\n    }\n    (void)p;"),
 }
 
 TESTS = ["tests/test_oracle_ga_ops.py", "tests/test_oracle_paper.py"]

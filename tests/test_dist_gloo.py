@@ -6,7 +6,9 @@
   allgather on raw pointers;
 * an island GA sharded over 2 ranks, exchanging through those collectives,
   is bit-identical to the single-process run (oracle GA as the engine: the
-  sharding / ring / E_max semantics are what is tested here).
+  sharding / ring / E_max semantics are what is tested here);
+* dist.global_best reduces the shards' local bests and traces to the
+  single-process run's best and trace on every rank.
 """
 import ctypes
 import os
@@ -40,6 +42,18 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _shard_best(ctx, ga):
+    """What ffs_best returns for a shard: its best history elite (ties ->
+    lowest island), decoded, and the shard's local trace."""
+    hx, hy, hobj, hfit = ga.history()
+    i = int(np.argmax(hfit))
+    r = ctx.decode_genes(hx[i], hy[i])
+    tmin, tsum = ga.trace()
+    return dict(x=hx[i], y=hy[i], assign=r["assign"], start=r["start"], objective=int(r["objective"]),
+                sum_tardiness=int(r["sum_tardiness"]), makespan=int(r["makespan"]),
+                trace_min=np.asarray(tmin, np.int64), trace_sum=np.asarray(tsum, np.int64))
 
 
 def _worker(rank, world, port, out_dir):
@@ -81,8 +95,12 @@ def _worker(rank, world, port, out_dir):
             ga.step()
         x, y, obj, fit = ga.population()
         tmin, tsum = ga.trace()
+        # --- the ring's global best + trace from the shards' local results
+        gb = fdist.global_best(_shard_best(ctx, ga))
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), x=x, y=y, obj=obj, fit=fit, tmin=tmin,
-                 tsum=tsum, emax=ga.emax)
+                 tsum=tsum, emax=ga.emax, gb_x=gb["x"], gb_y=gb["y"], gb_start=gb["start"],
+                 gb_assign=gb["assign"], gb_obj=gb["objective"], gb_T=gb["sum_tardiness"],
+                 gb_M=gb["makespan"], gb_tmin=gb["trace_min"], gb_tsum=gb["trace_sum"], gb_rank=gb["rank"])
     finally:
         dist.destroy_process_group()
 
@@ -110,3 +128,11 @@ def test_two_rank_island_ga_equals_single_process(tmp_path):
     # global trace = min / sum over the shards' local traces
     assert (np.minimum(parts[0]["tmin"], parts[1]["tmin"]) == rmin).all()
     assert (parts[0]["tsum"] + parts[1]["tsum"] == rsum).all()
+    # dist.global_best: every rank returns the single-process run's best and trace
+    ref_best = _shard_best(ctx, ref)
+    for p in parts:
+        assert int(p["gb_obj"]) == ref_best["objective"]
+        assert int(p["gb_T"]) == ref_best["sum_tardiness"] and int(p["gb_M"]) == ref_best["makespan"]
+        for k in ("x", "y", "start", "assign"):
+            assert (p["gb_" + k] == ref_best[k]).all(), k
+        assert (p["gb_tmin"] == rmin).all() and (p["gb_tsum"] == rsum).all()

@@ -47,8 +47,9 @@ def _worker(rank, world, port, out_dir):
         run.step(G)
         x, y, obj, fit = run.population()
         hx, hy, hobj, hfit = run.history()
+        gb = fdist.global_best(run.best())
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=x, y=y, obj=obj, fit=fit, hx=hx, hy=hy, hobj=hobj,
-                 emax=run.info()["emax"])
+                 emax=run.info()["emax"], **{"gb_" + k: np.asarray(v) for k, v in gb.items()})
     finally:
         dist.destroy_process_group()
 
@@ -70,3 +71,50 @@ def test_two_rank_ga_equals_single_process(tmp_path):
     for key, ref in (("x", x), ("y", y), ("obj", obj), ("fit", fit), ("hx", hx), ("hy", hy), ("hobj", hobj)):
         got = np.concatenate([p[key] for p in parts])
         assert (got == ref).all(), key
+    # the ring's global best and trace (dist.global_best) on every rank == the single run's ffs_best
+    b = run.best()
+    for p in parts:
+        for k in ("x", "y", "assign", "start", "trace_min", "trace_sum", "objective", "sum_tardiness", "makespan"):
+            assert (p["gb_" + k] == np.asarray(b[k])).all(), k
+
+
+def _nccl_worker(rank, world, port, out_dir):
+    """World-1 NCCL group on the GPU: the product's hooks (make_hooks with
+    device memory) called on raw device pointers and the library's stream
+    handle (ExternalStream), then global_best over NCCL."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1903_10741_b200 import dist as fdist
+        from paper_1903_10741_b200 import ffs
+        allreduce, allgather = fdist.make_hooks(device_memory=True)
+        s = torch.cuda.Stream()
+        v = torch.tensor([12345], dtype=torch.int64, device="cuda")
+        send = torch.arange(40, dtype=torch.uint8, device="cuda")
+        recv = torch.zeros(40 * world, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        assert allreduce(None, v.data_ptr(), s.cuda_stream) == 0
+        assert allgather(None, send.data_ptr(), recv.data_ptr(), 40, s.cuda_stream) == 0
+        s.synchronize()
+        assert int(v.item()) == 12345 and bool((recv == send).all())
+        st = _state()
+        run = ffs.Run(st, ISL_W, ISL_H, ISLANDS, 12, SEED, stream=s)
+        run.step(12)
+        gb = fdist.global_best(run.best())
+        b = run.best()
+        ok = all(bool((np.asarray(gb[k]) == np.asarray(b[k])).all())
+                 for k in ("x", "y", "start", "trace_min", "trace_sum", "objective"))
+        open(os.path.join(out_dir, "nccl_ok"), "w").write(f"{ok} {dist.get_backend()}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_hooks_world_one(tmp_path):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_nccl_worker, args=(1, port, str(tmp_path)), nprocs=1, join=True)
+    assert open(os.path.join(tmp_path, "nccl_ok")).read() == "True nccl"

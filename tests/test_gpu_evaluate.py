@@ -23,15 +23,17 @@ def gpu_eval(st, x, y, sched=False):
 
 
 def compare(octx, st, x, y, n_sched=None):
+    """Objective, sum T, C_max and the full schedule of EVERY chromosome (the
+    schedule-emitting launch), and the values of the plain launch."""
     obj, T, M, S = gpu_eval(st, x, y, sched=True)
-    oo, oT, oM, _ = octx.evaluate_batch(x, y, nthreads=8)
+    obj2, T2, M2, _ = gpu_eval(st, x, y, sched=False)
+    oo, oT, oM, oS = octx.evaluate_batch_schedule(x, y, nthreads=8)
     assert (obj == oo).all(), np.flatnonzero(obj != oo)[:10]
     assert (T == oT).all()
     assert (M == oM).all()
-    n_sched = len(x) if n_sched is None else n_sched
-    for i in range(min(n_sched, len(x))):
-        r = octx.decode_genes(x[i], y[i])
-        assert (S[i] == r["start"]).all(), i
+    assert (obj2 == oo).all() and (T2 == oT).all() and (M2 == oM).all()
+    bad = np.flatnonzero((S != oS).any(axis=1))
+    assert bad.size == 0, f"schedules differ at {bad[:10]}"
 
 
 def test_table4_printed_chromosome():
@@ -255,6 +257,20 @@ def test_long_jobs(g, n, o, q_max, path):
     compare(octx, st, x, y, n_sched=20)
 
 
+@pytest.mark.parametrize("q_max,power", [(4, "one"), (7, "u13")])
+def test_long_processing_times_warp_path(q_max, power):
+    """P_sm ~ U{9..40} (above the lane decoder's P <= 8): the warp-per-
+    chromosome kernel with runs longer than one 32-tick ballot window
+    (evaluate.cu multi-window run logic), uniform and general power."""
+    wl = wlmod.gen_v1("Plong", 14, 5, 3, q_max, arrivals_per_event=[4], ratios=[0.3], seed=40 + q_max,
+                      power=power, p_range=(9, 40))
+    assert wl.P.min() >= 9 and wl.P.max() > 32
+    octx, st, arr = both_event_ctx(wl)
+    check_gene_order(octx, st)
+    x, y = wlmod.random_chromosomes(400, st.K, wl.o, seed=19)
+    compare(octx, st, x, y)
+
+
 @pytest.mark.parametrize("n,g", [(16, 8), (32, 8), (43, 6), (16, 16), (65, 4)])
 def test_tile_boundary_K(n, g, path):
     """Static problems (RS = 0, K = n g) with K = 128, 256, 258, 256, 260:
@@ -339,6 +355,24 @@ def test_strided_rows_match_compact(pad, path):
     for u, v in zip(ref, got):
         assert (u == v).all()
     compare(octx, st, x[:60], y[:60], n_sched=10)
+
+
+@pytest.mark.parametrize("R", [1024, 2048])
+def test_wide_padded_rows_config_c(R, path):
+    """Rows much wider than K (K = 855 in rows of 1,024 / 2,048 genes, 16-B
+    aligned: the TMA row staging) -- the staging copies ceil16(K) genes, never
+    the whole row, so it cannot overrun the per-warp slots."""
+    wl = wlmod.config_C()
+    octx, st, arr = both_event_ctx(wl)
+    x, y = wlmod.random_chromosomes(200, st.K, wl.o, seed=31)
+    xp = np.full((len(x), R), 3, np.int8)     # junk in the padding
+    yp = np.full((len(y), R), 7, np.int16)
+    xp[:, :st.K] = x
+    yp[:, :st.K] = y
+    got = gpu_eval(st, xp, yp, sched=True)
+    oo, oT, oM, oS = octx.evaluate_batch_schedule(x, y, nthreads=8)
+    assert (got[0] == oo).all() and (got[1] == oT).all() and (got[2] == oM).all()
+    assert (got[3] == oS).all()
 
 
 def test_random_population_strided_equals_compact():

@@ -15,9 +15,9 @@ from tests import fixtures as fx
 pytestmark = pytest.mark.gpu
 
 
-def oracle_evolve(ctx, shape, G, seed):
+def oracle_evolve(ctx, shape, G, seed, nthreads=8):
     w, h, islands = shape
-    ga = orc.GA(ctx, w, h, islands, G, seed, nthreads=8)
+    ga = orc.GA(ctx, w, h, islands, G, seed, nthreads=nthreads)
     for _ in range(G + 1):
         ga.step()
     hx, hy, hobj, hfit = ga.history()
@@ -27,11 +27,11 @@ def oracle_evolve(ctx, shape, G, seed):
     return r, tmin, tsum
 
 
-def oracle_workflow(wl, shape, G, seed):
+def oracle_workflow(wl, shape, G, seed, nthreads=8):
     out = []
     base = wl.original_instance()
     c0 = orc.Ctx(fx.workload_instance(base), 0)
-    r, tmin, tsum = oracle_evolve(c0, shape, G, seed)
+    r, tmin, tsum = oracle_evolve(c0, shape, G, seed, nthreads)
     out.append((0, c0.K, r, tmin, tsum))
     c_plan = r["makespan"]
     rs_list = []
@@ -41,7 +41,7 @@ def oracle_workflow(wl, shape, G, seed):
         rs_list.append(rs)
         arr = wl.instance_at(e, rs_list)
         ctx = orc.Ctx(fx.workload_instance(arr), rs, assign, start)
-        r, tmin, tsum = oracle_evolve(ctx, shape, G, seed + 1 + e)
+        r, tmin, tsum = oracle_evolve(ctx, shape, G, seed + 1 + e, nthreads)
         assert ctx.validate(r["assign"], r["start"])[0] == 0      # Eqs. (4)-(10), frozen ops kept
         out.append((rs, ctx.K, r, tmin, tsum))
         assign, start = r["assign"], r["start"]

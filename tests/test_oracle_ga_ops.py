@@ -160,3 +160,5 @@ def test_migrate_across_shard_boundary(split):
 def test_trace_stats():
     d = G["trace"]
     assert orc.trace_stats(d["obj"]) == (d["min"], d["sum"])
+    d = G["trace_islands"]
+    assert orc.trace_stats(d["obj"], d["tile"]) == (d["min"], d["sum"])
