@@ -32,8 +32,37 @@ sys.path.insert(0, ROOT)
 METRIC = "chromosome evaluations/sec and GA generations/sec per GPU at 1/2/4/8 B200"
 ISLAND_W, ISLAND_H, ISLANDS_PER_GPU = 16, 16, 256
 SEED = 10741
-# issue-rate roofline: 148 SMs x 4 SMSPs x 1 warp-instruction/clk x 1.965 GHz
-ISSUE_PEAK = 148 * 4 * 1.965e9
+# algorithmic scalar operations per event of the literal Algorithms 1-2 and
+# Eqs. (1)-(3) ("Roofline"): a dispatch (t0 = max of RS,
+# predecessor / release and machine free time: 3 loads + 2 max; commit
+# C = S + p, machine free, store: 3), a power check at one instant (load
+# level, add q, compare: 3), a delay jump (earliest completion, move t: 2), a
+# committed profile interval (two breakpoint splits: 4), Algorithm 1 per gene
+# (prefix min, leader test, count, prefix, rank, scatter: 6), Eqs. (1)-(3) per
+# job (T_j = max(C - D, 0), sum, C_max: 4)
+OPS_PER = {"dispatches": 8, "checks": 3, "jumps": 2, "updates": 4}
+OPS_PER_GENE, OPS_PER_JOB = 6, 4
+
+
+def device_peaks(local):
+    """SM count (device), max SM clock (NVML, else MEASURED_PEAKS.json) and the
+    measured HBM copy bandwidth (MEASURED_PEAKS.json, else the guide's fallback)."""
+    import torch
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    mhz, src = None, "nvml max SM clock"
+    nv = ClockSampler.init(local)
+    if nv:
+        try:
+            mhz = float(nv[0].nvmlDeviceGetMaxClockInfo(nv[1], nv[0].NVML_CLOCK_SM))
+        except Exception:
+            mhz = None
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(mp)) if os.path.exists(mp) else {}
+    if mhz is None:
+        mhz, src = float(peaks.get("sm_max_mhz", 1965.0)), "MEASURED_PEAKS.json sm_max_mhz"
+    hbm = peaks.get("hbm_gbs")
+    hbm_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "of fallback (B200_PROFILING.md)"
+    return {"sms": sms, "sm_mhz": mhz, "clock_source": src, "hbm_gbs": float(hbm or 6650.0), "hbm_source": hbm_src}
 
 
 def parse():
@@ -186,26 +215,62 @@ def oracle_ctx():
     return wl, octx
 
 
+def alg_ops_per_eval(cnt, evals, K, NJ):
+    """Algorithmic scalar operations per evaluation from the instrumented
+    oracle's event counts (OPS_PER) plus Algorithm 1 per gene and Eqs. (1)-(3)
+    per job."""
+    return sum(OPS_PER[k] * cnt[k] for k in OPS_PER) / evals + OPS_PER_GENE * K + OPS_PER_JOB * NJ
+
+
 def cpu_baseline_eval(seconds):
-    """Oracle decode+evaluate of Philox-independent random chromosomes of
-    config C on every host core, for about `seconds`.  Returns (evals/s,
-    cores, sample, algorithmic ops per evaluation)."""
+    """The oracle as it stands on the host cores: decode+evaluate of random
+    config-C chromosomes on every core (~`seconds`) and on 1 thread (~1/4 of
+    it), plus the oracle island GA on configs A (in full: 1 x 8x8, 50
+    generations) and B (a bounded sample: 64 x 128 at event 1, 3
+    generations).  Returns (dict, algorithmic ops per evaluation)."""
+    from oracle import oracle as orc
     from paper_1903_10741_b200 import workload as wlmod
+    from tests import fixtures as fx
     wl, octx = oracle_ctx()
     cores = len(os.sched_getaffinity(0))
-    n = 0
-    cnt = {"dispatches": 0, "checks": 0, "jumps": 0, "updates": 0}
-    t0 = time.perf_counter()
-    batch = max(32, 16 * cores)
-    while time.perf_counter() - t0 < seconds:
-        x, y = wlmod.random_chromosomes(batch, octx.K, wl.o, seed=1000 + n)
-        _, _, _, c = octx.evaluate_batch(x, y, nthreads=cores)
-        for k in cnt:
-            cnt[k] += c[k]
-        n += batch
-    dt = time.perf_counter() - t0
-    ops = sum(cnt.values()) / n
-    return n / dt, cores, f"{n} random config-C chromosomes (K={octx.K}), oracle evaluate, {dt:.1f} s", ops, cnt
+
+    def timed_eval(nthreads, secs, seed0):
+        n, t0 = 0, time.perf_counter()
+        cnt = {"dispatches": 0, "checks": 0, "jumps": 0, "updates": 0}
+        batch = max(32, 16 * nthreads)
+        while time.perf_counter() - t0 < secs:
+            x, y = wlmod.random_chromosomes(batch, octx.K, wl.o, seed=seed0 + n)
+            _, _, _, c = octx.evaluate_batch(x, y, nthreads=nthreads)
+            for k in cnt:
+                cnt[k] += c[k]
+            n += batch
+        return n, time.perf_counter() - t0, cnt
+
+    n, dt, cnt = timed_eval(cores, seconds, 1000)
+    n1, dt1, _ = timed_eval(1, max(2.0, seconds / 4), 500000)
+    ops = alg_ops_per_eval(cnt, n, octx.K, octx.inst.n + octx.inst.n_prime)
+
+    def ga_rate(wlc, shape, G):
+        ctx, _, _, _ = fx.oracle_event_ctx(wlc)
+        w, h, isl = shape
+        ga = orc.GA(ctx, w, h, isl, G, 10741, nthreads=cores)
+        ga.step()
+        t0 = time.perf_counter()
+        for _ in range(G):
+            ga.step()
+        d = time.perf_counter() - t0
+        return {"gens_per_s": G / d, "evals_per_s": G * w * h * isl / d, "K": ctx.K,
+                "shape": f"{isl} x {w}x{h}", "generations": G, "seconds": d}
+
+    ga_a = ga_rate(wlmod.config_A2(), (8, 8, 1), 50)
+    ga_b = ga_rate(wlmod.config_B(), (16, 8, 64), 3)
+    out = {"value": n / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+           "sample": f"{n} random config-C chromosomes (K={octx.K}), oracle evaluate on {cores} threads, "
+                     f"{dt:.1f} s; 1 thread: {n1} in {dt1:.1f} s",
+           "value_1thread": n1 / dt1,
+           "ga_config_A": ga_a, "ga_config_B_sample": ga_b,
+           "counters_per_eval": {k: v / n for k, v in cnt.items()}}
+    return out, ops
 
 
 def run_reference(args):
@@ -541,29 +606,53 @@ def run_ours(args):
             "brute_force": brute,
             "clocks": clk.summary(),
         }
-        alg_ops = None
+        alg_ops, cnt_src = None, None
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, sample, alg_ops, cnt = cpu_baseline_eval(args.cpu_seconds)
-            out["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                                   "sample": sample}
-            out["alg_ops_per_eval"] = alg_ops
+            out["cpu_baseline"], alg_ops = cpu_baseline_eval(args.cpu_seconds)
+            cnt_src = "oracle counters of this run's cpu_baseline sample"
         if alg_ops is None:
-            alg_ops = 7.1 * K  # per-dispatch average measured by the instrumented oracle
-        achieved = eval_only * alg_ops
-        out["roofline"] = {"bound": "alu", "achieved": achieved / 1e9, "peak": ISSUE_PEAK / 1e9,
-                           "unit": "Gop/s", "frac": achieved / ISSUE_PEAK,
-                           "traffic": (latest_traffic() or (None, None, None))[0],
-                           "traffic_source": (latest_traffic() or (None, None, None))[1],
-                           "ncu": {k: (latest_traffic() or (None, None, {}))[2].get(k)
-                                   for k in ("kernels", "issue_active_pct", "alu_pipe_pct", "duration_us")},
-                           "algorithmic_bytes": float(pop_local * (3 * K + 20)),
-                           "note": "algorithmic ops (oracle-counted dispatches + power checks + delay jumps + "
-                                   "profile updates per evaluation) / evaluate-kernel time, against the issue "
-                                   "rate 148 SM x 4 SMSP x 1.965 GHz (one warp-instruction per op)",
-                           "pipes": "measured on B200 (scripts/micro/pipes.cu): LOP3/SHF/PRMT/IMNMX issue 2 "
-                                    "warp-instr/clk/SM on the alu pipe, IMAD 2 on the fma pipe; ncu: the decode "
-                                    "kernel keeps the alu pipe ~67% busy",
-                           "kernel": "evaluate launch (order_warp_kernel + lane_decode2_kernel)", "kernel_share_of_step": t_kernel / (t_local / args.steps)}
+            # counters measured by the oracle at config C:
+            # 855 dispatches, 3,870 checks, 522 jumps, 855 updates per evaluation
+            alg_ops = (alg_ops_per_eval({"dispatches": 855, "checks": 3870, "jumps": 522, "updates": 855}, 1, K,
+                                        wl.n + int(wl.arr_event.size)))
+            cnt_src = "oracle counters recorded in DESIGN.md (no cpu_baseline this run)"
+        out["alg_ops_per_eval"] = alg_ops
+        pk = device_peaks(local)
+        lane_peak = pk["sms"] * 4 * 32 * pk["sm_mhz"] * 1e6     # lane-instructions/s
+        warp_peak = pk["sms"] * 4 * pk["sm_mhz"] * 1e6          # warp-instructions/s
+        achieved = eval_only * alg_ops                            # algorithmic ops/s, evaluate launch
+        tr = latest_traffic()
+        traffic_b = tr[0] if tr else None
+        nc = tr[2] if tr else {}
+        frac_issue = None
+        if nc.get("inst_executed") and nc.get("duration_us"):
+            inst = sum(float(v) for v in nc["inst_executed"])
+            dur = sum(float(v) for v in nc["duration_us"]) * 1e-6
+            frac_issue = inst / (dur * warp_peak)
+        alg_bytes = pop_local * (3 * K + 20)
+        out["roofline"] = {
+            "bound": "alu", "achieved": achieved / 1e9, "peak": lane_peak / 1e9, "unit": "Gop/s",
+            "frac": achieved / lane_peak,
+            "traffic": traffic_b,
+            "kernel": "evaluate launch (order_warp_kernel + lane_decode2_kernel), 65,536 chromosomes",
+            "derivation": f"frac = alg_ops_per_eval {alg_ops:.0f} (OPS_PER x {cnt_src}) x eval_only "
+                          f"{eval_only:.4g} evals/s / lane-instruction peak {pk['sms']} SM x 4 SMSP x 32 lanes x "
+                          f"{pk['sm_mhz']:.0f} MHz ({pk['clock_source']})",
+            "frac_issue": frac_issue,
+            "frac_issue_derivation": "ncu smsp__inst_executed.sum (order + decode) / (gpu__time_duration.sum x "
+                                     f"{pk['sms']} SM x 4 SMSP x {pk['sm_mhz']:.0f} MHz) from {tr[1] if tr else None}",
+            "issue_active_pct_ncu": nc.get("issue_active_pct"),
+            "hbm": {"peak_gbs": pk["hbm_gbs"], "peak_source": pk["hbm_source"],
+                    "algorithmic_bytes": alg_bytes, "algorithmic_gbs": alg_bytes / t_kernel / 1e9,
+                    "frac_algorithmic": alg_bytes / t_kernel / 1e9 / pk["hbm_gbs"],
+                    "dram_bytes_ncu": traffic_b,
+                    "dram_gbs": traffic_b / t_kernel / 1e9 if traffic_b else None,
+                    "frac_dram": traffic_b / t_kernel / 1e9 / pk["hbm_gbs"] if traffic_b else None,
+                    "note": "algorithmic bytes = (3K + 20) per evaluation (int8 x + int16 y in; objective, "
+                            "sum T, C_max out); dram bytes = ncu dram__bytes_read + write of one evaluate"},
+            "traffic_source": tr[1] if tr else None,
+            "kernel_share_of_step": t_kernel / (t_local / args.steps),
+        }
         out["e2e"] = {"value": e2e_value, "unit": "evals/s",
                       "h2d_bytes_per_step": int(pop_local * K * 3),
                       "d2h_bytes_per_step": int(pop_local * (8 + 8 + 4)),

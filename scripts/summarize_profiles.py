@@ -103,6 +103,9 @@ for rep in ("prof_eval", "prof_gen"):
                    "issue_active_pct": col("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                    "alu_pipe_pct": col("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                    "duration_us": col("gpu__time_duration.sum"),
+                   "inst_executed": col("smsp__inst_executed.sum"),
+                   "thread_inst_per_inst": col("smsp__thread_inst_executed_per_inst_executed.ratio"),
+                   "sm_cycles_per_second": col("sm__cycles_elapsed.avg.per_second"),
                    "dram_bytes_per_evaluate": tot, "population": 65536,
                    "source": f"ncu --set full, gpurun_out/{tag}/prof_eval.ncu-rep (scripts/prof_eval.py 65536)"}
     out.append(f"## ncu --set full: {rep}\n")
