@@ -434,38 +434,40 @@ struct GenArgs {
   int8_t *xn; int16_t *yn;                     // next generation
 };
 
-__device__ __forceinline__ void argmax5(int lane, int sub, const int64_t *fitI, int row, int col, int w, int h,
-                                        int &winner) {
-  // lanes sub*16 + k, k < 5: candidate k of cell (row, col) in the order
-  // self, N, S, E, W (torus inside the island, R17)
-  const int cell = row * w + col;
-  int k = lane - sub * 16;
-  int nb = cell;
-  if (k == 1) nb = (row == 0 ? h - 1 : row - 1) * w + col;
-  else if (k == 2) nb = (row + 1 == h ? 0 : row + 1) * w + col;
-  else if (k == 3) nb = row * w + (col + 1 == w ? 0 : col + 1);
-  else if (k == 4) nb = row * w + (col == 0 ? w - 1 : col - 1);
-  long long f = (k >= 0 && k < 5) ? (long long)fitI[nb] : -1;  // fitness >= 0
-  int kk = (k >= 0 && k < 5) ? k : 99;
+// a6 for both cells of the pair at once: lane 16s + k, k < 5, holds
+// candidate k of cell s (s = 0: (row, col), s = 1: (row, col + 1)) in the
+// order self, N, S, E, W (torus inside the island, R17); a 3-step xor tree
+// inside each 8-lane group keeps the largest fitness, ties -> smaller k (R18)
+// (lanes k = 5..7 hold -1: every fitness is >= 0).
+__device__ __forceinline__ void select_pair(int lane, const int64_t *fitI, int row, int col, int w, int h, int &wa,
+                                            int &wb) {
+  const int k = lane & 15, c = col + (lane >> 4);
+  int nb = row * w + c;
+  if (k == 1) nb = (row == 0 ? h - 1 : row - 1) * w + c;
+  else if (k == 2) nb = (row + 1 == h ? 0 : row + 1) * w + c;
+  else if (k == 3) nb = row * w + (c + 1 == w ? 0 : c + 1);
+  else if (k == 4) nb = row * w + (c == 0 ? w - 1 : c - 1);
+  long long f = k < 5 ? (long long)fitI[nb] : -1;
+  int kk = k;
 #pragma unroll
-  for (int d = 8; d > 0; d >>= 1) {
-    long long f2 = __shfl_xor_sync(FULL, f, d);
-    int k2 = __shfl_xor_sync(FULL, kk, d);
-    int nb2 = __shfl_xor_sync(FULL, nb, d);
-    if (f2 > f || (f2 == f && k2 < kk)) { f = f2; kk = k2; nb = nb2; }
+  for (int d = 4; d > 0; d >>= 1) {
+    const long long f2 = __shfl_xor_sync(FULL, f, d);
+    const int k2 = __shfl_xor_sync(FULL, kk, d);
+    if (f2 > f || (f2 == f && k2 < kk)) { f = f2; kk = k2; }
   }
-  winner = __shfl_sync(FULL, nb, sub * 16);
+  const int ka = __shfl_sync(FULL, kk, 0), kb = __shfl_sync(FULL, kk, 16);
+  wa = __shfl_sync(FULL, nb, ka);
+  wb = __shfl_sync(FULL, nb, 16 + kb);
 }
 
-// byte / half-word masks of the genes before the cut inside one 16-B word
-// (n = cut - first gene of the word)
+// bit masks of the genes before the cut inside one 16-B chunk (n = cut -
+// first gene of the chunk): the low s bits of word k, by a clamping funnel
+// shift (s >= 32: all ones)
 __device__ __forceinline__ uint32_t mask_x(int n, int k) {   // word k of 16 int8 genes
-  const int nb = min(max(n - 4 * k, 0), 4);
-  return nb == 4 ? 0xFFFFFFFFu : (1u << (8 * nb)) - 1u;
+  return __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(8 * (n - 4 * k), 0));
 }
 __device__ __forceinline__ uint32_t mask_y(int n, int k) {   // word k of 8 int16 genes
-  const int nb = min(max(n - 2 * k, 0), 2);
-  return nb == 2 ? 0xFFFFFFFFu : (nb == 1 ? 0xFFFFu : 0u);
+  return __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(16 * (n - 2 * k), 0));
 }
 __device__ __forceinline__ uint32_t wsel(uint4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 __device__ __forceinline__ void wset(uint4 &v, int k, uint32_t w) {
@@ -507,21 +509,21 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
   uint8_t *FA = (uint8_t *)(LB + ((K * 2 + 15) & ~15) / 2);   // FA[v] = 1 iff v is in A's prefix
   uint8_t *FB = FA + fmb;
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int half = a.tile >> 1, wh = a.w >> 1;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t half = (uint32_t)a.tile >> 1, wh = (uint32_t)a.w >> 1;
   const int64_t row = a.row;
   const int nxv = (int)(row >> 4), nyv = (int)(row >> 3);   // 16-B words of a row
-  for (int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; pi < a.npairs; pi += nw) {
-    const int64_t li = pi / half;
-    const int pr = (int)(pi - li * half);
-    const int prow = pr / wh, pcol = 2 * (pr - prow * wh);
-    const int ca = prow * a.w + pcol, cb = ca + 1;
-    const uint32_t I = (uint32_t)(a.island0 + li), kg = (uint32_t)a.k;
-    const int64_t base = li * a.tile;
+  const uint32_t npairs = (uint32_t)a.npairs;               // < 2^30 (count < 2^31)
+  for (uint32_t pi = blockIdx.x * (blockDim.x >> 5) + warp; pi < npairs; pi += nw) {
+    const uint32_t li = pi / half, pr = pi - li * half;
+    const uint32_t prow = pr / wh;
+    const int pcol = 2 * (int)(pr - prow * wh);
+    const int ca = (int)prow * a.w + pcol, cb = ca + 1;
+    const uint32_t I = (uint32_t)a.island0 + li, kg = (uint32_t)a.k;
+    const int64_t base = (int64_t)li * a.tile;
     // a6: asteroid selection on the previous generation's fitness
     int wa, wb;
-    argmax5(lane, 0, a.fp + base, prow, pcol, a.w, a.h, wa);
-    argmax5(lane, 1, a.fp + base, prow, pcol + 1, a.w, a.h, wb);
+    select_pair(lane, a.fp + base, (int)prow, pcol, a.w, a.h, wa, wb);
     const uint4 *XA = (const uint4 *)(a.xp + (base + wa) * row), *XB = (const uint4 *)(a.xp + (base + wb) * row);
     const uint4 *YA = (const uint4 *)(a.yp + (base + wa) * row), *YB = (const uint4 *)(a.yp + (base + wb) * row);
     uint4 *xa = (uint4 *)(a.xn + (base + ca) * row), *xb = (uint4 *)(a.xn + (base + cb) * row);
@@ -552,6 +554,11 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
     }
     const bool ma = rma.x < a.mut_thr, mb = rmb.x < a.mut_thr;
     const bool repair = kc > 0 && kc < K;
+    // the membership maps cover the shorter side of the cut: the parents'
+    // prefix values (inv = false) or, when the suffix is shorter, their suffix
+    // values (inv = true: "in the prefix" = "not in the suffix" for a value
+    // in [1, K])
+    const bool inv = 2 * kc > K;
     if (repair) {
       // correction (R14): duplicates of child a are the suffix genes of B
       // whose value occurs in A's prefix; missing values = in B's prefix, not
@@ -562,11 +569,13 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
         ((uint4 *)FB)[i] = make_uint4(0, 0, 0, 0);
       }
       __syncwarp();
-      for (int i = lane; i < ((kc + 7) >> 3); i += 32) {
+      const int g_lo = inv ? kc : 0, g_hi = inv ? K : kc;
+      for (int i = (g_lo >> 3) + lane; i < ((g_hi + 7) >> 3); i += 32) {
         const uint4 va = YA[i], vb = YB[i];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (8 * i + j < kc) {   // prefix genes: values in [1, K]
+          const int g = 8 * i + j;
+          if (g >= g_lo && g < g_hi) {   // values in [1, K]
             const int sh = 16 * (j & 1);
             const int va1 = (int)((wsel(va, j >> 1) >> sh) & 0xFFFFu), vb1 = (int)((wsel(vb, j >> 1) >> sh) & 0xFFFFu);
             const int ta = va1 - 1, tb = vb1 - 1;
@@ -581,8 +590,10 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
       int offa = 0, offb = 0;
       for (int i0 = 0; i0 < nwd; i0 += 32) {
         int i = i0 + lane;
-        uint32_t wa_ = i < nwd ? (PB[i] & ~PA[i]) : 0u;
-        uint32_t wb_ = i < nwd ? (PA[i] & ~PB[i]) : 0u;
+        const uint32_t pa_ = i < nwd ? PA[i] : 0u, pb_ = i < nwd ? PB[i] : 0u;
+        // missing of child a: in B's prefix and not in A's (= in A's suffix and not in B's)
+        uint32_t wa_ = inv ? pa_ & ~pb_ : pb_ & ~pa_;
+        uint32_t wb_ = inv ? pb_ & ~pa_ : pa_ & ~pb_;
         int na = __popc(wa_), nb = __popc(wb_);
         int ia = na | (nb << 16);
 #pragma unroll
@@ -630,7 +641,7 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
         wset(za, k, (wa_ & m) | (wb_ & ~m));
         wset(zb, k, (wb_ & m) | (wa_ & ~m));
       }
-      if (repair) {
+      if (repair && 8 * (i0 + 32) > kc) {   // warp-uniform: some lane's word reaches the suffix
         // duplicates: suffix genes (kc <= g < K) whose value is in the own
         // parent's prefix -- one byte-map load per gene, no bit arithmetic
         // (padding genes hold value 0, slot 0 of the maps)
@@ -643,6 +654,10 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
           const uint32_t ta = (wsel(za, j >> 1) >> sh) & 0xFFFFu, tb = (wsel(zb, j >> 1) >> sh) & 0xFFFFu;
           fa += (uint32_t)FA[ta] << j;
           fb += (uint32_t)FB[tb] << j;
+        }
+        if (inv) {   // the maps hold the suffix values: "not in it" = "in the prefix"
+          fa = ~fa;
+          fb = ~fb;
         }
         fa &= sfx;
         fb &= sfx;
