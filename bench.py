@@ -341,6 +341,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
+            # NCCL's own log names the communicator (ranks, transport: NVLink / NVLS)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -395,7 +398,9 @@ def run_ours(args):
     t_max = float(t.item())
     evals_total = pop_local * world * args.steps
     value = evals_total / t_max
-    best = run.best()
+    # the ring's answer: the best of every shard's ffs_best and the global trace
+    # (one allgather after the timed region)
+    best = fdist.global_best(run.best()) if world > 1 else run.best()
 
     # ---- dominant kernel alone (decode + evaluate of the same 65,536 population,
     # same launch configuration), CUDA events on its stream
@@ -598,6 +603,10 @@ def run_ours(args):
                           "population": pop_local},
             "gpu_launches": launches,
             "best_objective": best["objective"],
+            "best": {"objective": best["objective"], "makespan": best["makespan"],
+                     "sum_tardiness": best["sum_tardiness"], "shard_rank": best.get("rank", 0),
+                     "trace_min_last": int(best["trace_min"][-1]),
+                     "scope": "global over all ranks (dist.global_best)" if world > 1 else "single GPU"},
             "sweep_E": sweep,
             "workflow_B": wf,
             "static_C": static_c,

@@ -425,6 +425,7 @@ __global__ void trace0_kernel(const int64_t *obj, int tile, int real, int nisl, 
 // ---- one generation's breeding for one horizontal pair (a, b = a + 1)
 struct GenArgs {
   int32_t K, O, cells, w, h, tile, island0, k;
+  int32_t half_sh, wh_sh;                      // log2(tile/2), log2(w/2) when powers of two, else -1
   uint32_t xo_thr, mut_thr;
   uint64_t seed;
   int64_t npairs;
@@ -493,18 +494,27 @@ __device__ __forceinline__ uint4 mutate16(uint4 v, int g0, uint32_t cell, uint32
   return v;
 }
 
+// 32 byte-map entries (0 or 1, 16-B aligned) -> one word, entry b at bit b:
+// (w * 0x01020408) >> 24 gathers the four bytes' low bits of w in order (no
+// carries: the partial products land on distinct bits)
+__device__ __forceinline__ uint32_t pack32(const uint8_t *m) {
+  const uint4 lo = ((const uint4 *)m)[0], hi = ((const uint4 *)m)[1];
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r |= ((w[k] * 0x01020408u) >> 24) << (4 * k);
+  return r;
+}
+
 __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
   extern __shared__ __align__(16) unsigned char gsm[];
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = a.K, nwd = (K + 31) >> 5;
-  const int fmb = (K + 1 + 15) & ~15;   // byte maps indexed by value 0..K (slot 0: padding genes)
-  const size_t pbm = ((size_t)2 * nwd * 4 + 15) & ~(size_t)15;   // both bit maps, 16-B multiple
-  const size_t per_warp = pbm + (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * fmb;
-  uint32_t *PA = (uint32_t *)(gsm + warp * per_warp);
-  uint32_t *PB = PA + nwd;
-  uint16_t *LA = (uint16_t *)((unsigned char *)PA + pbm);
+  const int K = a.K, nwd = (K + 32) >> 5;   // 32-value words of the maps (values 0..K)
+  const int fmb = nwd * 32;                 // byte maps indexed by value 0..K (slot 0: padding genes)
+  const size_t per_warp = (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * fmb;
+  uint16_t *LA = (uint16_t *)(gsm + warp * per_warp);
   uint16_t *LB = LA + ((K * 2 + 15) & ~15) / 2;
   uint8_t *FA = (uint8_t *)(LB + ((K * 2 + 15) & ~15) / 2);   // FA[v] = 1 iff v is in A's prefix
   uint8_t *FB = FA + fmb;
@@ -515,8 +525,8 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
   const int nxv = (int)(row >> 4), nyv = (int)(row >> 3);   // 16-B words of a row
   const uint32_t npairs = (uint32_t)a.npairs;               // < 2^30 (count < 2^31)
   for (uint32_t pi = blockIdx.x * (blockDim.x >> 5) + warp; pi < npairs; pi += nw) {
-    const uint32_t li = pi / half, pr = pi - li * half;
-    const uint32_t prow = pr / wh;
+    const uint32_t li = a.half_sh >= 0 ? pi >> a.half_sh : pi / half, pr = pi - li * half;
+    const uint32_t prow = a.wh_sh >= 0 ? pr >> a.wh_sh : pr / wh;
     const int pcol = 2 * (int)(pr - prow * wh);
     const int ca = (int)prow * a.w + pcol, cb = ca + 1;
     const uint32_t I = (uint32_t)a.island0 + li, kg = (uint32_t)a.k;
@@ -563,7 +573,6 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
       // correction (R14): duplicates of child a are the suffix genes of B
       // whose value occurs in A's prefix; missing values = in B's prefix, not
       // in A's prefix; assigned in ascending order to duplicates in gene order.
-      for (int i = lane; i < nwd; i += 32) { PA[i] = 0u; PB[i] = 0u; }
       for (int i = lane; i < (fmb >> 4); i += 32) {
         ((uint4 *)FA)[i] = make_uint4(0, 0, 0, 0);
         ((uint4 *)FB)[i] = make_uint4(0, 0, 0, 0);
@@ -578,9 +587,6 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
           if (g >= g_lo && g < g_hi) {   // values in [1, K]
             const int sh = 16 * (j & 1);
             const int va1 = (int)((wsel(va, j >> 1) >> sh) & 0xFFFFu), vb1 = (int)((wsel(vb, j >> 1) >> sh) & 0xFFFFu);
-            const int ta = va1 - 1, tb = vb1 - 1;
-            atomicOr(&PA[ta >> 5], 1u << (ta & 31));
-            atomicOr(&PB[tb >> 5], 1u << (tb & 31));
             FA[va1] = 1;
             FB[vb1] = 1;
           }
@@ -590,7 +596,8 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
       int offa = 0, offb = 0;
       for (int i0 = 0; i0 < nwd; i0 += 32) {
         int i = i0 + lane;
-        const uint32_t pa_ = i < nwd ? PA[i] : 0u, pb_ = i < nwd ? PB[i] : 0u;
+        // the maps' value bits (bit b of word i: value 32 i + b), packed in registers
+        const uint32_t pa_ = i < nwd ? pack32(FA + 32 * i) : 0u, pb_ = i < nwd ? pack32(FB + 32 * i) : 0u;
         // missing of child a: in B's prefix and not in A's (= in A's suffix and not in B's)
         uint32_t wa_ = inv ? pa_ & ~pb_ : pb_ & ~pa_;
         uint32_t wb_ = inv ? pb_ & ~pa_ : pa_ & ~pb_;
@@ -602,8 +609,8 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
           if (lane >= d) ia += t1;
         }
         int pa = offa + (ia & 0xFFFF) - na, pb = offb + (ia >> 16) - nb;
-        while (wa_) { int bit = __ffs(wa_) - 1; wa_ &= wa_ - 1; LA[pa++] = (uint16_t)(i * 32 + bit + 1); }
-        while (wb_) { int bit = __ffs(wb_) - 1; wb_ &= wb_ - 1; LB[pb++] = (uint16_t)(i * 32 + bit + 1); }
+        while (wa_) { int bit = __ffs(wa_) - 1; wa_ &= wa_ - 1; LA[pa++] = (uint16_t)(i * 32 + bit); }
+        while (wb_) { int bit = __ffs(wb_) - 1; wb_ &= wb_ - 1; LB[pb++] = (uint16_t)(i * 32 + bit); }
         const int tot = __shfl_sync(FULL, ia, 31);
         offa += tot & 0xFFFF;
         offb += tot >> 16;
@@ -704,8 +711,8 @@ __global__ void __launch_bounds__(256, 4) generation_kernel(GenArgs a) {
 }
 
 size_t gen_smem_per_warp(int K) {
-  int nwd = (K + 31) >> 5;
-  return (((size_t)2 * nwd * 4 + 15) & ~(size_t)15) + (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * ((K + 1 + 15) & ~15);
+  const int nwd = (K + 32) >> 5;
+  return (size_t)2 * ((K * 2 + 15) & ~15) + (size_t)2 * nwd * 32;
 }
 
 }  // namespace
@@ -774,6 +781,9 @@ static ffs_status ga_generation(Run &r) {
   GenArgs g{};
   g.K = r.K; g.O = st.inst->o; g.cells = st.cells; g.w = r.cfg.island_w; g.h = r.cfg.island_h;
   g.tile = r.tile; g.island0 = r.cfg.island_begin; g.k = k;
+  auto log2_or = [](int v) { return (v > 0 && (v & (v - 1)) == 0) ? __builtin_ctz((unsigned)v) : -1; };
+  g.half_sh = log2_or(r.tile / 2);
+  g.wh_sh = log2_or(r.cfg.island_w / 2);
   g.xo_thr = r.cfg.xo_threshold; g.mut_thr = r.cfg.mut_threshold; g.seed = r.cfg.seed;
   g.npairs = r.nloc / 2;
   g.cut = st.cut_dev;
