@@ -210,6 +210,80 @@ struct TraceArgs {
 __device__ void island_trace(const int64_t *obj_isl, int tile, int real, int li, int nisl, int64_t *parts,
                              unsigned *counter, int64_t *tmin, int64_t *tsum, int k);
 
+__device__ void block_min_sum(const int64_t *v, int64_t n, int real, long long &mn, long long &sm);
+
+// one pass over an island's cells for the integer objective: best / worst
+// fitness (ties -> lowest index), the worst cell's objective, and the island's
+// objective min and sum (the trace partial before replacement)
+__device__ void island_scan(const int64_t *fit, const int64_t *obj, int tile, int &best, int &worst, long long &ow,
+                            long long &omin, long long &osum) {
+  __shared__ long long sfb[32], sfw[32], sow[32], smn[32], ssm[32];
+  __shared__ int sib[32], siw[32];
+  int64_t fb = LLONG_MIN, fw = LLONG_MAX;
+  int ib = INT_MAX, iw = INT_MAX;
+  long long o_w = 0, mn = LLONG_MAX, sm = 0;
+  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+    const int64_t f = fit[i];
+    const long long o = obj[i];
+    better_max(fb, ib, f, i);
+    if (f < fw || (f == fw && i < iw)) { fw = f; iw = i; o_w = o; }
+    mn = min(mn, o);
+    sm += o;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    better_max(fb, ib, __shfl_xor_sync(FULL, fb, d), __shfl_xor_sync(FULL, ib, d));
+    const int64_t f2 = __shfl_xor_sync(FULL, fw, d);
+    const int i2 = __shfl_xor_sync(FULL, iw, d);
+    const long long o2 = __shfl_xor_sync(FULL, o_w, d);
+    if (f2 < fw || (f2 == fw && i2 < iw)) { fw = f2; iw = i2; o_w = o2; }
+    mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+    sm += __shfl_xor_sync(FULL, sm, d);
+  }
+  const int wp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sfb[wp] = fb; sib[wp] = ib; sfw[wp] = fw; siw[wp] = iw; sow[wp] = o_w; smn[wp] = mn; ssm[wp] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      better_max(fb, ib, sfb[k], sib[k]);
+      if (sfw[k] < fw || (sfw[k] == fw && siw[k] < iw)) { fw = sfw[k]; iw = siw[k]; o_w = sow[k]; }
+      mn = min(mn, smn[k]);
+      sm += ssm[k];
+    }
+    sib[0] = ib; siw[0] = iw; sow[0] = o_w; smn[0] = mn; ssm[0] = sm;
+  }
+  __syncthreads();
+  best = sib[0];
+  worst = siw[0];
+  ow = sow[0];
+  omin = smn[0];
+  osum = ssm[0];
+  __syncthreads();
+}
+
+// the island's trace partial is final: publish it; the last island block
+// (ticket) reduces the partials in island order into trace[k]
+__device__ void trace_publish(long long mn, long long sm, int real, int li, int nisl, int64_t *parts,
+                              unsigned *counter, int64_t *tmin, int64_t *tsum, int k) {
+  __shared__ unsigned ticket;
+  if (threadIdx.x == 0) {
+    parts[2 * li] = mn;
+    parts[2 * li + 1] = sm;
+    __threadfence();
+    ticket = atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  if (ticket != (unsigned)(nisl - 1)) return;
+  __threadfence();
+  block_min_sum(parts, nisl, real, mn, sm);
+  if (threadIdx.x == 0) {
+    tmin[k] = mn;
+    tsum[k] = sm;
+    *counter = 0u;
+  }
+}
+
 __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int64_t *obj, int64_t *fit, int8_t *hx,
                                int16_t *hy, int64_t *hobj, int64_t *hfit, TraceArgs tr) {
   pdl_trigger();
@@ -221,8 +295,15 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
     s_hist[0] = hfit[li];
     s_hist[1] = hobj[li];
   }
+  // integer objective with the trace due now: one pass gives the trace partial
+  // too (the worst cell's objective w_o is replaced by the elite's e_o <= w_o,
+  // Eq. (13) being decreasing: min' = min(min, e_o), sum' = sum - w_o + e_o);
+  // binary64 (f3) keeps R33's sequential sum over the updated cells below
+  const bool fused = tr.on && !tr.real;
   int b, w;
-  island_best_worst(fit + base, tile, b, w);   // (its barriers publish s_hist)
+  long long ow = 0, omin = 0, osum = 0;
+  if (fused) island_scan(fit + base, obj + base, tile, b, w, ow, omin, osum);
+  else island_best_worst(fit + base, tile, b, w);   // (their barriers publish s_hist)
   const int64_t cb = base + b, cw = base + w;
   int8_t *hxr = hx + (int64_t)li * row;
   int16_t *hyr = hy + (int64_t)li * row;
@@ -248,8 +329,9 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
       }
     }
   }
+  const int64_t ob = upd ? obj[cb] : (int64_t)s_hist[1];
   if (threadIdx.x == 0) {
-    const int64_t ob = upd ? obj[cb] : (int64_t)s_hist[1], fv = upd ? fb : (int64_t)s_hist[0];
+    const int64_t fv = upd ? fb : (int64_t)s_hist[0];
     if (upd) {
       hobj[li] = ob;
       hfit[li] = fv;
@@ -257,7 +339,10 @@ __global__ void replace_kernel(int64_t row, int tile, int8_t *x, int16_t *y, int
     obj[cw] = ob;
     fit[cw] = fv;
   }
-  if (tr.on) {   // no migration this generation: the trace is final now
+  if (fused) {   // no migration this generation: the trace is final now
+    trace_publish(min(omin, (long long)ob), osum - ow + (long long)ob, 0, li, tr.nisl, tr.parts, tr.counter,
+                  tr.tmin, tr.tsum, tr.k);
+  } else if (tr.on) {
     __syncthreads();
     island_trace(obj + base, tile, tr.real, li, tr.nisl, tr.parts, tr.counter, tr.tmin, tr.tsum, tr.k);
   }
