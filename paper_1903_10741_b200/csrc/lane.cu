@@ -249,28 +249,35 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   }
   __syncthreads();
   const int64_t ntile = (a.count + 31) / 32;
+  // BULK: one elected lane stages the warp's chromosome of tile `tl` (y row
+  // into pmv, x row into xs) by TMA bulk copies on the warp's mbarrier --
+  // ceil16(K) genes of the row (<= row: row % 16 == 0 and row >= K), never the
+  // whole row (the smem slots are sized from K, 128 * ceil(K/128)).  The copy
+  // of the warp's NEXT chromosome is issued as soon as pass D has consumed
+  // pmv / xs, so it lands during the CTA's write-out of the current tile.
+  auto stage_row = [&](const int64_t tl) {
+    const int64_t cc = tl * 32 + warp;
+    if (!BULK || lane != 0 || tl >= ntile || cc >= a.count) return;
+    const uint32_t kc = ((uint32_t)K + 15u) & ~15u;
+    const uint32_t yb = kc * 2u, xb = XS ? kc : 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the previous row's generic accesses
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(yb + xb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(pmv)),
+                 "l"(a.y + (a.first + cc) * a.row), "r"(yb), "r"(bar)
+                 : "memory");
+    if (XS)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(xs)),
+                   "l"(a.x + (a.first + cc) * a.row), "r"(xb), "r"(bar)
+                   : "memory");
+  };
+  stage_row(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     const int64_t c = tile * 32 + warp;
     if (c < a.count) {
       const int16_t *yr = a.y + (a.first + c) * a.row;
       const int8_t *xr = a.x + (a.first + c) * a.row;
-      if (BULK && lane == 0) {
-        // ceil16(K) genes of the row (<= row: row % 16 == 0 and row >= K), never
-        // the whole row: the smem slots are sized from K (128 * ceil(K/128))
-        const uint32_t kc = ((uint32_t)K + 15u) & ~15u;
-        const uint32_t yb = kc * 2u, xb = XS ? kc : 0u;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the previous row's generic writes
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(yb + xb) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(pmv)),
-                     "l"(yr), "r"(yb), "r"(bar)
-                     : "memory");
-        if (XS)
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           smem_u32(xs)),
-                       "l"(xr), "r"(xb), "r"(bar)
-                       : "memory");
-      }
       // hist/start are indexed by u = K - pm (descending prefix minimum)
       for (int i = lane; i < ((K + 511) >> 9) << 6; i += 32) ((uint4 *)hist)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncwarp();
@@ -281,7 +288,6 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       }
       // ---- pass A: prefix minima (kept with a leader flag in bit 15), run lengths
       int carry = INT_MAX;
-      int open_u = -1, open_pos = 0;   // the last run seen, length not yet known (warp-uniform)
       // software pipeline (global loads): tile t+1's genes are loaded while
       // tile t is scanned
       int yq[4];
@@ -307,50 +313,26 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         }
         pm_quad<SCAN>(y, *(const uint4 *)(mtab + g0), dtab[(t << 5) + lane], (uint32_t)carry, Z, pm);
         // leaders = new prefix minima (pm == y); each distinct pm is one run
-        // (a leader and the non-leaders after it in its job), and a run's
-        // length is stored once, by its leader, at u = K - pm: hist[u] = len
-        uint32_t pk[4], ua[4], lm = 0, lu = 0;
+        // (a leader and the non-leaders after it in its job) at u = K - pm,
+        // so hist[u] = run length: every gene of the tile adds one to its
+        // run's u16 slot (red.shared.add on the slot's 32-bit word; a half
+        // never carries, counts <= K < 2^16)
+        uint32_t pk[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const unsigned v = (unsigned)(pm[k] - 1);
           const bool ok = FT || (g0 + k < K && v < (unsigned)K);
           const unsigned u = ok ? (unsigned)K - 1u - v : (unsigned)K;
           const bool ld = ok && pm[k] == y[k];
-          lm |= (ld ? 1u : 0u) << k;
           pk[k] = u | (ld ? 0x8000u : 0u);
-          ua[k] = h16s + 2u * u;   // hist slot of the gene's run
-          lu = ld ? u : lu;   // the lane's last leader
+          const uint32_t wa = (h16s + 2u * u) & ~3u, inc = (u & 1u) * 0xFFFFu + 1u;
+          if (ok) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(wa), "r"(inc) : "memory");
         }
         *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
-        // next leader after each of the lane's leaders: inside the quad, else
-        // the first leader of the next lane holding one, else (the tile's
-        // last leader) still open: closed by a later tile or by K
-        const uint32_t B = __ballot_sync(FULL, lm != 0u);
-        const int fpos = g0 + __ffs(lm) - 1;
-        const uint32_t hiB = B & (0xFFFFFFFEu << lane);
-        const int nxl = __shfl_sync(FULL, fpos, hiB ? __ffs(hiB) - 1 : 0);
-        {   // branch-free (B == 0: fl = ll = -1, nothing changes)
-          const int fl = __ffs(B) - 1;
-          const int first = __shfl_sync(FULL, fpos, fl & 31);
-          sts16_if(open_u >= 0 && lane == fl, h16s + 2u * (uint32_t)open_u, (uint32_t)(first - open_pos));
-          const int ll = (31 - __clz(B)) & 31;
-          const int np = __shfl_sync(FULL, g0 + 31 - __clz(lm | 1u), ll);
-          const int nu = __shfl_sync(FULL, (int)lu, ll);
-          open_pos = B ? np : open_pos;
-          open_u = B ? nu : open_u;
-        }
-        int nx = hiB ? nxl : -1;
-#pragma unroll
-        for (int k = 3; k >= 0; --k) {
-          const bool ldk = (lm >> k) & 1u;
-          sts16_if(ldk && nx >= 0, ua[k], (uint32_t)(nx - (g0 + k)));
-          nx = ldk ? g0 + k : nx;
-        }
         carry = __shfl_sync(FULL, pm[3], 31);
       };
       for (int t = 0; t + 1 < NT; ++t) tileA(t, std::true_type{});
       tileA(NT - 1, std::false_type{});
-      if (open_u >= 0 && lane == 0) h16[open_u] = (uint16_t)(K - open_pos);
       __syncwarp();
       // ---- pass C: start[u] = #genes with u' < u (exclusive prefix over u),
       // 16 counts (u16 pairs) per lane per step of 512 (entries >= K are
@@ -440,6 +422,10 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
       };
       for (int t = 0; t + 1 < NT; ++t) tileD(t, std::true_type{});
       tileD(NT - 1, std::false_type{});
+      if (BULK) {   // pmv / xs are consumed: stage the warp's next chromosome
+        __syncwarp();
+        stage_row(tile + gridDim.x);
+      }
     }
     __syncthreads();
     // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome
