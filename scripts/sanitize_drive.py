@@ -6,7 +6,8 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 Covers: state staging, the lane path (order kernel with and without x
 staging, both row layouts; decode modes 0/1/2; the LIST re-decode), the warp
 path and the overflow fallback, random_population, the island GA (generation, replace,
-migration, trace), the brute force.  Checks nothing itself -- the tool does."""
+migration, trace; config A and the config C shape; the binary64 trace), calls on
+two streams, the brute force.  Checks nothing itself -- the tool does."""
 import os
 import sys
 
@@ -70,6 +71,24 @@ def main():
         run = ffs.Run(st, 4, 4, 4, 12, 10741)
         run.step(12)
         run.best()
+        # config C shape (K = 1,000 at RS = 0): multi-word breeding loops, both
+        # sides of the cut, migration every 2, the one-pass replacement + trace
+        wc = wlmod.config_C()
+        stc = state_of(wc.original_instance())
+        runc = ffs.Run(stc, 16, 16, 2, 3, 10741, migration_interval=2)
+        runc.step(3)
+        runc.best()
+        # binary64 objective (f3): the R33 sequential trace sums
+        str_ = state_of(wa.original_instance())
+        str_.set_objective_weight(0.37)
+        runr = ffs.Run(str_, 4, 4, 4, 5, 7)
+        runr.step(5)
+        runr.best()
+        # device calls on two streams sharing the state's scratch
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        x1, y1 = ffs.random_population(stc, 64, 1)
+        ffs.evaluate(stc, x1, y1, stream=s1)
+        ffs.evaluate(stc, x1, y1, stream=s2)
     if which in ("all", "brute"):
         rng = np.random.default_rng(1)
         n, g, o = 3, 2, 2
