@@ -87,6 +87,7 @@ def main():
         # device calls on two streams sharing the state's scratch
         s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
         x1, y1 = ffs.random_population(stc, 64, 1)
+        torch.cuda.synchronize()   # the rows come from the default stream
         ffs.evaluate(stc, x1, y1, stream=s1)
         ffs.evaluate(stc, x1, y1, stream=s2)
     if which in ("all", "brute"):

@@ -32,7 +32,22 @@ def _state():
     return st
 
 
-def _worker(rank, world, port, out_dir):
+def _state_c():
+    """Config C's frozen state (K = 855), built on the GPU as bench.py does."""
+    from paper_1903_10741_b200 import ffs
+    from paper_1903_10741_b200 import workload as wlmod
+    wl = wlmod.config_C()
+    base = ffs.Instance.from_arrays(wl.original_instance(), device=0)
+    st0 = ffs.make_state(base, 0)
+    assign, start, _, _, M = ffs.decode_schedule(st0, wl.plan_x, wl.plan_y)
+    rs = wl.rs_from_makespan(wl.ratios[0], M)
+    inst = ffs.Instance.from_arrays(wl.instance_at(0, [rs]), device=0)
+    st = ffs.make_state(inst, rs, wl.plan_x.astype(np.int32), start[: wl.n * wl.g])
+    st._keep = (base, st0, inst)
+    return st
+
+
+def _worker(rank, world, port, out_dir, cfg="A"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,11 +55,11 @@ def _worker(rank, world, port, out_dir):
         from paper_1903_10741_b200 import dist as fdist
         from paper_1903_10741_b200 import ffs
         torch.cuda.set_device(0)
-        st = _state()
-        b, e = fdist.shard(ISLANDS, rank, world)
-        run = ffs.Run(st, ISL_W, ISL_H, ISLANDS, G, SEED, island_begin=b, island_end=e, rank=rank, world=world,
-                      hooks=fdist.make_hooks(device_memory=True))
-        run.step(G)
+        st, (w, h, isl, g, mi) = (_state(), (ISL_W, ISL_H, ISLANDS, G, 10)) if cfg == "A" else (_state_c(), C_SHAPE)
+        b, e = fdist.shard(isl, rank, world)
+        run = ffs.Run(st, w, h, isl, g, SEED, island_begin=b, island_end=e, rank=rank, world=world,
+                      hooks=fdist.make_hooks(device_memory=True), migration_interval=mi)
+        run.step(g)
         x, y, obj, fit = run.population()
         hx, hy, hobj, hfit = run.history()
         gb = fdist.global_best(run.best())
@@ -54,16 +69,22 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def test_two_rank_ga_equals_single_process(tmp_path):
+C_SHAPE = (16, 16, 6, 9, 4)   # config C tiles, 6 islands over 2 ranks, 9 generations, migration every 4
+
+
+@pytest.mark.parametrize("cfg", ["A", "C"])
+def test_two_rank_ga_equals_single_process(tmp_path, cfg):
+    """cfg C: config C's instance (K = 855: 2,581-byte migration records) in
+    16x16 tiles, the ring crossing the shard boundary in both migrations."""
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, str(tmp_path), cfg), nprocs=2, join=True)
     from paper_1903_10741_b200 import ffs
-    st = _state()
-    run = ffs.Run(st, ISL_W, ISL_H, ISLANDS, G, SEED)
-    run.step(G)
+    st, (w, h, isl, g, mi) = (_state(), (ISL_W, ISL_H, ISLANDS, G, 10)) if cfg == "A" else (_state_c(), C_SHAPE)
+    run = ffs.Run(st, w, h, isl, g, SEED, migration_interval=mi)
+    run.step(g)
     x, y, obj, fit = run.population()
     hx, hy, hobj, _ = run.history()
     parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(2)]
