@@ -427,23 +427,29 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         stage_row(tile + gridDim.x);
       }
     }
-    __syncthreads();
     // lane-interleaved write-out: element (q, cc) = ranks 4q..4q+3 of chromosome
-    // cc, at dst[32 q + cc]; with 32 x 32 threads, thread (warp w, lane l) moves
-    // chromosome l's elements q = w, w + 32, ... (conflict-free: the staged
-    // arrays are an odd number of 8-byte words apart).  Ranks >= K hold the
-    // zeros written at kernel start (a valid table index).
-    if (lane < a.count - tile * 32) {
-      const unsigned char *src = ordb + (size_t)lane * a.ord_stride + (size_t)warp * 8;
-      uint2 *dst = (uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + warp * 32 + lane;
+    // cc, at dst[32 q + cc].  Four independent groups of 8 warps (named
+    // barriers 1..4, 256 threads): group G moves chromosomes 8G..8G+7, i.e.
+    // bytes 64G..64G+63 (two whole sectors) of every 256-byte quad row; its
+    // thread t moves chromosome 8G + t%8's quads q = t/8, t/8 + 32, ...
+    // (conflict-free: the staged arrays are an odd number of 8-byte words
+    // apart).  Ranks >= K hold the zeros written at kernel start.
+    {
+      const int grp = warp >> 3, t = ((warp & 7) << 5) | lane;
+      const int cc = (grp << 3) | (t & 7);
+      asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
+      if (cc < a.count - tile * 32) {
+        const unsigned char *src = ordb + (size_t)cc * a.ord_stride + (size_t)(t >> 3) * 8;
+        uint2 *dst = (uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + (t >> 3) * 32 + cc;
 #pragma unroll 2
-      for (int qd = warp; qd < KQ; qd += 32) {
-        *dst = *(const uint2 *)src;
-        src += 256;
-        dst += 1024;
+        for (int qd = t >> 3; qd < KQ; qd += 32) {
+          *dst = *(const uint2 *)src;
+          src += 256;
+          dst += 1024;
+        }
       }
+      asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
     }
-    __syncthreads();
   }
 }
 
