@@ -136,6 +136,15 @@ FFS_API ffs_status ffs_state_cut_table(const ffs_state *st, int32_t *pending_bef
 FFS_API ffs_status ffs_state_set_horizon_cap(ffs_state *st, int32_t cap);
 FFS_API ffs_status ffs_state_info(const ffs_state *st, int32_t *K, int32_t *cells, int32_t *horizon_cap,
                           int32_t *horizon_bound, int32_t *smem_bytes_per_cta);
+/* Which decode path ffs_evaluate takes for this state (diagnostic; host
+ * pointers, each may be NULL): *lane_path = 1 for the lane path (order kernel
+ * + lane-per-chromosome decode: P <= 8, Q_max <= 127, the order kernel's
+ * shared memory fits, and every job's pending genes fit the order kernel's
+ * u16 gene key: max_pending <= 2^(16 - ceil(log2 K))), else 0 (the general
+ * warp-per-chromosome kernel, same results); *lane_mode = the lane decoder's
+ * profile mode (2: uniform power, headroom bit planes; 0/1: byte levels);
+ * *max_pending = the most pending genes of one job. */
+FFS_API ffs_status ffs_state_path(const ffs_state *st, int32_t *lane_path, int32_t *lane_mode, int32_t *max_pending);
 FFS_API void ffs_state_destroy(ffs_state *st);
 
 /* ------------------------------------------------------------------------

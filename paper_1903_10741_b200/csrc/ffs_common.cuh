@@ -204,6 +204,7 @@ struct State {
   bool ord_xs = false;   // order kernel stages x rows (ord_smem + ord_xs_bytes fits)
   // ^ order kernel (32 warps per CTA)
   int32_t max_pending = 0;                                   // most pending genes of one job
+  int32_t ord_ubits = 1;                                     // order kernel: bits of u = K - pm (2^ubits >= K)
   int ord_ctas_per_sm = 1;
   OvfScratch scratch;
   HostStage stage;

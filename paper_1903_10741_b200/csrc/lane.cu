@@ -67,6 +67,9 @@ __device__ __forceinline__ uint32_t lds16_if_flag(bool p, uint32_t a) {
                : "memory");
   return v;
 }
+// keep a staged value in a register (no rematerialisation on the critical path)
+__device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
+__device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
 // lane-interleaved u16 element v: word v/2, half v%2
 [[maybe_unused]] __device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
   return base + ((v >> 1) << 7) + ((v & 1u) << 1);
@@ -87,14 +90,15 @@ __device__ __forceinline__ uint32_t flag_nibble(uint32_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// Algorithm 1: one WARP per chromosome (2 genes per lane per 64-gene tile),
+// Algorithm 1: one WARP per chromosome (4 genes per lane per 128-gene tile),
 // 32 chromosomes per CTA; the CTA writes the tile's orders lane-interleaved.
-//   pass A  pm(g) = min y over the job's pending stages <= s (segmented warp
-//           scan, segments start at each job's first pending gene);
-//           hist[pm - 1] += 1  (shared atomics on u16 halves of u32 words)
-//   pass C  start[v] = #genes with pm > v + 1 (exclusive suffix sum)
-//   pass D  rank(g) = start[pm(g) - 1] + (g - position of g's run leader),
-//           leaders being the genes with pm == y (new prefix minima)
+//   pass A  (pm(g), g_L(g)) = min of the keys y << 16 | g over the job's
+//           pending stages <= s (segmented warp scan, segments start at each
+//           job's first pending gene): pm = the prefix minimum of y, g_L =
+//           the gene holding it (the run's leader, a new prefix minimum);
+//           the run's last gene stores hist[u] = g - g_L + 1, u = K - pm
+//   pass C  start[u] = #genes with u' < u (exclusive prefix sum)
+//   pass D  rank(g) = start[u(g)] + (g - g_L(g))
 // ---------------------------------------------------------------------------
 struct OrdArgs {
   const int8_t *x;
@@ -110,6 +114,7 @@ struct OrdArgs {
   uint32_t ord_stride;     // bytes between staged ord arrays (8 * odd)
   uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
   int32_t *zero0, *zero1;  // first chunk: the overflow lists' counts to reset (else null)
+  int32_t ubits;           // pass A/D key: u = K - pm in the low ubits, g - g_L above (2^ubits >= K)
 };
 
 // prefix minima of the lane's four genes given the running min before the tile.
@@ -121,8 +126,9 @@ struct OrdArgs {
 // iff the gene starts a segment: a job's first pending gene, or padding), and
 // dsc = the lane's scan-step enables (bit i: combine with lane - 2^i) and, in
 // bit 31, "a segment starts in an earlier lane of this tile".  A reset is an
-// OR with all ones before an unsigned min (y and the running minima are in
-// [1, INT_MAX]), so no compare / select per gene.
+// OR with all ones before an unsigned min (the keys y << 16 | g and the
+// running minima are below 2^31 (y <= K < 2^15); padding keys are all ones),
+// so no compare / select per gene.
 template <int SCAN>
 __device__ __forceinline__ void pm_quad(const int y[4], const uint4 M, uint32_t dsc, uint32_t carry, uint32_t Z,
                                         int pm[4]) {
@@ -208,14 +214,14 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   // segment reset masks and per-lane scan descriptors (pm_quad); and (XS)
   // per-warp staging of the chromosome's machines
   unsigned char *tail = smem + (size_t)32 * (a.hist_bytes + a.ord_stride + a.pm_bytes);
-  // gene table TRANSPOSED inside each 128-gene tile: gene 128t + 4l + k at
-  // 128t + 32k + l, so pass D's reads (lane l, gene k) hit 32 distinct banks
+  // gene table (pass D's strided reads hit 32 distinct banks)
   uint32_t *gtab = (uint32_t *)tail;
   uint32_t *mtab = gtab + 128 * NT;
   uint32_t *dtab = mtab + 128 * NT;
-  uint8_t *xs = (uint8_t *)(dtab + 32 * NT) + (size_t)warp * 128 * NT;   // XS only
+  uint32_t *btab = dtab + 32 * NT;   // per (tile, lane): byte k = 0xFF iff gene k of the quad starts a segment
+  uint8_t *xs = (uint8_t *)(btab + 32 * NT) + (size_t)warp * 128 * NT;   // XS only
   for (int i = threadIdx.x; i < K; i += blockDim.x)
-    gtab[(i & ~127) | ((i & 3) << 5) | ((i >> 2) & 31)] = __ldg(a.gbase + i);
+    gtab[i] = __ldg(a.gbase + i);
   for (int i = threadIdx.x; i < 128 * NT; i += blockDim.x)
     mtab[i] = (i >= K || ((__ldg(a.head + (i >> 5)) >> (i & 31)) & 1u)) ? 0xFFFFFFFFu : 0u;
   __syncthreads();
@@ -225,6 +231,10 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
     const uint32_t below = hb & (0xFFFFFFFFu >> (31 - lane));
     const int s0 = below ? 31 - __clz(below) : -1;
     uint32_t dsc = (hb & ((1u << lane) - 1u)) ? 0x80000000u : 0u;
+    // bit 30: the gene after the lane's quad starts a job, or is past K
+    const int gn = (t << 7) + 4 * lane + 4;
+    if (gn >= 128 * NT || mtab[gn] != 0u) dsc |= 0x40000000u;
+    btab[(t << 5) + lane] = (m.x & 0xFFu) | (m.y & 0xFF00u) | (m.z & 0xFF0000u) | (m.w & 0xFF000000u);
 #pragma unroll
     for (int i = 0; i < 5; ++i)
       if (lane - (1 << i) >= s0 && lane >= (1 << i)) dsc |= 1u << i;
@@ -286,50 +296,80 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         }
         phase ^= 1u;
       }
-      // ---- pass A: prefix minima (kept with a leader flag in bit 15), run lengths
-      int carry = INT_MAX;
+      // ---- pass A: prefix minima over packed keys (y << 16 | g): the minimum
+      // carries its own gene, so every gene knows its run's leader g_L
+      // (y is a permutation: the minimum is unique).  A run = a leader (new
+      // prefix minimum) and the non-leaders after it in its job, all at
+      // u = K - pm; its LAST gene (the next gene leads a run or starts a job)
+      // stores the run length g - g_L + 1 into hist[u] -- one plain u16
+      // store per run, no atomics.  pmv keeps u | (g - g_L) << ub per gene.
+      uint32_t carry = 0xFFFFFFFFu;
+      uint32_t umul = 1u << a.ubits;
+      pin(umul);   // multiplies (fma pipe), not shifts
+      const uint32_t hK2 = h16s + 2u * (uint32_t)K;
       // software pipeline (global loads): tile t+1's genes are loaded while
       // tile t is scanned
       int yq[4];
-      uint32_t xq = 0;
+      uint32_t xq = 0, ynq = 0;
       if (!BULK) {
         load_quad<false>(yr, K, 4 * lane, yq);
+        ynq = 4 * lane + 4 < K ? (uint32_t)__ldg(yr + 4 * lane + 4) : 0u;
         if (XS) load_xquad(xr, K, 4 * lane, xq);
       }
       auto tileA = [&](const int t, auto fullc) {
         constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
         const int g0 = (t << 7) + 4 * lane;
-        int y[4], pm[4];
+        // keys y << 16 | g (padding: all ones); yn = y of the gene after the
+        // quad (only read when it continues the job)
+        uint32_t yp[4], yn;
         if (BULK) {
-          load_quad<true, FT>((const int16_t *)pmv, K, g0, y);
+          const uint2 w = *(const uint2 *)(pmv + g0);
+          yp[0] = __byte_perm(w.x, (uint32_t)g0, 0x1054);
+          yp[1] = __byte_perm(w.x, (uint32_t)(g0 + 1), 0x3254);
+          yp[2] = __byte_perm(w.y, (uint32_t)(g0 + 2), 0x1054);
+          yp[3] = __byte_perm(w.y, (uint32_t)(g0 + 3), 0x3254);
+          // lane 31's successor is the next tile's first gene, not yet overwritten
+          const uint32_t nt = t + 1 < NT ? (uint32_t)pmv[(t + 1) << 7] : 0u;
+          const uint32_t dn = __shfl_down_sync(FULL, w.x & 0xFFFFu, 1);
+          yn = lane == 31 ? nt : dn;
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) y[k] = yq[k];
+          for (int k = 0; k < 4; ++k) yp[k] = ((uint32_t)yq[k] << 16) | (uint32_t)(g0 + k);
+          yn = ynq;
           if (XS) *(uint32_t *)(xs + g0) = xq;
           if (t + 1 < NT) {
             load_quad<false>(yr, K, g0 + 128, yq);
+            ynq = g0 + 132 < K ? (uint32_t)__ldg(yr + g0 + 132) : 0u;
             if (XS) load_xquad(xr, K, g0 + 128, xq);
           }
         }
-        pm_quad<SCAN>(y, *(const uint4 *)(mtab + g0), dtab[(t << 5) + lane], (uint32_t)carry, Z, pm);
-        // leaders = new prefix minima (pm == y); each distinct pm is one run
-        // (a leader and the non-leaders after it in its job) at u = K - pm,
-        // so hist[u] = run length: every gene of the tile adds one to its
-        // run's u16 slot (red.shared.add on the slot's 32-bit word; a half
-        // never carries, counts <= K < 2^16)
+        if (!FT) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) yp[k] = g0 + k < K ? yp[k] : 0xFFFFFFFFu;
+        }
+        int rp[4];
+        const uint32_t dsc = dtab[(t << 5) + lane];
+        const uint32_t bf = btab[(t << 5) + lane];   // reset masks by sign-replicating byte permutes
+        const uint4 M = make_uint4(__byte_perm(bf, 0u, 0x8888u), __byte_perm(bf, 0u, 0x9999u),
+                                   __byte_perm(bf, 0u, 0xAAAAu), __byte_perm(bf, 0u, 0xBBBBu));
+        pm_quad<SCAN>((const int *)yp, M, dsc, carry, Z, rp);
+        // the gene after gene k leads a run (a new minimum, or a job's first
+        // pending gene: its reset makes it its own minimum); after the quad:
+        // dsc bit 30 (job start or past K) or y below the running minimum
+        bool last[4];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) last[k] = (uint32_t)rp[k + 1] == yp[k + 1];
+        last[3] = ((dsc >> 30) & 1u) || (yn << 16) < (uint32_t)rp[3];
         uint32_t pk[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const unsigned v = (unsigned)(pm[k] - 1);
-          const bool ok = FT || (g0 + k < K && v < (unsigned)K);
-          const unsigned u = ok ? (unsigned)K - 1u - v : (unsigned)K;
-          const bool ld = ok && pm[k] == y[k];
-          pk[k] = u | (ld ? 0x8000u : 0u);
-          const uint32_t wa = (h16s + 2u * u) & ~3u, inc = (u & 1u) * 0xFFFFu + 1u;
-          if (ok) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(wa), "r"(inc) : "memory");
+          const uint32_t pm = (uint32_t)rp[k] >> 16;
+          const uint32_t o1 = (uint32_t)(g0 + k + 1) - ((uint32_t)rp[k] & 0xFFFFu);   // g - g_L + 1
+          pk[k] = o1 * umul - pm;   // (g - g_L) << ub | (2^ub - pm), 2^ub - pm = u + 2^ub - K
+          sts16_if((FT || g0 + k < K) && last[k], hK2 - 2u * pm, o1);   // hist[u], u = K - pm
         }
-        *(uint2 *)(pmv + g0) = make_uint2(pk[0] | (pk[1] << 16), pk[2] | (pk[3] << 16));
-        carry = __shfl_sync(FULL, pm[3], 31);
+        *(uint2 *)(pmv + g0) = make_uint2(__byte_perm(pk[0], pk[1], 0x5410), __byte_perm(pk[2], pk[3], 0x5410));
+        carry = __shfl_sync(FULL, (uint32_t)rp[3], 31);
       };
       for (int t = 0; t + 1 < NT; ++t) tileA(t, std::true_type{});
       tileA(NT - 1, std::false_type{});
@@ -367,58 +407,45 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
         acc += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
-      // ---- pass D: a leader at g ranks start[u(g)]; the genes after it in its
-      // run follow consecutively: rank(g) = base + g with base = start - g_leader
-      int carry_b = 0;
+      // ---- pass D: rank(g) = start[u(g)] + (g - g_L): per gene, no cross-lane work
       // the lane's four machines of tile t (!XS): one aligned word of a padded
       // row (BULK), else bytes; loaded one tile ahead to hide the latency
+      // Genes are STRIDED here (lane l takes genes 128t + 32k + l), so the 32
+      // lanes of one access hold consecutive genes: a run's genes read the
+      // same start[u] (broadcast) and write consecutive ranks, which keeps the
+      // gathers and the scatter nearly free of bank conflicts.
+      // The lane's four machines of tile t (!XS): bytes of the x row, loaded
+      // one tile ahead to hide the latency.
+      uint32_t xnext[4] = {0u, 0u, 0u, 0u};
       auto loadx = [&](const int t) {
-        const int g0 = (t << 7) + 4 * lane;
-        uint32_t v = 0u;
-        if (XS) {
-        } else if (BULK) {
-          if (g0 < K) v = __ldg((const uint32_t *)(xr + g0));
-        } else {
-          load_xquad(xr, K, g0, v);
-        }
-        return v;
-      };
-      uint32_t xnext = loadx(0);
-      auto tileD = [&](const int t, auto fullc) {
-        constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
-        const int g0 = (t << 7) + 4 * lane;
-        const uint2 w = *(const uint2 *)(pmv + g0);
-        const uint32_t pk[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
-        int bk[4], lastb = 0;
-        uint32_t lm = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {   // leaders only: padding genes carry u = K, no flag
-          const bool ldk = (pk[k] & 0x8000u) != 0u;
-          bk[k] = (int)lds16_if_flag(ldk, h16s + 2u * pk[k]) - (g0 + k);
-          lastb = ldk ? bk[k] : lastb;
-          lm |= (ldk ? 1u : 0u) << k;
-        }
-        const uint32_t B = __ballot_sync(FULL, lm != 0u);
-        const uint32_t lb = B & ((1u << lane) - 1u);
-        const int inb = __shfl_sync(FULL, lastb, lb ? 31 - __clz(lb) : 0);
-        int base = lb ? inb : carry_b;
-        const int tb = (int)(t << 7) + lane;   // transposed gene-table column of gene k: tb + 32k
-        uint32_t xw = xnext;
-        if (XS)
-          xw = *(const uint32_t *)(xs + g0);
-        else if (t + 1 < NT)
-          xnext = loadx(t + 1);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int g = g0 + k;
-          base = ((lm >> k) & 1u) ? bk[k] : base;
-          if (FT)
-            ord[base + g] = (uint16_t)(gtab[tb + 32 * k] + __byte_perm(xw, 0u, 0x4440u + k));
-          else
-            sts16_if(g < K, ords + 2u * (uint32_t)(base + g), gtab[tb + 32 * k] + __byte_perm(xw, 0u, 0x4440u + k));
+          const int g = (t << 7) + 32 * k + lane;
+          xnext[k] = g < K ? (uint32_t)(uint8_t)__ldg(xr + g) : 0u;
         }
-        const int cb = __shfl_sync(FULL, lastb, (31 - __clz(B)) & 31);
-        carry_b = B ? cb : carry_b;
+      };
+      if (!XS) loadx(0);
+      const uint32_t umask = umul - 1u, hbase = hK2 - 2u * umul;   // start[u] at hbase + 2 (u + 2^ub - K)
+      auto tileD = [&](const int t, auto fullc) {
+        constexpr bool FT = decltype(fullc)::value;   // every gene of the tile < K
+        const int gb = (t << 7) + lane;
+        uint32_t xk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xk[k] = XS ? (uint32_t)xs[gb + 32 * k] : xnext[k];
+        if (!XS && t + 1 < NT) loadx(t + 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int g = gb + 32 * k;
+          const bool ok = FT || g < K;
+          const uint32_t pk = pmv[g];
+          const uint32_t st = ok ? lds16(hbase + 2u * (pk & umask)) : 0u;
+          const uint32_t rank = st + (pk >> a.ubits);
+          const uint32_t e = gtab[g] + xk[k];
+          if (FT)
+            ord[rank] = (uint16_t)e;
+          else
+            sts16_if(ok, ords + 2u * rank, e);
+        }
       };
       for (int t = 0; t + 1 < NT; ++t) tileD(t, std::true_type{});
       tileD(NT - 1, std::false_type{});
@@ -500,9 +527,6 @@ struct OpA {
   uint32_t e, ra, ma, QQ, M1, M2, M4;
   int p, q, rsh, msh, sft;
 };
-// keep a staged value in a register (no rematerialisation on the critical path)
-__device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
-__device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
 __device__ __forceinline__ OpA stage_a(const uint32_t *pqt, const LaneCtx &L, int GO, uint32_t e) {
   OpA A;
   const uint32_t tv = pqt[e];
@@ -1103,6 +1127,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.hist_bytes = (uint32_t)st.ord_hist_bytes;
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
+    oa.ubits = st.ord_ubits;
     oa.zero0 = first == 0 ? scr.list : nullptr;
     oa.zero1 = first == 0 ? scr.list2 : nullptr;
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);

@@ -336,6 +336,11 @@ ffs_status State::build_image() {
   fb_smem_bytes = H.image_bytes + (size_t)fb_warps_per_cta * fb_per_warp_bytes;
 
   // --- lane-decode path (one lane per chromosome): eligibility and geometry
+  max_pending = 0;
+  for (int k = 0, run = 0; k < K; ++k) {   // longest run of one job's pending genes
+    run = (k > 0 && gene_job[k] == gene_job[k - 1]) ? run + 1 : 1;
+    max_pending = std::max(max_pending, run);
+  }
   lane_ok = !lane_disabled && K >= 1 && in.q_max <= 127 && pmax <= 8 && (int64_t)NJ * G * O <= 65536 && lvl_bytes == 1;
   if (lane_ok) {
     const int64_t lbudget = kSmemLimit - (int64_t)H.lane_image_bytes - 3072;   // static smem: mask tables + mbarrier
@@ -355,22 +360,22 @@ ffs_status State::build_image() {
     int warps = (int)std::min<int64_t>(16, lbudget / (words(hc) * 128));
     // order kernel: 32 warps, per warp hist[K] u16 + ord[K] u16 (stride 8*odd)
     ord_hist_bytes = (size_t)((K + 511) / 512 * 512) * 2;                              // u16 [K], steps of 512
-    max_pending = 0;
-    for (int k = 0, run = 0; k < K; ++k) {   // longest run of one job's pending genes
-      run = (k > 0 && gene_job[k] == gene_job[k - 1]) ? run + 1 : 1;
-      max_pending = std::max(max_pending, run);
-    }
     ord_stride = ((size_t)(K + 1) * 2 + 7) / 8 * 8;                                    // ord [K] + dummy slot
     if ((ord_stride / 8) % 2 == 0) ord_stride += 8;
     {
       const size_t ntl = (size_t)(K + 127) / 128;
       ord_smem = 32 * (ord_hist_bytes + ord_stride + ((ntl * 128 * 2 + 15) & ~(size_t)15)) +   // per warp
-                 ntl * 128 * 4 * 2 + ntl * 32 * 4;                                               // gtab, mtab, dtab
+                 ntl * 128 * 4 * 2 + ntl * 32 * 4 * 2;                                           // gtab, mtab, dtab, btab
       ord_xs_bytes = 32 * ntl * 128;   // per-warp x staging, when it fits
       ord_xs = !ord_xs_disabled && ord_smem + ord_xs_bytes + 2048 <= (size_t)kSmemLimit;
     }
     ord_ctas_per_sm = 1;  // 32 warps x <= 64 registers
-    if (warps < 2 || hc < 32 || ord_smem + 2048 > (size_t)kSmemLimit || K > 65535) {   // + static smem
+    // the order kernel keeps u = K - pm (< K) and g - g_L (< max_pending) in
+    // one u16 per gene (keys y << 16 | g, y <= K < 2^15)
+    ord_ubits = 1;
+    while ((1 << ord_ubits) < K) ++ord_ubits;
+    const bool ord_fits = ord_ubits <= 15 && max_pending <= (1 << (16 - ord_ubits));
+    if (!ord_fits || warps < 2 || hc < 32 || ord_smem + 2048 > (size_t)kSmemLimit) {   // + static smem
       lane_ok = false;
     } else {
       lane_hcap = (int32_t)hc;
@@ -652,6 +657,14 @@ ffs_status ffs_state_info(const ffs_state *h, int32_t *K, int32_t *cells, int32_
   if (hcap) *hcap = h->v.lane_ok ? h->v.lane_hcap : h->v.h_cap;
   if (hb) *hb = h->v.h_bound;
   if (smem) *smem = (int32_t)(h->v.lane_ok ? h->v.lane_smem : h->v.smem_bytes);
+  return FFS_OK;
+}
+
+ffs_status ffs_state_path(const ffs_state *h, int32_t *lane_path, int32_t *lane_mode, int32_t *max_pending) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null state");
+  if (lane_path) *lane_path = h->v.lane_ok ? 1 : 0;
+  if (lane_mode) *lane_mode = ((const ImageHdr *)h->v.image_host.data())->lane_mode;
+  if (max_pending) *max_pending = h->v.max_pending;
   return FFS_OK;
 }
 

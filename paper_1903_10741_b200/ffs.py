@@ -25,7 +25,7 @@ MUT_010 = 429496729   # floor(0.1 * 2^32), mutation rate of P:395
 EXPORTS = [
     "ffs_last_error", "ffs_version", "ffs_instance_create", "ffs_instance_destroy",
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
-    "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_destroy", "ffs_evaluate",
+    "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_path", "ffs_state_destroy", "ffs_evaluate",
     "ffs_evaluate_host", "ffs_evaluate_strided", "ffs_brute_force", "ffs_random_population", "ffs_random_population_strided", "ffs_evolve_begin", "ffs_evolve_step",
     "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
     "ffs_run_destroy",
@@ -81,7 +81,7 @@ def lib():
             "ffs_state_set_horizon_cap": ([P, C.c_int32], C.c_int),
             "ffs_state_set_objective_weight": ([P, C.c_double], C.c_int),
             "ffs_brute_force": ([P, C.c_int64, P, P, P, P, P], C.c_int),
-            "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
+            "ffs_state_info": ([P, P, P, P, P, P], C.c_int), "ffs_state_path": ([P, P, P, P], C.c_int), "ffs_state_destroy": ([P], None),
             "ffs_evaluate": ([P, C.c_int64, P, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_host": ([P, C.c_int64, P, P, P, P, P, P], C.c_int),
             "ffs_evaluate_strided": ([P, C.c_int64, P, P, C.c_int64, P, P, P, P, P], C.c_int),
@@ -216,6 +216,11 @@ class State:
         _check(lib().ffs_state_info(self.h, *[C.byref(x) for x in v]), "ffs_state_info")
         return dict(K=v[0].value, cells=v[1].value, horizon_cap=v[2].value, horizon_bound=v[3].value,
                     smem_bytes=v[4].value)
+
+    def path(self):
+        v = [C.c_int32() for _ in range(3)]
+        _check(lib().ffs_state_path(self.h, *[C.byref(x) for x in v]), "ffs_state_path")
+        return dict(lane_path=bool(v[0].value), lane_mode=v[1].value, max_pending=v[2].value)
 
 
 def evaluate(state: State, x, y, objective=None, total_tardiness=None, makespan=None, start_out=None,
