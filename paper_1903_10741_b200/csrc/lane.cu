@@ -57,19 +57,21 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {   // 
                "h"((unsigned short)v), "r"((uint32_t)p)
                : "memory");
 }
-// predicated load at a - 65536: the caller's address carries a leader flag
-// (bit 15 of a u16 key, doubled) that the offset removes
-__device__ __forceinline__ uint32_t lds16_if_flag(bool p, uint32_t a) {
-  uint32_t v = 0;   // zero-extended by the load (a 32-bit destination)
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u16 %0, [%1+-65536];\n}\n"
-               : "+r"(v)
-               : "r"(a), "r"((uint32_t)p)
-               : "memory");
-  return v;
-}
 // keep a staged value in a register (no rematerialisation on the critical path)
 __device__ __forceinline__ void pin(uint32_t &v) { asm volatile("" : "+r"(v)); }
 __device__ __forceinline__ void pin(int &v) { asm volatile("" : "+r"(v)); }
+// zero-extended halves by one byte permute each (opaque to the compiler, so a
+// table address becomes one shift-add instead of mask + shift + add)
+__device__ __forceinline__ uint32_t lo16(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x4410;" : "=r"(r) : "r"(w));
+  return r;
+}
+__device__ __forceinline__ uint32_t hi16(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x4432;" : "=r"(r) : "r"(w));
+  return r;
+}
 // lane-interleaved u16 element v: word v/2, half v%2
 [[maybe_unused]] __device__ __forceinline__ uint32_t h16addr(uint32_t base, uint32_t v) {
   return base + ((v >> 1) << 7) + ((v & 1u) << 1);
@@ -607,7 +609,6 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     const int64_t c = tile * 32 + lane;
     const bool active = c < a.count;
     const int64_t gc = a.first + c;
-    const int kq_pref = active ? KQ : 0;     // prefetch bound (0 for inactive lanes)
     // --- initial state: ready/machine times, profile of the RUNNING ops
     for (int w = 0; w < L.RW; ++w) sts(waddr(L, w), r16[w]);
     for (int w = 0; w < L.MW; ++w) sts(waddr(L, L.RW + w), m16[w]);
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
     OpA nA = stage_a(pqt, L, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
-      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      const uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -751,17 +752,17 @@ struct Op2 {
   uint32_t rmul, mmul;    // 1 << rsh, 1 << msh: field updates by IMAD (fma pipe)
   uint32_t m1n, m2, m4;   // run-test multipliers: -(1 << s1), 1 << s2, 1 << s4
   uint32_t top;           // the p ticks of an interval starting a 16-tick window: bits 15..16-p
-  int p;
+  int pm1;                // p - 1
   uint32_t e;             // table index (SCHED: cell = e / O)
 };
 
 // The integer ALU pipe (LOP3/SHF/IADD3/SEL/...) issues every other cycle per
 // SMSP and bounds this kernel; multiplies by powers of two run on the fma
 // pipe, so left shifts by per-op amounts are written as IMADs.
-__device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint32_t mbase, uint32_t pt_base,
+__device__ __forceinline__ Op2 stage2(uint32_t pqt_s, uint32_t lbase, uint32_t mbase, uint32_t pt_base,
                                       uint32_t e) {
   // host-packed: rsh[0:5] | msh[5:10] | ready word[10:21] | machine word[21:29] | p-1[29:32]
-  const uint32_t tv = pqt[e];
+  const uint32_t tv = lds(pqt_s + 4u * e);
   Op2 A;
   A.e = e;
   A.rsh = tv;
@@ -775,7 +776,7 @@ __device__ __forceinline__ Op2 stage2(const uint32_t *pqt, uint32_t lbase, uint3
   A.ra = lbase + ((tv >> 3) & 0x3FF80u);
   A.ma = mbase + ((tv >> 14) & 0x7F80u);
   const uint32_t pm1 = tv >> 29;
-  A.p = (int)pm1 + 1;
+  A.pm1 = (int)pm1;
   uint4 pt;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(pt.x), "=r"(pt.y), "=r"(pt.z), "=r"(pt.w)
@@ -810,17 +811,20 @@ __device__ __noinline__ void reset_fields(uint32_t lbase, int n) {
 __device__ __forceinline__ int search2(const Op2 &A, int t0, uint32_t bb_base, int hcap, uint32_t lbase,
                                        int nfield_words, uint32_t &rw, uint32_t &mw, uint32_t &rf, uint32_t &mf,
                                        int &sgn) {
-  const uint32_t wa = bb_base + ((uint32_t)(t0 >> 5) << 7);
+  uint32_t q = (uint32_t)t0 >> 5;
+  pin(q);   // shift + IMAD, not shift-left + mask + add
+  const uint32_t wa = bb_base + q * 128u;
   uint32_t f = runs2(__funnelshift_l(lds(wa + 128), lds(wa), (uint32_t)t0), A);
   int t = t0;
   if (f == 0u) {
     // window miss: slide by 33 - p ticks (a run starting in the last p - 1
     // ticks of the window was not testable); blocked sentinels end it
     do {
-      t += 33 - A.p;
-      if (t + A.p > hcap) {
+      t += 32 - A.pm1;
+      if (t + A.pm1 >= hcap) {
         reset_fields(lbase, nfield_words);
         rw = mw = rf = mf = 0u;
+
         sgn = -1;
         return 0;
       }
@@ -846,10 +850,15 @@ __device__ __forceinline__ uint32_t dec8(uint32_t W, uint32_t mrep) {   // mrep:
 // 7 - i: group N0 in byte 0, group N1 in byte 2
 __device__ __forceinline__ uint32_t blk2(uint32_t N0, uint32_t N1) {
   const uint32_t z = __byte_perm(N0, N1, 0x5410) | __byte_perm(N0, N1, 0x7632);   // planes 0|2, 1|3
-  return ~(z | (z >> 8));
+  uint32_t r;   // ~(z | z >> 8) in one LOP3
+  asm("lop3.b32 %0, %1, %2, 0, 0x03;" : "=r"(r) : "r"(z), "r"(z >> 8));
+  return r;
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts8m1(uint32_t a, uint32_t v) {   // byte at a - 1
+  asm volatile("st.shared.u8 [%0+-1], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 // min(field, cap) for the three 10-bit fields of a word
@@ -896,7 +905,9 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
   pin(mbase);
   pin(pl_base);
   pin(bb_base);
-  const uint32_t *pqt = (const uint32_t *)(smem + h.off_pqt);
+  const uint32_t bb3 = bb_base + 3u;
+  uint32_t pqt_s = smem_u32(smem + h.off_pqt);
+  pin(pqt_s);
   const uint32_t *r10 = (const uint32_t *)(smem + h.off_ready16);
   const uint32_t *m10 = (const uint32_t *)(smem + h.off_mfree16);
   const uint32_t *pl0 = (const uint32_t *)(smem + h.off_hn0);   // initial planes, 5 words per tick-word
@@ -955,12 +966,11 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     }
     // the chromosome's ranks: lane c % 32 of ordg tile c / 32
     const uint2 *op = (const uint2 *)(a.ordg + (c >> 5) * (int64_t)KQ * 128) + (c & 31);
-    const int kq_pref = active ? KQ : 0;
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
     // prologue: ops 0 and 1 staged, op 0 searched
-    Op2 A = stage2(pqt, lbase, mbase, pt_base, cur.x & 0xFFFFu);
-    Op2 An = stage2(pqt, lbase, mbase, pt_base, K > 1 ? cur.x >> 16 : 0u);
+    Op2 A = stage2(pqt_s, lbase, mbase, pt_base, lo16(cur.x));
+    Op2 An = stage2(pqt_s, lbase, mbase, pt_base, K > 1 ? hi16(cur.x) : 0u);
     uint32_t rw = lds(A.ra), mw = lds(A.ma);
     uint32_t rf = __funnelshift_r(rw, 0u, A.rsh) & 0x3FFu, mf = __funnelshift_r(mw, 0u, A.msh) & 0x3FFu;
     int sgn = 0;
@@ -970,7 +980,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     auto step = [&](const int r, const uint32_t e2, const bool more) {
       // commit-1 of op r: job / machine times, field += (C - field) << shift
       const int Sx = S;
-      const uint32_t C = (uint32_t)(Sx + A.p);
+      const uint32_t C = (uint32_t)Sx + (uint32_t)A.pm1 + 1u;
       sts(A.ra, rw + (C - rf) * A.rmul);
       sts(A.ma, mw + (C - mf) * A.mmul);
       if (more) {
@@ -987,14 +997,20 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
         const uint32_t N0 = dec8(W0, __byte_perm(m16, 0u, 0x1111)), N1 = dec8(W1, __byte_perm(m16, 0u, 0x0000));
         sts(pa, N0);
         sts(pa + 128, N1);
-        const uint32_t ba = bb_base + ((w >> 2) << 7) + (~w & 3u);
+        // group v's blocked byte: word v/4, byte 3 - v%4, i.e. bb_base + 128 q
+        // + 3 - (v - 4q) = 132 q + (bb_base + 3 - v) with q = v/4 (one IMAD);
+        // group w+1 at 132 q' + (bb_base + 3 - w) - 1, q' = (S + 8) / 32
+        uint32_t q = (uint32_t)Sx >> 5, q2 = ((uint32_t)Sx + 8u) >> 5;
+        pin(q);
+        pin(q2);
+        const uint32_t tq = bb3 - w;
         const uint32_t bk = blk2(N0, N1);
-        sts8(ba, bk);
-        sts8((w & 3u) == 3u ? ba + 131u : ba - 1u, bk >> 16);
+        sts8(q * 132u + tq, bk);
+        sts8m1(q2 * 132u + tq, bk >> 16);
       }
       if (SCHED && active) srow[A.e / h.O] = Sx + h.rs;
       // stage A of op r+2 (ranks >= K carry the padding index 0: harmless)
-      const Op2 A2 = stage2(pqt, lbase, mbase, pt_base, e2);
+      const Op2 A2 = stage2(pqt_s, lbase, mbase, pt_base, e2);
       A = An;
       An = A2;
       // search of op r+1
@@ -1007,18 +1023,18 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     // main loop: whole quads whose every op has a successor (no exits inside)
     int qd = 0;
     for (; 4 * qd + 4 < K; ++qd) {
-      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
-      step(4 * qd + 0, cur.y & 0xFFFFu, true);
-      step(4 * qd + 1, cur.y >> 16, true);
-      step(4 * qd + 2, nxt.x & 0xFFFFu, true);
-      step(4 * qd + 3, nxt.x >> 16, true);
+      const uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      step(4 * qd + 0, lo16(cur.y), true);
+      step(4 * qd + 1, hi16(cur.y), true);
+      step(4 * qd + 2, lo16(nxt.x), true);
+      step(4 * qd + 3, hi16(nxt.x), true);
       cur = nxt;
       nxt = pre;
     }
     // tail: the last 1..4 ops
     for (int r = 4 * qd; r < K; ++r) {
       const int k = r & 3;
-      const uint32_t e2 = k == 0 ? cur.y & 0xFFFFu : k == 1 ? cur.y >> 16 : k == 2 ? nxt.x & 0xFFFFu : nxt.x >> 16;
+      const uint32_t e2 = k == 0 ? lo16(cur.y) : k == 1 ? hi16(cur.y) : k == 2 ? lo16(nxt.x) : hi16(nxt.x);
       step(r, e2, r + 1 < K);
     }
     if (!active) continue;
