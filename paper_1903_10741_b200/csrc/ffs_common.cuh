@@ -80,7 +80,7 @@ struct ImageHdr {
   uint32_t off_pjob;             // i32 [n_pjobs] job index
   uint32_t off_pdue;             // i32 [n_pjobs] D_j - RS
   // lane-decode path (one lane per chromosome), see lane.cu
-  uint32_t off_pqt;              // u32 [NJ*G*O]  p | q << 8 | j << 16
+  uint32_t off_pqt;              // lane decoder's op table: mode 2 u32 [K*O] by gene (lane.cu), modes 0/1 u32 [NJ*G*O] p | q << 8 | j << 16
   uint32_t off_ready16;          // u32 [ceil(NJ/2)]  ready0 as u16 pairs
   uint32_t off_mfree16;          // u32 [ceil(G*O/2)] mfree0 as u16 pairs
   int32_t thr_min;               // Q_max - min Q: a slot is "blocked" for every op iff level > thr_min

@@ -117,6 +117,7 @@ struct OrdArgs {
   uint32_t pm_bytes;       // per warp, K u16 rounded to 16 B
   int32_t *zero0, *zero1;  // first chunk: the overflow lists' counts to reset (else null)
   int32_t ubits;           // pass A/D key: u = K - pm in the low ubits, g - g_L above (2^ubits >= K)
+  int32_t O;               // machines per stage (GIDX: table index g * O + machine)
 };
 
 // prefix minima of the lane's four genes given the running min before the tile.
@@ -200,7 +201,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // XS: the warp also stages the chromosome's machines (x row) in shared memory
 // during pass A (TMA under BULK); without it (long rows whose staging would
 // not fit in 227 KB) pass D reads them from global memory one tile ahead.
-template <bool BULK, int SCAN, bool XS>
+template <bool BULK, int SCAN, bool XS, bool GIDX>
 __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int K = a.K, KQ = (K + 3) >> 2, NT = (K + 127) >> 7;
@@ -222,8 +223,8 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   uint32_t *dtab = mtab + 128 * NT;
   uint32_t *btab = dtab + 32 * NT;   // per (tile, lane): byte k = 0xFF iff gene k of the quad starts a segment
   uint8_t *xs = (uint8_t *)(btab + 32 * NT) + (size_t)warp * 128 * NT;   // XS only
-  for (int i = threadIdx.x; i < K; i += blockDim.x)
-    gtab[i] = __ldg(a.gbase + i);
+  if (!GIDX)   // GIDX: the rank's op is g * O + machine (mode 2's gene-indexed table)
+    for (int i = threadIdx.x; i < K; i += blockDim.x) gtab[i] = __ldg(a.gbase + i);
   for (int i = threadIdx.x; i < 128 * NT; i += blockDim.x)
     mtab[i] = (i >= K || ((__ldg(a.head + (i >> 5)) >> (i & 31)) & 1u)) ? 0xFFFFFFFFu : 0u;
   __syncthreads();
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
           const uint32_t pk = pmv[g];
           const uint32_t st = ok ? lds16(hbase + 2u * (pk & umask)) : 0u;
           const uint32_t rank = st + (pk >> a.ubits);
-          const uint32_t e = gtab[g] + xk[k];
+          const uint32_t e = GIDX ? (uint32_t)g * (uint32_t)a.O + xk[k] : gtab[g] + xk[k];
           if (FT)
             ord[rank] = (uint16_t)e;
           else
@@ -1008,7 +1009,10 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
         sts8(q * 132u + tq, bk);
         sts8m1(q2 * 132u + tq, bk >> 16);
       }
-      if (SCHED && active) srow[A.e / h.O] = Sx + h.rs;
+      if (SCHED && active) {   // gene-indexed table: the op's cell from the image's gene info
+        const uint32_t gi = __ldg((const uint32_t *)((const unsigned char *)a.image + h.off_ginfo) + A.e / h.O);
+        srow[(gi & 0xFFFFu) * h.G + (gi >> 16)] = Sx + h.rs;
+      }
       // stage A of op r+2 (ranks >= K carry the padding index 0: harmless)
       const Op2 A2 = stage2(pqt_s, lbase, mbase, pt_base, e2);
       A = An;
@@ -1091,21 +1095,19 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
   // genes can span - 1 (pm_quad)
   const int span = (st.max_pending + 2) / 4 + 1;
   const int scan = span <= 4 ? 2 : span <= 8 ? 3 : 5;
-  // [scan 2/3/5][XS][BULK]
-  static void (*const okerns[3][2][2])(OrdArgs) = {
-      {{order_warp_kernel<false, 2, false>, order_warp_kernel<true, 2, false>},
-       {order_warp_kernel<false, 2, true>, order_warp_kernel<true, 2, true>}},
-      {{order_warp_kernel<false, 3, false>, order_warp_kernel<true, 3, false>},
-       {order_warp_kernel<false, 3, true>, order_warp_kernel<true, 3, true>}},
-      {{order_warp_kernel<false, 5, false>, order_warp_kernel<true, 5, false>},
-       {order_warp_kernel<false, 5, true>, order_warp_kernel<true, 5, true>}}};
-  const int si = scan == 2 ? 0 : scan == 3 ? 1 : 2, xi = st.ord_xs ? 1 : 0;
-  void (*okern)(OrdArgs) = okerns[si][xi][0], (*okern_v)(OrdArgs) = okerns[si][xi][1];
+  // [GIDX][scan 2/3/5][XS][BULK]
+#define OKS(G, S) {{order_warp_kernel<false, S, false, G>, order_warp_kernel<true, S, false, G>}, \
+                   {order_warp_kernel<false, S, true, G>, order_warp_kernel<true, S, true, G>}}
+  static void (*const okerns[2][3][2][2])(OrdArgs) = {{OKS(false, 2), OKS(false, 3), OKS(false, 5)},
+                                                       {OKS(true, 2), OKS(true, 3), OKS(true, 5)}};
+#undef OKS
+  const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
+  const int si = scan == 2 ? 0 : scan == 3 ? 1 : 2, xi = st.ord_xs ? 1 : 0, gi = mode == 2 ? 1 : 0;
+  void (*okern)(OrdArgs) = okerns[gi][si][xi][0], (*okern_v)(OrdArgs) = okerns[gi][si][xi][1];
   const size_t osm = st.ord_smem + (st.ord_xs ? st.ord_xs_bytes : 0);
   ffs_status e = smem_attr(okern, osm);
   if (e == FFS_OK) e = smem_attr(okern_v, osm);
   if (e != FFS_OK) return e;
-  const int mode = ((const ImageHdr *)st.image_host.data())->lane_mode;
   const bool sched = a0.start_out != nullptr;
   void (*kern)(EvalArgs, int32_t) =
       mode == 2 ? (sched ? lane_decode2_kernel<true, false> : lane_decode2_kernel<false, false>)
@@ -1144,6 +1146,7 @@ ffs_status launch_lane(const State &st, const EvalArgs &a0, OvfScratch &scr, cud
     oa.ord_stride = (uint32_t)st.ord_stride;
     oa.pm_bytes = (uint32_t)(((size_t)(K + 127) / 128 * 128 * 2 + 15) & ~(size_t)15);
     oa.ubits = st.ord_ubits;
+    oa.O = st.inst->o;
     oa.zero0 = first == 0 ? scr.list : nullptr;
     oa.zero1 = first == 0 ? scr.list2 : nullptr;
     int64_t og = std::min<int64_t>(ntile, (int64_t)st.num_sms * st.ord_ctas_per_sm);

@@ -218,7 +218,9 @@ ffs_status State::build_image() {
   H.bn_words0 = 0;
   H.off_hn0 = off; off += r16((uint64_t)H.hn_words0 * 4);
   H.off_bn0 = off; off += r16((uint64_t)H.bn_words0 * 4);
-  H.off_pqt = off; off += r16((uint64_t)NJ * G * O * 4);
+  // mode 2: indexed by gene (g * O + machine: the order kernel's ranks need no
+  // per-gene table); modes 0/1: by cell ((j * G + s) * O + machine)
+  H.off_pqt = off; off += r16((uint64_t)(lmode == 2 ? K : NJ * G) * O * 4);
   H.off_ready16 = off; off += r16((uint64_t)((NJ + 1) / 2) * 4);
   H.off_mfree16 = off; off += r16((uint64_t)((G * O + 1) / 2) * 4);
   int64_t lvl_bytes0 = Lr * lvl_bytes;
@@ -274,20 +276,25 @@ ffs_status State::build_image() {
   }
   {
     uint32_t *pqt = (uint32_t *)(img + H.off_pqt);
-    for (int j = 0; j < NJ; ++j)
-      for (int so = 0; so < G * O; ++so) {
-        size_t i = (size_t)j * G * O + so;
-        if (lmode == 2) {
-          // everything the lane decoder needs about the op, precomputed:
-          // shift of the job's 10-bit ready field [0:5] | of the machine's
-          // field [5:10] | ready word j/3 [10:21] | machine word mi/3 [21:29] | p-1 [29:32]
-          const uint32_t pv = (uint32_t)in.P[i];
-          pqt[i] = (uint32_t)((j % 3) * 10) | ((uint32_t)((so % 3) * 10) << 5) | ((uint32_t)(j / 3) << 10) |
-                   ((uint32_t)(so / 3) << 21) | ((pv - 1) << 29);
-        } else {
+    if (lmode == 2) {
+      // everything the lane decoder needs about the op of gene k on machine m,
+      // precomputed: shift of the job's 10-bit ready field [0:5] | of the
+      // machine's field [5:10] | ready word j/3 [10:21] | machine word mi/3
+      // [21:29] | p-1 [29:32]
+      for (int k = 0; k < K; ++k)
+        for (int m = 0; m < O; ++m) {
+          const int j = gene_job[k], so = gene_stage[k] * O + m;
+          const uint32_t pv = (uint32_t)in.P[(size_t)j * G * O + so];
+          pqt[(size_t)k * O + m] = (uint32_t)((j % 3) * 10) | ((uint32_t)((so % 3) * 10) << 5) |
+                                   ((uint32_t)(j / 3) << 10) | ((uint32_t)(so / 3) << 21) | ((pv - 1) << 29);
+        }
+    } else {
+      for (int j = 0; j < NJ; ++j)
+        for (int so = 0; so < G * O; ++so) {
+          const size_t i = (size_t)j * G * O + so;
           pqt[i] = ((uint32_t)in.P[i] & 0xFFu) | (((uint32_t)in.Q[i] & 0xFFu) << 8) | ((uint32_t)j << 16);
         }
-      }
+    }
     if (lmode == 2) {   // three 10-bit times per word (times >= 1023 overflow to the fallback anyway)
       uint32_t *r10 = (uint32_t *)(img + H.off_ready16);
       for (int j = 0; j < NJ; ++j) r10[j / 3] |= (uint32_t)std::min<int32_t>(ready0[j], 1023) << ((j % 3) * 10);
