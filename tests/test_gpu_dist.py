@@ -139,3 +139,30 @@ def test_nccl_hooks_world_one(tmp_path):
     s.close()
     mp.spawn(_nccl_worker, args=(1, port, str(tmp_path)), nprocs=1, join=True)
     assert open(os.path.join(tmp_path, "nccl_ok")).read() == "True nccl"
+
+
+def test_bench_two_ranks_under_torchrun():
+    """bench.py's multi-GPU launch (torchrun, one process per rank, barrier +
+    max-over-ranks timing, global best of the ring) with two ranks sharing
+    cuda:0 over gloo (this box has one GPU; NCCL refuses two ranks on one
+    device): rank 0 prints one JSON line for the whole 2 x 256-island job."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, FFS_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["config"]["islands_total"] == 512 and d["config"]["population_total"] == 2 * 65536
+    assert d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["value"] == pytest.approx(2 * 65536 * 3 / (d["ms_per_step"] * 3e-3), rel=1e-6)
