@@ -825,7 +825,6 @@ __device__ __forceinline__ int search2(const Op2 &A, int t0, uint32_t bb_base, i
       if (t + A.pm1 >= hcap) {
         reset_fields(lbase, nfield_words);
         rw = mw = rf = mf = 0u;
-
         sgn = -1;
         return 0;
       }
