@@ -257,18 +257,22 @@ def test_long_jobs(g, n, o, q_max, path):
     compare(octx, st, x, y, n_sched=20)
 
 
-@pytest.mark.parametrize("n,lane", [(3, True), (9, False)])
-def test_order_key_bound(n, lane):
+@pytest.mark.parametrize("g,n,lane", [(70, 3, True), (70, 9, False), (128, 1, True)])
+def test_order_key_bound(g, n, lane):
     """The order kernel keeps u = K - pm and g - g_L (< max_pending) in one u16
     per gene, u in the low ceil(log2 K) bits: the lane path is taken only when
     max_pending <= 2^(16 - ceil(log2 K)).  Jobs of 70 stages: at K <= 256 the
     offsets fit (the lane path, one job spanning tile boundaries), at K ~ 600
-    they do not (the general kernel); both equal the oracle."""
-    wl = wlmod.gen_v1(f"G70n{n}", n, 70, 2, 3, arrivals_per_event=[2], ratios=[0.3], seed=70 + n)
+    they do not (the general kernel); jobs of 128 stages at 256 < K <= 512:
+    max_pending = 128 = 2^7 exactly, every offset bit in use (lane path); all
+    equal the oracle."""
+    wl = wlmod.gen_v1(f"G{g}n{n}", n, g, 2, 3, arrivals_per_event=[2], ratios=[0.3], seed=g + n)
     octx, st, arr = both_event_ctx(wl)
     p = st.path()
     ub = max(1, (st.K - 1).bit_length())
     assert p["max_pending"] > 32 and p["lane_mode"] == 2
+    if g == 128:
+        assert p["max_pending"] == 128 and 256 < st.K <= 512
     assert p["lane_path"] == lane == (p["max_pending"] <= 2 ** (16 - ub))
     check_gene_order(octx, st)
     x, y = wlmod.random_chromosomes(200, st.K, wl.o, seed=23)
