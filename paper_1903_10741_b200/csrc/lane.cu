@@ -100,7 +100,8 @@ __device__ __forceinline__ uint32_t flag_nibble(uint32_t v) {
 //           the gene holding it (the run's leader, a new prefix minimum);
 //           the run's last gene stores hist[u] = g - g_L + 1, u = K - pm
 //   pass C  start[u] = #genes with u' < u (exclusive prefix sum)
-//   pass D  rank(g) = start[u(g)] + (g - g_L(g))
+//   pass D  rank(g) = start[u(g)] + (g - g_L(g)); ord[rank] = the op's table
+//           index (mode 2: g * O + machine; modes 0/1: cell base + machine)
 // ---------------------------------------------------------------------------
 struct OrdArgs {
   const int8_t *x;
@@ -110,7 +111,7 @@ struct OrdArgs {
   int32_t vec;             // row % 16 == 0 and 16-B aligned bases: TMA bulk row staging
   int32_t K;
   const uint32_t *head;    // [ceil(K/32)] bit g: first pending gene of its job
-  const uint32_t *gbase;   // [K] (j*G + s)*O
+  const uint32_t *gbase;   // [K] (j*G + s)*O (cell-indexed tables, modes 0/1; unused when GIDX)
   uint16_t *ordg;
   uint32_t hist_bytes;     // per warp
   uint32_t ord_stride;     // bytes between staged ord arrays (8 * odd)
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(1024, 1) order_warp_kernel(OrdArgs a) {
   uint32_t *hist = (uint32_t *)(smem + (size_t)warp * a.hist_bytes);          // u16 pairs
   uint16_t *h16 = (uint16_t *)hist;
   uint16_t *pmv = (uint16_t *)(smem + (size_t)32 * a.hist_bytes + (size_t)32 * a.ord_stride +
-                               (size_t)warp * a.pm_bytes);                      // [K] pm-1 | leader<<15
+                               (size_t)warp * a.pm_bytes);                      // [K] y, then (g - g_L) << ub | (2^ub - pm)
   unsigned char *ordb = smem + (size_t)32 * a.hist_bytes;
   uint16_t *ord = (uint16_t *)(ordb + (size_t)warp * a.ord_stride);
   const uint32_t h16s = smem_u32(h16), ords = smem_u32(ord);   // shared-window addresses
