@@ -344,6 +344,8 @@ def run_ours(args):
             # NCCL's own log names the communicator (ranks, transport: NVLink / NVLS)
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # NCCL logs to stdout by default; stdout carries rank 0's one JSON line
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
