@@ -629,6 +629,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     }
     bool live = active;            // false when inactive or overflowed
     bool ovf = false;
+    int kq_pref = active ? KQ : 0;   // prefetch bound (0 for inactive lanes): one 32-bit compare per quad
+    pin(kq_pref);                    // (not re-derived from the 64-bit c < count)
     const uint2 *op = (const uint2 *)(a.ordg + tile * (int64_t)KQ * 128) + lane;
     // software pipeline: the next op's table lookup and every p-dependent
     // constant (stage A) is computed while the current op runs (B..E)
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode_kernel(EvalArgs a, int32_t
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
     OpA nA = stage_a(pqt, L, GO, cur.x & 0xFFFFu);
     for (int qd = 0; qd < KQ; ++qd) {
-      const uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       const int nk = min(4, K - 4 * qd);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -966,6 +968,8 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
       for (int k = 0; k < h.cells; ++k) srow[k] = a.fstart[k];
     }
     // the chromosome's ranks: lane c % 32 of ordg tile c / 32
+    int kq_pref = active ? KQ : 0;   // prefetch bound (0 for inactive lanes): one 32-bit compare per quad
+    pin(kq_pref);                    // (not re-derived from the 64-bit c < count)
     const uint2 *op = (const uint2 *)(a.ordg + (c >> 5) * (int64_t)KQ * 128) + (c & 31);
     uint2 cur = active ? op[0] : make_uint2(0, 0);
     uint2 nxt = (active && KQ > 1) ? op[32] : make_uint2(0, 0);
@@ -1027,7 +1031,7 @@ __global__ void __launch_bounds__(512, 1) lane_decode2_kernel(EvalArgs a, int32_
     // main loop: whole quads whose every op has a successor (no exits inside)
     int qd = 0;
     for (; 4 * qd + 4 < K; ++qd) {
-      const uint2 pre = (active && qd + 2 < KQ) ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
+      const uint2 pre = qd + 2 < kq_pref ? op[(size_t)(qd + 2) * 32] : make_uint2(0, 0);
       step(4 * qd + 0, lo16(cur.y), true);
       step(4 * qd + 1, hi16(cur.y), true);
       step(4 * qd + 2, lo16(nxt.x), true);
