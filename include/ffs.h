@@ -290,6 +290,26 @@ FFS_API ffs_status ffs_run_population(ffs_run *run, int8_t *x, int16_t *y, int64
 FFS_API ffs_status ffs_run_history(ffs_run *run, int8_t *x, int16_t *y, int64_t *objective, int64_t *fitness);
 FFS_API ffs_status ffs_run_info(const ffs_run *run, int32_t *generation, int64_t *emax, int64_t *evaluations,
                         int32_t *kernel_launches);
+/* Checkpoint / resume.  A checkpoint of a run after generation k is what the
+ * calls above return: ffs_run_population (x, y, objective, fitness words),
+ * ffs_run_history (the per-island elites), ffs_run_info (k, E_max word) and
+ * ffs_best's trace_min / trace_sum [k+1].  ffs_run_restore loads such a
+ * checkpoint into a run created by ffs_evolve_begin with the SAME
+ * ffs_ga_config (shape, shard, seed, thresholds, interval, generations >= k;
+ * the state must be the same rescheduling point), after which
+ * ffs_evolve_step continues at generation k+1 exactly as the uninterrupted
+ * run does: every random draw is keyed by (seed, island, generation,
+ * individual, gene) and the rest of the run's state is a function of the
+ * restored arrays.  Host buffers (copied synchronously), all required when
+ * K > 0: x, y [cells_local*K], objective, fitness [cells_local], hx, hy
+ * [islands_local*K], hobj, hfit [islands_local], trace_min, trace_sum [k+1];
+ * emax = the E_max word.  0 <= generation <= cfg.generations, else
+ * FFS_ERR_INVALID_ARG.  The chromosomes are not re-validated (a checkpoint
+ * carries the run's own permutations). */
+FFS_API ffs_status ffs_run_restore(ffs_run *run, int32_t generation, const int8_t *x, const int16_t *y,
+                           const int64_t *objective, const int64_t *fitness, const int8_t *hx,
+                           const int16_t *hy, const int64_t *hobj, const int64_t *hfit, int64_t emax,
+                           const int64_t *trace_min, const int64_t *trace_sum);
 FFS_API void ffs_run_destroy(ffs_run *run);
 
 #ifdef __cplusplus

@@ -1150,6 +1150,43 @@ ffs_status ffs_run_info(const ffs_run *h, int32_t *generation, int64_t *emax, in
   return FFS_OK;
 }
 
+ffs_status ffs_run_restore(ffs_run *h, int32_t generation, const int8_t *x, const int16_t *y,
+                           const int64_t *objective, const int64_t *fitness, const int8_t *hx, const int16_t *hy,
+                           const int64_t *hobj, const int64_t *hfit, int64_t emax, const int64_t *trace_min,
+                           const int64_t *trace_sum) {
+  if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
+  Run &r = h->v;
+  if (generation < 0 || generation > r.cfg.generations)
+    return fail(FFS_ERR_INVALID_ARG, "checkpoint generation outside [0, generations]");
+  if (r.K == 0) {   // nothing evolves: only the generation counter
+    r.gen = generation;
+    return FFS_OK;
+  }
+  if (!x || !y || !objective || !fitness || !hx || !hy || !hobj || !hfit || !trace_min || !trace_sum)
+    return fail(FFS_ERR_INVALID_ARG, "null checkpoint array");
+  cudaSetDevice(r.st->inst->dev);
+  FFS_CUDA(cudaStreamSynchronize(r.s));
+  const size_t K = (size_t)r.K;
+  // rows padded to r.row genes: only the K genes are restored (the padding
+  // stays the zeros written at creation)
+  FFS_CUDA(cudaMemcpy2DAsync(r.x[r.cur], (size_t)r.row, x, K, K, (size_t)r.nloc, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpy2DAsync(r.y[r.cur], (size_t)r.row * 2, y, K * 2, K * 2, (size_t)r.nloc, cudaMemcpyHostToDevice,
+                             r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.obj[r.cur], objective, (size_t)r.nloc * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.fit[r.cur], fitness, (size_t)r.nloc * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpy2DAsync(r.hx, (size_t)r.row, hx, K, K, (size_t)r.nisl, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpy2DAsync(r.hy, (size_t)r.row * 2, hy, K * 2, K * 2, (size_t)r.nisl, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.hobj, hobj, (size_t)r.nisl * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.hfit, hfit, (size_t)r.nisl * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.scal, &emax, 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.tmin, trace_min, (size_t)(generation + 1) * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaMemcpyAsync(r.tsum, trace_sum, (size_t)(generation + 1) * 8, cudaMemcpyHostToDevice, r.s));
+  FFS_CUDA(cudaStreamSynchronize(r.s));   // the host arrays may go away after the call
+  r.gen = generation;
+  r.evaluations = (int64_t)(generation + 1) * r.nloc;
+  return FFS_OK;
+}
+
 void ffs_run_destroy(ffs_run *h) {
   if (!h) return;
   cudaSetDevice(h->v.st->inst->dev);

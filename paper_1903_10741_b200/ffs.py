@@ -27,7 +27,7 @@ EXPORTS = [
     "ffs_reschedule_state", "ffs_static_state", "ffs_state_genes", "ffs_state_cells", "ffs_state_cut_table",
     "ffs_state_set_horizon_cap", "ffs_state_set_objective_weight", "ffs_state_info", "ffs_state_path", "ffs_state_destroy", "ffs_evaluate",
     "ffs_evaluate_host", "ffs_evaluate_strided", "ffs_brute_force", "ffs_random_population", "ffs_random_population_strided", "ffs_evolve_begin", "ffs_evolve_step",
-    "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info",
+    "ffs_evolve", "ffs_best", "ffs_run_population", "ffs_run_history", "ffs_run_info", "ffs_run_restore",
     "ffs_run_destroy",
 ]
 
@@ -94,6 +94,7 @@ def lib():
             "ffs_run_population": ([P, P, P, P, P], C.c_int),
             "ffs_run_history": ([P, P, P, P, P], C.c_int),
             "ffs_run_info": ([P, P, P, P, P], C.c_int), "ffs_run_destroy": ([P], None),
+            "ffs_run_restore": ([P, C.c_int32, P, P, P, P, P, P, P, P, C.c_int64, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -418,6 +419,58 @@ class Run:
         fit = np.zeros(self.nisl, np.int64)
         _check(lib().ffs_run_history(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)), "ffs_run_history")
         return x, y, _words(self.state, obj), _words(self.state, fit)
+
+    def checkpoint(self) -> dict:
+        """Everything ffs_run_restore needs to continue this run bit-identically
+        (numpy arrays; objective/fitness/trace as raw 64-bit words)."""
+        K = self.state.K
+        x = np.zeros((self.nloc, K), np.int8)
+        y = np.zeros((self.nloc, K), np.int16)
+        obj = np.zeros(self.nloc, np.int64)
+        fit = np.zeros(self.nloc, np.int64)
+        _check(lib().ffs_run_population(self.h, _np_ptr(x), _np_ptr(y), _np_ptr(obj), _np_ptr(fit)),
+               "ffs_run_population")
+        hx = np.zeros((self.nisl, K), np.int8)
+        hy = np.zeros((self.nisl, K), np.int16)
+        hobj = np.zeros(self.nisl, np.int64)
+        hfit = np.zeros(self.nisl, np.int64)
+        _check(lib().ffs_run_history(self.h, _np_ptr(hx), _np_ptr(hy), _np_ptr(hobj), _np_ptr(hfit)),
+               "ffs_run_history")
+        g, e = C.c_int32(), C.c_int64()
+        _check(lib().ffs_run_info(self.h, C.byref(g), C.byref(e), None, None), "ffs_run_info")
+        b = self.best()
+        words = lambda a: np.ascontiguousarray(np.asarray(a)).view(np.int64)
+        c = self.cfg
+        config = np.array([K, c.island_w, c.island_h, c.islands_total, c.island_begin, c.island_end,
+                           c.migration_interval, c.seed & 0x7FFFFFFFFFFFFFFF, c.xo_threshold, c.mut_threshold], np.int64)
+        return dict(generation=g.value, emax=e.value, x=x, y=y, objective=obj, fitness=fit, hx=hx, hy=hy,
+                    hobj=hobj, hfit=hfit, trace_min=words(b["trace_min"]), trace_sum=words(b["trace_sum"]),
+                    config=config)
+
+    def restore(self, ck: dict):
+        """Load a checkpoint() of a run with the same configuration (ffs_run_restore);
+        step() then continues at generation ck['generation'] + 1."""
+        g = int(ck["generation"])
+        K = self.state.K
+        c = self.cfg
+        mine = np.array([K, c.island_w, c.island_h, c.islands_total, c.island_begin, c.island_end,
+                         c.migration_interval, c.seed & 0x7FFFFFFFFFFFFFFF, c.xo_threshold, c.mut_threshold], np.int64)
+        if "config" in ck and not np.array_equal(np.asarray(ck["config"]), mine):
+            raise ValueError("checkpoint of a run with another configuration (K, shape, shard, interval, seed, rates)")
+        want = {"x": ((self.nloc, K), np.int8), "y": ((self.nloc, K), np.int16), "objective": ((self.nloc,), np.int64),
+                "fitness": ((self.nloc,), np.int64), "hx": ((self.nisl, K), np.int8), "hy": ((self.nisl, K), np.int16),
+                "hobj": ((self.nisl,), np.int64), "hfit": ((self.nisl,), np.int64),
+                "trace_min": ((max(g + 1, 1),), np.int64), "trace_sum": ((max(g + 1, 1),), np.int64)}
+        arr = {}
+        for k, (shape, dt) in want.items():
+            a = np.ascontiguousarray(ck[k])
+            if a.dtype.itemsize != np.dtype(dt).itemsize or a.size != int(np.prod(shape)):
+                raise ValueError(f"checkpoint array {k}: {a.dtype}{a.shape}, expected {np.dtype(dt)}{shape}")
+            arr[k] = a.view(dt).reshape(shape)
+        _check(lib().ffs_run_restore(self.h, g, *[_np_ptr(arr[k]) for k in ("x", "y", "objective", "fitness", "hx",
+                                                                             "hy", "hobj", "hfit")],
+                                     int(ck["emax"]), _np_ptr(arr["trace_min"]), _np_ptr(arr["trace_sum"])),
+               "ffs_run_restore")
 
     def best(self):
         K, cells = self.state.K, self.state.cells

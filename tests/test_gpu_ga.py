@@ -167,3 +167,64 @@ def test_trajectory_parity_through_overflows(relist, monkeypatch):
     tmin, tsum = ga.trace()
     b = run.best()
     assert (b["trace_min"] == tmin).all() and (b["trace_sum"] == tsum).all()
+
+
+@pytest.mark.parametrize("k,wt", [(0, None), (7, None), (10, None), (12, None), (9, 0.37)])
+def test_checkpoint_resume_is_bit_identical(k, wt, tmp_path):
+    """Run.checkpoint() after generation k -> an .npz file -> a fresh run of the
+    same configuration restores it (ffs_run_restore) and finishes: population,
+    objective / fitness words, history elites, E_max, the best schedule and the
+    whole trace equal the uninterrupted run's (k = 7 and 9 resume before the
+    generation-10 migration, k = 10 right after it, k = 0 from the initial
+    population; wt: fractional WT, binary64 words)."""
+    wl = wlmod.config_A2()
+    _, st, _ = both_event_ctx(wl)
+    if wt is not None:
+        st.set_objective_weight(wt)
+    G, shape = 23, (4, 4, 4)
+    full = ffs.Run(st, *shape, G, 10741)
+    full.step(G)
+    a = ffs.Run(st, *shape, G, 10741)
+    a.step(k)
+    ck = a.checkpoint()
+    del a
+    np.savez(tmp_path / "ck.npz", **ck)
+    ck2 = dict(np.load(tmp_path / "ck.npz"))
+    b = ffs.Run(st, *shape, G, 10741)
+    b.restore(ck2)
+    assert b.info()["generation"] == k
+    b.step(G - k)
+    for u, v in zip(full.population(), b.population()):   # 64-bit words compared as bit patterns
+        u, v = np.asarray(u), np.asarray(v)
+        if u.dtype.itemsize == 8:
+            u, v = u.view(np.int64), v.view(np.int64)
+        assert (u == v).all()
+    for u, v in zip(full.history(), b.history()):
+        u, v = np.asarray(u), np.asarray(v)
+        if u.dtype.itemsize == 8:
+            u, v = u.view(np.int64), v.view(np.int64)
+        assert (u == v).all()
+    fi, bi = full.info(), b.info()
+    assert fi["generation"] == bi["generation"] == G and fi["emax"] == bi["emax"]
+    fb, bb = full.best(), b.best()
+    assert (fb["x"] == bb["x"]).all() and (fb["y"] == bb["y"]).all() and (fb["start"] == bb["start"]).all()
+    assert (np.asarray(fb["trace_min"]).view(np.int64) == np.asarray(bb["trace_min"]).view(np.int64)).all()
+    assert (np.asarray(fb["trace_sum"]).view(np.int64) == np.asarray(bb["trace_sum"]).view(np.int64)).all()
+
+
+def test_restore_rejects_bad_generation():
+    wl = wlmod.config_A2()
+    _, st, _ = both_event_ctx(wl)
+    r = ffs.Run(st, 4, 4, 2, 5, 1)
+    ck = r.checkpoint()
+    ck["generation"] = 6   # beyond the configured 5 generations
+    ck["trace_min"] = ck["trace_sum"] = np.zeros(7, np.int64)
+    with pytest.raises(ffs.FFSError):
+        r.restore(ck)
+    other = ffs.Run(st, 4, 4, 2, 5, 2)   # another seed: refused before any copy
+    with pytest.raises(ValueError):
+        r.restore(other.checkpoint())
+    ck = r.checkpoint()
+    ck["x"] = ck["x"][:-1]               # wrong size: refused before any copy
+    with pytest.raises(ValueError):
+        r.restore(ck)
