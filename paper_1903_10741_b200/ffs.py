@@ -354,6 +354,25 @@ def evolve(state: State, island_w: int, island_h: int, islands_total: int, gener
     return Run(state, island_w, island_h, islands_total, generations, seed, one_shot=True, **kw)
 
 
+def trace_rows(best: dict, population: int):
+    """RunTrace rows: (generation, best objective, mean objective)
+    for k = 0..G from a Run.best() / dist.global_best() record: best = the
+    minimum objective of generation k's population (after replacement and
+    migration), mean = the sum of its objectives / population (the integer
+    sum is exact; one division; binary64 sums in fractional-WT mode)."""
+    tmin = np.asarray(best["trace_min"])
+    tsum = np.asarray(best["trace_sum"])
+    return [(k, tmin[k].item(), float(tsum[k]) / float(population)) for k in range(len(tmin))]
+
+
+def write_trace_csv(path, best: dict, population: int):
+    """The trace as CSV `generation,best_objective,mean_objective`."""
+    with open(path, "w") as f:
+        f.write("generation,best_objective,mean_objective\n")
+        for k, b, m in trace_rows(best, population):
+            f.write(f"{k},{b},{m!r}\n")
+
+
 class Run:
     """Island GA of one rescheduling point (ffs_evolve_begin / _step / ffs_best).
 

@@ -62,3 +62,16 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dp, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|ffs_oracle|or_ctx|or_decode)", s), f
+
+
+def test_trace_csv_format(tmp_path):
+    """RunTrace rows and CSV from a best record: best =
+    trace_min, mean = trace_sum / population, one row per generation."""
+    import numpy as np
+    best = {"trace_min": np.array([30, 29, 29], np.int64), "trace_sum": np.array([100, 95, 90], np.int64)}
+    rows = ffs.trace_rows(best, 4)
+    assert rows == [(0, 30, 25.0), (1, 29, 23.75), (2, 29, 22.5)]
+    p = tmp_path / "trace.csv"
+    ffs.write_trace_csv(p, best, 4)
+    assert p.read_text().splitlines() == ["generation,best_objective,mean_objective", "0,30,25.0", "1,29,23.75",
+                                          "2,29,22.5"]
