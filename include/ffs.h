@@ -304,8 +304,9 @@ FFS_API ffs_status ffs_run_info(const ffs_run *run, int32_t *generation, int64_t
  * K > 0: x, y [cells_local*K], objective, fitness [cells_local], hx, hy
  * [islands_local*K], hobj, hfit [islands_local], trace_min, trace_sum [k+1];
  * emax = the E_max word.  0 <= generation <= cfg.generations, else
- * FFS_ERR_INVALID_ARG.  The chromosomes are not re-validated (a checkpoint
- * carries the run's own permutations). */
+ * FFS_ERR_INVALID_ARG.  K = 0 (nothing evolves): only generation == the run's
+ * own counter is accepted; the arrays are not read.  The chromosomes are not
+ * re-validated (a checkpoint carries the run's own permutations). */
 FFS_API ffs_status ffs_run_restore(ffs_run *run, int32_t generation, const int8_t *x, const int16_t *y,
                            const int64_t *objective, const int64_t *fitness, const int8_t *hx,
                            const int16_t *hy, const int64_t *hobj, const int64_t *hfit, int64_t emax,

@@ -1156,12 +1156,12 @@ ffs_status ffs_run_restore(ffs_run *h, int32_t generation, const int8_t *x, cons
                            const int64_t *trace_sum) {
   if (!h) return fail(FFS_ERR_INVALID_ARG, "null run");
   Run &r = h->v;
-  if (generation < 0 || generation > r.cfg.generations)
-    return fail(FFS_ERR_INVALID_ARG, "checkpoint generation outside [0, generations]");
-  if (r.K == 0) {   // nothing evolves: only the generation counter
-    r.gen = generation;
+  if (r.K == 0) {   // nothing evolves: the run has no generations to restore
+    if (generation != r.gen) return fail(FFS_ERR_INVALID_ARG, "K = 0: the checkpoint generation must be the run's");
     return FFS_OK;
   }
+  if (generation < 0 || generation > r.cfg.generations)
+    return fail(FFS_ERR_INVALID_ARG, "checkpoint generation outside [0, generations]");
   if (!x || !y || !objective || !fitness || !hx || !hy || !hobj || !hfit || !trace_min || !trace_sum)
     return fail(FFS_ERR_INVALID_ARG, "null checkpoint array");
   cudaSetDevice(r.st->inst->dev);

@@ -476,6 +476,10 @@ class Run:
                          c.migration_interval, c.seed & 0x7FFFFFFFFFFFFFFF, c.xo_threshold, c.mut_threshold], np.int64)
         if "config" in ck and not np.array_equal(np.asarray(ck["config"]), mine):
             raise ValueError("checkpoint of a run with another configuration (K, shape, shard, interval, seed, rates)")
+        if K == 0:   # nothing evolves: only the generation counter must agree
+            _check(lib().ffs_run_restore(self.h, g, None, None, None, None, None, None, None, None, 0, None, None),
+                   "ffs_run_restore")
+            return
         want = {"x": ((self.nloc, K), np.int8), "y": ((self.nloc, K), np.int16), "objective": ((self.nloc,), np.int64),
                 "fitness": ((self.nloc,), np.int64), "hx": ((self.nisl, K), np.int8), "hy": ((self.nisl, K), np.int16),
                 "hobj": ((self.nisl,), np.int64), "hfit": ((self.nisl,), np.int64),

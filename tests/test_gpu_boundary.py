@@ -141,3 +141,19 @@ def test_sharded_run_needs_both_hooks(which):
                                     C.byref(h))
     assert rc == 1 and not h.value
     assert b"hooks" in ffs.lib().ffs_last_error()
+
+
+def test_checkpoint_restore_K0():
+    """A K = 0 run (nothing pending) checkpoints and restores its
+    (empty) state; another generation is refused; its best stays the frozen
+    plan."""
+    octx, st, plan = _k0_state()
+    run = ffs.Run(st, 2, 1, 1, 5, 7)
+    run.step(5)
+    ck = run.checkpoint()
+    other = ffs.Run(st, 2, 1, 1, 5, 7)
+    other.restore(ck)
+    bad = dict(ck, generation=3)
+    with pytest.raises(ffs.FFSError):
+        other.restore(bad)
+    assert (other.best()["start"] == plan["start"]).all()
