@@ -220,6 +220,30 @@ def test_full_size_sampled_parity(path):
     assert bool((ysort == torch.arange(1, st.K + 1, device=y.device, dtype=torch.int32)).all())
 
 
+def test_config_e_million_sampled_parity():
+    """Config E's sweep at 1e6 Philox chromosomes on the 100-job instance
+    (padded rows, 8 chunks of 2^17 in one call, as bench.py's sweep): every
+    chunk's first and last chromosome plus random ones against the oracle,
+    one by one; every objective of the population is positive."""
+    wl = wlmod.config_C()
+    octx, st, arr = both_event_ctx(wl)
+    KP = (st.K + 15) // 16 * 16
+    n = 1_000_000
+    x, y = ffs.random_population(st, n, seed=2024, row=KP)
+    obj, T, M, _ = ffs.evaluate(st, x, y)
+    torch.cuda.synchronize()
+    chunk = 1 << 17
+    edges = sorted({i for c in range(0, n, chunk) for i in (c, min(c + chunk, n) - 1)})
+    idx = np.array(edges + list(np.random.default_rng(5).choice(n, 32, replace=False)))
+    it = torch.as_tensor(idx, device=x.device)
+    xs = x.index_select(0, it)[:, :st.K].cpu().numpy()
+    ys = y.index_select(0, it)[:, :st.K].cpu().numpy()
+    oo, oT, oM, _ = octx.evaluate_batch(np.ascontiguousarray(xs), np.ascontiguousarray(ys), nthreads=8)
+    assert (obj.index_select(0, it).cpu().numpy() == oo).all()
+    assert (T.index_select(0, it).cpu().numpy() == oT).all() and (M.index_select(0, it).cpu().numpy() == oM).all()
+    assert bool((obj > 0).all())
+
+
 def test_multi_chunk_equals_per_chunk():
     """Above 2^17 chromosomes the lane path runs in chunks (order + decode
     per chunk, the overflow counts reset by the first chunk's order kernel,
