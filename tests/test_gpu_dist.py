@@ -72,22 +72,24 @@ def _worker(rank, world, port, out_dir, cfg="A"):
 C_SHAPE = (16, 16, 6, 9, 4)   # config C tiles, 6 islands over 2 ranks, 9 generations, migration every 4
 
 
-@pytest.mark.parametrize("cfg", ["A", "C"])
-def test_two_rank_ga_equals_single_process(tmp_path, cfg):
+@pytest.mark.parametrize("cfg,world", [("A", 2), ("C", 2), ("A", 3), ("A", 4)])
+def test_two_rank_ga_equals_single_process(tmp_path, cfg, world):
     """cfg C: config C's instance (K = 855: 2,581-byte migration records) in
-    16x16 tiles, the ring crossing the shard boundary in both migrations."""
+    16x16 tiles, the ring crossing the shard boundary in both migrations.
+    world 3 / 4: uneven and one-island shards (6 islands), the ring's
+    wrap-around import (rank 0 <- the last rank) through the allgather."""
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.spawn(_worker, args=(2, port, str(tmp_path), cfg), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, port, str(tmp_path), cfg), nprocs=world, join=True)
     from paper_1903_10741_b200 import ffs
     st, (w, h, isl, g, mi) = (_state(), (ISL_W, ISL_H, ISLANDS, G, 10)) if cfg == "A" else (_state_c(), C_SHAPE)
     run = ffs.Run(st, w, h, isl, g, SEED, migration_interval=mi)
     run.step(g)
     x, y, obj, fit = run.population()
     hx, hy, hobj, _ = run.history()
-    parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(2)]
+    parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
     assert all(int(p["emax"]) == run.info()["emax"] for p in parts)
     for key, ref in (("x", x), ("y", y), ("obj", obj), ("fit", fit), ("hx", hx), ("hy", hy), ("hobj", hobj)):
         got = np.concatenate([p[key] for p in parts])
